@@ -1,0 +1,381 @@
+"""ctypes bindings for the CPU ORACLE (test infrastructure only).
+
+Two libraries with the same shape of API:
+
+* ``oracle/liboracle.so``       — the plain-C restatement (``oracle/axb_oracle.c``);
+* ``oracle/_ref/libaxbref.so``  — the UNMODIFIED reference engine compiled from
+  ``/root/reference/proj/include`` (``oracle/ref_driver.cpp``); present only
+  where it was built (this container, and GPU boxes that received the prebuilt .so).
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline legs import
+this module.  The product (``paper_2408_05444_b200``) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+ORACLE_SO = os.path.join(ORACLE_DIR, "liboracle.so")
+REF_SO = os.path.join(ORACLE_DIR, "_ref", "libaxbref.so")
+
+BK, RBK, GRBK, RGRBK, MWRBK = range(5)
+SAFE, PAPER, FIXED = range(3)
+SOLUTION_RRN, RESIDUAL_REL = range(2)
+
+_dp = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+
+
+class Config(C.Structure):
+    """SolveConfig (solver.hpp:100-109) — same layout as axb_config / orc_config."""
+
+    _fields_ = [
+        ("method", C.c_int32),
+        ("has_theta", C.c_int32),
+        ("theta", C.c_double),
+        ("alpha_rule", C.c_int32),
+        ("stop_kind", C.c_int32),
+        ("alpha_value", C.c_double),
+        ("tol", C.c_double),
+        ("reference", _dp),
+        ("max_iter", C.c_uint64),
+        ("seed", C.c_uint64),
+        ("record_trace", C.c_int32),
+        ("_pad", C.c_int32),
+        ("refresh_interval", C.c_uint64),
+    ]
+
+
+class Report(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_uint64),
+        ("wall_seconds", C.c_double),
+        ("final_rrn", C.c_double),
+        ("final_residual_rel", C.c_double),
+        ("terminated_by", C.c_int32),
+        ("alpha_outside_bound", C.c_int32),
+        ("alpha", C.c_double),
+        ("seed", C.c_uint64),
+        ("skipped_zero_rows", C.c_uint64),
+        ("trace_len", C.c_uint64),
+        ("diverged_iteration", C.c_uint64),
+        ("diverged_residual", C.c_double),
+    ]
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def make_config(method=GRBK, theta=None, alpha_rule=SAFE, alpha_value=0.0, stop_kind=RESIDUAL_REL,
+                tol=1e-6, reference=None, max_iter=200000, seed=0, record_trace=False,
+                refresh_interval=1000):
+    cfg = Config()
+    cfg.method = method
+    cfg.has_theta = 0 if theta is None else 1
+    cfg.theta = 0.0 if theta is None else float(theta)
+    cfg.alpha_rule = alpha_rule
+    cfg.alpha_value = alpha_value
+    cfg.stop_kind = stop_kind
+    cfg.tol = tol
+    keep = None
+    if reference is not None:
+        keep = np.ascontiguousarray(reference, dtype=np.float64)
+        cfg.reference = keep.ctypes.data_as(_dp)
+    cfg.max_iter = max_iter
+    cfg.seed = seed
+    cfg.record_trace = 1 if record_trace else 0
+    cfg.refresh_interval = refresh_interval
+    cfg._keep = keep  # keep the reference buffer alive as long as the config
+    return cfg
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def ensure_built():
+    """Compile liboracle.so (and _ref where /root/reference exists)."""
+    if not os.path.exists(ORACLE_SO) or (
+        os.path.getmtime(ORACLE_SO) < os.path.getmtime(os.path.join(ORACLE_DIR, "axb_oracle.c"))
+    ):
+        subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+
+
+class _Lib:
+    prefix = ""
+
+    def __init__(self, path):
+        self.lib = C.CDLL(path)
+        self._declare()
+
+    def _f(self, name, restype, argtypes):
+        fn = getattr(self.lib, self.prefix + name)
+        fn.restype = restype
+        fn.argtypes = argtypes
+        return fn
+
+
+class OracleLib(_Lib):
+    """The C restatement (oracle/axb_oracle.c)."""
+
+    prefix = "orc_"
+
+    def _declare(self):
+        S = C.c_size_t
+        self.generate_gaussian = self._f(
+            "generate_gaussian", None, [C.c_uint64, S, S, S, S, _dp, _dp, _dp, _dp])
+        self.spectral_norm = self._f(
+            "spectral_norm", C.c_double, [_dp, S, S, C.c_double, S, C.POINTER(C.c_int), _dp])
+        self.create = self._f(
+            "solver_create", C.c_void_p,
+            [_dp, S, S, _dp, S, S, _dp, _dp, C.POINTER(Config), C.POINTER(C.c_int), C.c_char_p, S])
+        self.destroy = self._f("solver_destroy", None, [C.c_void_p])
+        self.last_error = self._f("solver_last_error", C.c_char_p, [C.c_void_p])
+        self.step = self._f("solver_step", C.c_int, [C.c_void_p, _u64p])
+        self.update_row = self._f("solver_update_row", C.c_int, [C.c_void_p, C.c_uint64])
+        self.run = self._f("solver_run", C.c_int,
+                           [C.c_void_p, C.POINTER(Report), _u64p, _dp, _dp, _u64p, C.c_uint64, _dp])
+        self.checkpoint = self._f("solver_checkpoint", C.c_int, [C.c_void_p])
+        self.greedy_threshold = self._f("solver_greedy_threshold", C.c_int,
+                                        [C.c_void_p, C.c_double, _dp])
+        self.rgrbk_threshold = self._f("solver_rgrbk_threshold", C.c_int,
+                                       [C.c_void_p, C.c_double, _dp])
+        self.greedy_index_set = self._f("solver_greedy_index_set", C.c_int,
+                                        [C.c_void_p, C.c_double, _u64p, _u64p])
+        self.max_residual_ratio = self._f("solver_max_residual_ratio", C.c_int,
+                                          [C.c_void_p, _u64p, _dp])
+        self.select_cyclic = self._f("solver_select_cyclic", C.c_int, [C.c_void_p, _u64p])
+        self.select_rbk = self._f("solver_select_rbk", C.c_int, [C.c_void_p, _u64p])
+        self.select_greedy = self._f("solver_select_greedy", C.c_int,
+                                     [C.c_void_p, C.c_double, _u64p])
+        self.select_mwrbk = self._f("solver_select_mwrbk", C.c_int, [C.c_void_p, _u64p])
+        self.exact_metric = self._f("solver_exact_metric", C.c_int, [C.c_void_p, _dp])
+        self.residual_drift = self._f("solver_residual_drift", C.c_int, [C.c_void_p, _dp])
+        self.current_metric = self._f("solver_current_metric", C.c_double, [C.c_void_p])
+        self.iteration = self._f("solver_iteration", C.c_uint64, [C.c_void_p])
+        self.alpha = self._f("solver_alpha", C.c_double, [C.c_void_p])
+        self.spectral_norm_b = self._f("solver_spectral_norm_b", C.c_double, [C.c_void_p])
+        self.a_fro_sq = self._f("solver_a_fro_sq", C.c_double, [C.c_void_p])
+        self.residual_fro_sq = self._f("solver_residual_fro_sq", C.c_double, [C.c_void_p])
+        self.get_X = self._f("solver_get_X", None, [C.c_void_p, _dp])
+        self.get_R = self._f("solver_get_R", None, [C.c_void_p, _dp])
+        self.get_r_sq = self._f("solver_get_r_sq", None, [C.c_void_p, _dp])
+        self.get_a_sq = self._f("solver_get_a_sq", None, [C.c_void_p, _dp])
+        self.rng_state = self._f("solver_rng_state", None, [C.c_void_p, _u64p])
+
+
+class RefLib(_Lib):
+    """The unmodified reference engine (oracle/_ref/libaxbref.so)."""
+
+    prefix = "ref_"
+
+    def _declare(self):
+        S = C.c_size_t
+        self.generate_gaussian = self._f(
+            "generate_gaussian", None, [C.c_uint64, S, S, S, S, _dp, _dp, _dp, _dp])
+        self.rng_stream = self._f("rng_stream", C.c_uint64, [C.c_uint64, C.c_uint64, _u64p, _dp])
+        self.substream_seed = self._f("substream_seed", C.c_uint64, [C.c_uint64, C.c_uint64])
+        self.spectral_norm = self._f("spectral_norm", C.c_double,
+                                     [_dp, S, S, C.c_double, C.c_uint64, C.POINTER(C.c_int)])
+        self.create = self._f("solver_create", C.c_void_p,
+                              [_dp, S, S, _dp, S, S, _dp, _dp, C.POINTER(Config), C.POINTER(C.c_int)])
+        self.destroy = self._f("solver_destroy", None, [C.c_void_p])
+        self.last_error = self._f("solver_last_error", C.c_char_p, [C.c_void_p])
+        self.step = self._f("solver_step", C.c_int, [C.c_void_p, _u64p])
+        self.steps = self._f("solver_steps", C.c_int,
+                             [C.c_void_p, C.c_uint64, _u64p, C.c_int, C.c_uint64])
+        self.update_row = self._f("solver_update_row", C.c_int, [C.c_void_p, C.c_uint64])
+        self.run = self._f("solver_run", C.c_int,
+                           [C.c_void_p, C.POINTER(Report), _u64p, _dp, C.c_uint64, _dp])
+        self.checkpoint = self._f("solver_checkpoint", C.c_int, [C.c_void_p])
+        self.greedy_threshold = self._f("solver_greedy_threshold", C.c_int,
+                                        [C.c_void_p, C.c_double, _dp])
+        self.greedy_index_set = self._f("solver_greedy_index_set", C.c_int,
+                                        [C.c_void_p, C.c_double, _u64p, _u64p])
+        self.max_residual_ratio = self._f("solver_max_residual_ratio", C.c_int,
+                                          [C.c_void_p, _u64p, _dp])
+        self.exact_metric = self._f("solver_exact_metric", C.c_int, [C.c_void_p, _dp])
+        self.residual_drift = self._f("solver_residual_drift", C.c_int, [C.c_void_p, _dp])
+        self.current_metric = self._f("solver_current_metric", C.c_double, [C.c_void_p])
+        self.iteration = self._f("solver_iteration", C.c_uint64, [C.c_void_p])
+        self.alpha = self._f("solver_alpha", C.c_double, [C.c_void_p])
+        self.spectral_norm_b = self._f("solver_spectral_norm_b", C.c_double, [C.c_void_p])
+        self.a_fro_sq = self._f("solver_a_fro_sq", C.c_double, [C.c_void_p])
+        self.residual_fro_sq = self._f("solver_residual_fro_sq", C.c_double, [C.c_void_p])
+        self.get_X = self._f("solver_get_X", None, [C.c_void_p, _dp])
+        self.get_R = self._f("solver_get_R", None, [C.c_void_p, _dp])
+        self.get_r_sq = self._f("solver_get_r_sq", None, [C.c_void_p, _dp])
+        self.get_a_sq = self._f("solver_get_a_sq", None, [C.c_void_p, _dp])
+
+
+_oracle = None
+_ref = None
+
+
+def oracle() -> OracleLib:
+    global _oracle
+    if _oracle is None:
+        ensure_built()
+        _oracle = OracleLib(ORACLE_SO)
+    return _oracle
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref() -> RefLib:
+    global _ref
+    if _ref is None:
+        _ref = RefLib(REF_SO)
+    return _ref
+
+
+def generate(lib, seed, m, p, q, n):
+    """problems.hpp:345-364 for Gaussian sources: returns A, B, X*, C."""
+    A = np.empty((m, p)); B = np.empty((q, n)); X = np.empty((p, q)); Cm = np.empty((m, n))
+    lib.generate_gaussian(seed, m, p, q, n, _ptr(A), _ptr(B), _ptr(X), _ptr(Cm))
+    return A, B, X, Cm
+
+
+class Solver:
+    """Thin Python handle over either library's solver (mirrors axb::Solver)."""
+
+    def __init__(self, lib, A, B, Cm, X0, cfg):
+        self.lib = lib
+        self.A = np.ascontiguousarray(A, dtype=np.float64)
+        self.B = np.ascontiguousarray(B, dtype=np.float64)
+        self.C = np.ascontiguousarray(Cm, dtype=np.float64)
+        self.m, self.p = self.A.shape
+        self.q, self.n = self.B.shape
+        self.X0 = (np.zeros((self.p, self.q)) if X0 is None
+                   else np.ascontiguousarray(X0, dtype=np.float64))
+        self.cfg = cfg
+        st = C.c_int(0)
+        if isinstance(lib, OracleLib):
+            buf = C.create_string_buffer(256)
+            self.h = lib.create(_ptr(self.A), self.m, self.p, _ptr(self.B), self.q, self.n,
+                                _ptr(self.C), _ptr(self.X0), C.byref(cfg), C.byref(st), buf, 256)
+            msg = buf.value.decode()
+        else:
+            self.h = lib.create(_ptr(self.A), self.m, self.p, _ptr(self.B), self.q, self.n,
+                                _ptr(self.C), _ptr(self.X0), C.byref(cfg), C.byref(st))
+            msg = "reference ctor failed"
+        if not self.h:
+            raise OracleError(st.value, msg)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.destroy(self.h)
+            self.h = None
+
+    def _chk(self, code):
+        if code:
+            raise OracleError(code, self.lib.last_error(self.h).decode())
+
+    def step(self):
+        r = C.c_uint64()
+        self._chk(self.lib.step(self.h, C.byref(r)))
+        return r.value
+
+    def steps(self, k, mirror_refresh=False, refresh_interval=0):
+        rows = np.empty(k, dtype=np.uint64)
+        if isinstance(self.lib, RefLib):
+            self._chk(self.lib.steps(self.h, k, rows.ctypes.data_as(_u64p), int(mirror_refresh),
+                                     refresh_interval))
+        else:
+            for t in range(k):
+                rows[t] = self.step()
+                if mirror_refresh and refresh_interval and self.iteration % refresh_interval == 0:
+                    self.checkpoint()
+        return rows
+
+    def update_row(self, i):
+        self._chk(self.lib.update_row(self.h, i))
+
+    def checkpoint(self):
+        self._chk(self.lib.checkpoint(self.h))
+
+    def run(self, trace_cap=0):
+        rep = Report()
+        rows = np.zeros(max(trace_cap, 1), dtype=np.uint64)
+        rrn = np.zeros(max(trace_cap, 1))
+        X = np.empty((self.p, self.q))
+        if isinstance(self.lib, OracleLib):
+            code = self.lib.run(self.h, C.byref(rep), None, rrn.ctypes.data_as(_dp), None,
+                                rows.ctypes.data_as(_u64p), trace_cap, _ptr(X))
+        else:
+            code = self.lib.run(self.h, C.byref(rep), rows.ctypes.data_as(_u64p),
+                                rrn.ctypes.data_as(_dp), trace_cap, _ptr(X))
+        self._chk(code)
+        n = min(rep.trace_len, trace_cap)
+        return rep, rows[:n].copy(), rrn[:n].copy(), X
+
+    def greedy_threshold(self, theta):
+        out = C.c_double()
+        self._chk(self.lib.greedy_threshold(self.h, theta, C.byref(out)))
+        return out.value
+
+    def greedy_index_set(self, theta):
+        out = np.empty(self.m, dtype=np.uint64)
+        cnt = C.c_uint64()
+        self._chk(self.lib.greedy_index_set(self.h, theta, out.ctypes.data_as(_u64p), C.byref(cnt)))
+        return out[: cnt.value].copy()
+
+    def max_residual_ratio(self):
+        r = C.c_uint64(); v = C.c_double()
+        self._chk(self.lib.max_residual_ratio(self.h, C.byref(r), C.byref(v)))
+        return r.value, v.value
+
+    def exact_metric(self):
+        v = C.c_double()
+        self._chk(self.lib.exact_metric(self.h, C.byref(v)))
+        return v.value
+
+    def residual_drift(self):
+        v = C.c_double()
+        self._chk(self.lib.residual_drift(self.h, C.byref(v)))
+        return v.value
+
+    @property
+    def iteration(self):
+        return self.lib.iteration(self.h)
+
+    @property
+    def alpha(self):
+        return self.lib.alpha(self.h)
+
+    @property
+    def spectral_norm_b(self):
+        return self.lib.spectral_norm_b(self.h)
+
+    @property
+    def residual_fro_sq(self):
+        return self.lib.residual_fro_sq(self.h)
+
+    @property
+    def a_fro_sq(self):
+        return self.lib.a_fro_sq(self.h)
+
+    def current_metric(self):
+        return self.lib.current_metric(self.h)
+
+    def X(self):
+        out = np.empty((self.p, self.q)); self.lib.get_X(self.h, _ptr(out)); return out
+
+    def R(self):
+        out = np.empty((self.m, self.n)); self.lib.get_R(self.h, _ptr(out)); return out
+
+    def r_sq(self):
+        out = np.empty(self.m); self.lib.get_r_sq(self.h, _ptr(out)); return out
+
+    def a_sq(self):
+        out = np.empty(self.m); self.lib.get_a_sq(self.h, _ptr(out)); return out
