@@ -1,0 +1,185 @@
+/*
+ * axb_b200.h — C-ABI of the B200-native row-action solver for A·X·B = C.
+ *
+ * Drop-in boundary for the reference's header-only engine
+ * (/root/reference/proj/include/axb/solver.hpp).  Every entry point below names
+ * the reference interface it replaces.  Plain pointers and sizes only; no torch
+ * or CUDA types in the signatures.  All matrices are dense, row-major FP64
+ * (matrix.hpp:37-70): A is m×p, B is q×n, C and R are m×n, X is p×q.
+ *
+ * Errors: every function returns an axb_status; the codes map 1:1 onto the
+ * reference's exception types (errors.hpp:10-72).  The message of the last
+ * failure on a handle is available from axb_solver_last_error().  The C++ shim
+ * include/axb_b200/solver.hpp rethrows them as the axb:: exception types.
+ *
+ * Threading: a handle is single-owner and not thread-safe, like axb::Solver
+ * (rng.hpp:15-17); different handles may run concurrently on
+ * different devices/streams.
+ *
+ * There is no CPU fallback: creating a solver without a usable sm_100 device
+ * fails with AXB_CUDA_ERROR.
+ */
+#ifndef AXB_B200_H
+#define AXB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AXB_B200_ABI_VERSION 1
+
+typedef enum {
+    AXB_OK = 0,
+    AXB_SHAPE_ERROR = 1,       /* axb::ShapeError       errors.hpp:15-17 */
+    AXB_DOMAIN_ERROR = 2,      /* axb::DomainError      errors.hpp:20-22 */
+    AXB_CONFIG_ERROR = 3,      /* axb::ConfigError      errors.hpp:30-32 */
+    AXB_DIVERGENCE_ERROR = 4,  /* axb::DivergenceError  errors.hpp:60-67 */
+    AXB_INVARIANT_ERROR = 5,   /* axb::InvariantError   errors.hpp:70-72 */
+    AXB_CONVERGENCE_ERROR = 6, /* axb::ConvergenceError errors.hpp:53-57 */
+    AXB_CUDA_ERROR = 7,        /* device / runtime failure (no reference analogue) */
+    AXB_CAPACITY_ERROR = 8     /* axb::CapacityError    errors.hpp:25-27 (HBM exhausted) */
+} axb_status;
+
+/* MethodTag (solver.hpp:16) */
+enum { AXB_BK = 0, AXB_RBK = 1, AXB_GRBK = 2, AXB_RGRBK = 3, AXB_MWRBK = 4 };
+/* AlphaRule (solver.hpp:68) */
+enum { AXB_ALPHA_SAFE = 0, AXB_ALPHA_PAPER = 1, AXB_ALPHA_FIXED = 2 };
+/* StopRule::Kind (solver.hpp:80) */
+enum { AXB_STOP_SOLUTION_RRN = 0, AXB_STOP_RESIDUAL_REL = 1 };
+/* Terminated (solver.hpp:118) */
+enum { AXB_TERMINATED_TOLERANCE = 0, AXB_TERMINATED_MAX_ITER = 1 };
+
+/* SolveConfig (solver.hpp:100-109), flattened.  `reference` is the p×q X_ref of
+ * StopRule::solution_rrn (host pointer; copied at create). */
+typedef struct {
+    int32_t method;
+    int32_t has_theta;
+    double theta;
+    int32_t alpha_rule;
+    int32_t stop_kind;
+    double alpha_value;
+    double tol;
+    const double* reference;
+    uint64_t max_iter;
+    uint64_t seed;
+    int32_t record_trace;
+    int32_t _pad;
+    uint64_t refresh_interval;
+} axb_config;
+
+/* SolveReport (solver.hpp:120-133) minus the owned vectors (trace and X are
+ * copied into caller buffers by axb_solver_run). */
+typedef struct {
+    uint64_t iterations;
+    double wall_seconds;
+    double final_rrn;
+    double final_residual_rel;
+    int32_t terminated_by;
+    int32_t alpha_outside_bound;
+    double alpha;
+    uint64_t seed;
+    uint64_t skipped_zero_rows;
+    uint64_t trace_len;
+    uint64_t diverged_iteration; /* DivergenceError::iteration */
+    double diverged_residual;    /* DivergenceError::residual_norm */
+} axb_report;
+
+/* B200 placement / execution options (no reference analogue).  Zero-initialise
+ * and set what you need; axb_options_default() fills the defaults. */
+typedef struct {
+    int32_t device;            /* CUDA ordinal */
+    int32_t inputs_on_device;  /* 1: A,B,C,X0 (and cfg.reference) are device pointers */
+    int32_t cache_gram;        /* -1 auto, 0 form g = A·A_iᵀ per step, 1 cache G = A·Aᵀ */
+    int32_t spectral_on_device;/* -1 auto, 0 host (bitwise reference α), 1 device */
+    int32_t graph_iters;       /* iterations captured per CUDA graph (0 = default) */
+    int32_t tie_guard;         /* 1 (default): exact sequential re-check of near-boundary draws */
+    uint64_t spectral_max_iter;/* power-iteration cap (0 = reference default 5000) */
+    double alpha_override;     /* >0: use this α verbatim (e.g. the oracle's), skip ‖B‖₂ */
+    /* row sharding (§8(e)): this handle owns rows [row_offset, row_offset+m) of an
+     * m_global-row system; NULL comm = single GPU. */
+    void* nccl_comm;           /* ncclComm_t, or NULL */
+    int32_t world_size;
+    int32_t rank;
+    uint64_t m_global;
+    uint64_t row_offset;
+} axb_options;
+
+typedef struct axb_solver axb_solver;
+
+void axb_options_default(axb_options* opt);
+int axb_abi_version(void);
+/* 1 when a device that can run the sm_100a kernels is visible. */
+int axb_device_available(void);
+
+/* Solver::Solver(A, B, C, X0, cfg)  — solver.hpp:146-192.
+ * A m×p, B q×n, C m×n, X0 p×q (NULL = zeros). */
+int axb_solver_create(const double* A, uint64_t m, uint64_t p, const double* B, uint64_t q,
+                      uint64_t n, const double* C, const double* X0, const axb_config* cfg,
+                      const axb_options* opt, axb_solver** out);
+void axb_solver_destroy(axb_solver* s);
+const char* axb_solver_last_error(const axb_solver* s);
+/* message for failures of axb_solver_create (handle-less), thread-local */
+const char* axb_last_create_error(void);
+
+/* Solver::step() — solver.hpp:321-333.  One iteration; returns the row. */
+int axb_solver_step(axb_solver* s, uint64_t* row);
+/* k consecutive step() calls (the acceptance.cpp:128-141 driver loop, batched
+ * on the device).  rows (may be NULL) receives the k selected rows.  When
+ * mirror_refresh is set, checkpoint() runs every cfg.refresh_interval
+ * iterations exactly as run() schedules it (solver.hpp:359-360). */
+int axb_solver_steps(axb_solver* s, uint64_t k, uint64_t* rows, int32_t mirror_refresh);
+/* Solver::update_row(i) — solver.hpp:264-318. */
+int axb_solver_update_row(axb_solver* s, uint64_t i);
+/* Solver::run() — solver.hpp:337-372.  trace_* (may be NULL) receive up to
+ * trace_cap TracePoints (:111-116); x_out (may be NULL) receives X (p×q). */
+int axb_solver_run(axb_solver* s, axb_report* rep, uint64_t* trace_k, double* trace_rrn,
+                   double* trace_rel, uint64_t* trace_row, uint64_t trace_cap, double* x_out);
+
+/* selection rules, as public methods of Solver (solver.hpp:197-258, 387-400) */
+int axb_solver_select_cyclic(axb_solver* s, uint64_t* row);
+int axb_solver_select_rbk(axb_solver* s, uint64_t* row);
+int axb_solver_select_greedy(axb_solver* s, double theta, uint64_t* row);
+int axb_solver_select_mwrbk(axb_solver* s, uint64_t* row);
+int axb_solver_greedy_threshold(axb_solver* s, double theta, double* out);
+int axb_solver_rgrbk_threshold(axb_solver* s, double theta, double* out);
+int axb_solver_greedy_index_set(axb_solver* s, double theta, uint64_t* out, uint64_t* count);
+int axb_solver_max_residual_ratio(axb_solver* s, uint64_t* row, double* ratio);
+
+/* metrics and drift checkpoint (solver.hpp:403-436) */
+int axb_solver_current_metric(axb_solver* s, double* out);
+int axb_solver_current_residual_rel(axb_solver* s, double* out);
+int axb_solver_exact_metric(axb_solver* s, double* out);
+int axb_solver_exact_residual_rel(axb_solver* s, double* out);
+int axb_solver_residual_drift(axb_solver* s, double* out);
+int axb_solver_checkpoint(axb_solver* s);
+
+/* accessors (solver.hpp:376-385); copy-out into caller-owned host buffers */
+uint64_t axb_solver_iteration(const axb_solver* s);
+double axb_solver_alpha(const axb_solver* s);
+double axb_solver_spectral_norm_b(const axb_solver* s);
+int axb_solver_alpha_outside_bound(const axb_solver* s);
+double axb_solver_a_fro_sq(const axb_solver* s);
+int axb_solver_residual_fro_sq(axb_solver* s, double* out);
+int axb_solver_get_X(axb_solver* s, double* out);        /* p×q */
+int axb_solver_get_R(axb_solver* s, double* out);        /* m×n (local rows) */
+int axb_solver_get_r_sq(axb_solver* s, double* out);     /* m */
+int axb_solver_get_a_sq(axb_solver* s, double* out);     /* m */
+int axb_solver_dims(const axb_solver* s, uint64_t dims[4]); /* m, p, q, n */
+
+/* ---- measurement hooks (bench.py) ---- */
+/* Device time (ms) of the last run()/steps() loop, CUDA events on the solver's
+ * stream, and the summed device time of the residual-update kernel (K2) inside
+ * it, with its launch count. */
+int axb_solver_last_timing(const axb_solver* s, double* loop_ms, double* k2_ms,
+                           uint64_t* k2_launches, uint64_t* kernel_launches);
+/* Enable per-kernel CUDA-event timing of K2 inside steps()/run() (adds events to
+ * the captured graph; off by default). */
+int axb_solver_set_profiling(axb_solver* s, int32_t on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AXB_B200_H */

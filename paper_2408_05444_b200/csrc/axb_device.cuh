@@ -1,0 +1,161 @@
+// axb_device.cuh — device-side state and kernel interfaces of the B200 solver.
+//
+// The reference keeps the whole iteration state in host memory inside
+// axb::Solver (solver.hpp:496-514).  Here it lives in HBM: the matrices in
+// row-major FP64 buffers and the scalar state (iteration counter, xoshiro256**
+// stream, selected row, running reductions, stop flags) in one DevState block
+// that every kernel of an iteration reads, so an iteration needs no host
+// round trip and a batch of iterations is one captured CUDA graph.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace axb_dev {
+
+// status values of DevState::status
+enum : int32_t {
+    ST_RUN = 0,       // iterate
+    ST_PAUSE = 1,     // tracked stop metric <= tol: host confirms (solver.hpp:351-358)
+    ST_ZERO = 2,      // ‖R‖² == 0 in run(): nothing to select (solver.hpp:347)
+    ST_ERROR = 3      // err_code holds the axb_status (DivergenceError, DomainError, …)
+};
+
+// finalize modes of the residual kernel
+enum : int32_t {
+    FIN_NORMS = 0,     // init / adopt: norms + reductions + (re)select
+    FIN_ITERATION = 1, // a step(): k++, trace, stop check, pre-select the next row
+    FIN_UPDATE_ROW = 2 // public update_row(i): no k++, no trace, no stop check
+};
+
+struct alignas(16) DevState {
+    // control
+    unsigned long long k;        // iterations completed
+    unsigned long long k_limit;  // kernels are no-ops once k >= k_limit
+    unsigned long long k0;       // iteration index stored in trace slot 0
+    int32_t status;
+    int32_t err_code;
+    unsigned long long err_k;
+    double err_val;
+    int32_t fin_mode;
+    int32_t run_mode;            // 1 inside run() (zero-residual break), 0 in step()/steps()
+    // selection (rng.hpp:18-123 state; solver.hpp:511 cyclic_pos_, skipped_zero_rows_)
+    unsigned long long rng[4];
+    unsigned long long cyclic_pos;
+    unsigned long long skipped_zero_rows;
+    // snapshot taken before the speculative pre-selection (rolled back when R
+    // changes outside the iteration pipeline or a public select_* is called)
+    unsigned long long rng_snap[4];
+    unsigned long long cyclic_snap;
+    unsigned long long skipped_snap;
+    int32_t sel_valid;
+    int32_t tie_guard_hits;
+    long long sel;               // selected row (global index)
+    double coef;                 // α / ‖A_sel‖²
+    // reductions of the current residual
+    double r_fro_sq;             // Σ_l ‖R_l‖² (fresh tree sum)
+    double max_ratio;            // max_l ‖R_l‖²/‖A_l‖²
+    long long argmax;            // smallest l attaining it
+    double err_sq;               // ‖X − X_ref‖²_F (fresh, solution_rrn)
+    double metric;               // current stop metric
+    int32_t x_finite;            // X all finite (checkpoint guard, solver.hpp:428)
+    int32_t _pad0;
+    // query results (greedy_threshold / max_residual_ratio)
+    double q_zeta;
+    long long q_row;
+    long long q_count;
+    // self-resetting last-block counters
+    unsigned int cnt_r;
+    unsigned int cnt_x;
+    unsigned int cnt_red;
+    unsigned int _pad1;
+};
+
+struct RowRecord {   // per-CTA partial of the residual reduction
+    double sum;      // Σ ‖R_l‖² over the CTA's rows
+    double max_ratio;
+    long long argmax;
+    double _pad;
+};
+
+// Everything an iteration needs; constant for the life of a solver, so the
+// captured graph's kernel parameters never change.
+struct Params {
+    long long m, p, q, n;        // m = local rows of A, C, R
+    long long row0;              // global index of local row 0
+    long long m_global;
+    const double* A;             // m×p
+    const double* B;             // q×n
+    double* R;                   // m×n
+    double* X;                   // p×q
+    const double* Xref;          // p×q or null
+    const double* a_sq;          // m   (host-computed in reference order)
+    const double* rbk_cum;       // m_global (host-computed in reference order)
+    double* r_sq;                // m
+    const double* G;             // cached Gram columns: G[i*m + l] = A_i·A_l, or null
+    double* g;                   // m   (when G is null)
+    double* y;                   // q
+    double* z;                   // n
+    double* zpart;               // nzj × n
+    unsigned int* zcnt;          // nslab counters
+    double* xpart;               // x-update partials
+    RowRecord* rrec;             // residual partials
+    long long* trace_row;        // batch trace of selected rows
+    double* trace_metric;        // batch trace of the stop metric
+    double* trace_rel;           // batch trace of ‖R‖/‖C‖
+    unsigned long long trace_cap;
+    int* member_flags;           // m (greedy_index_set query)
+    DevState* st;
+    double alpha, theta, a_fro_sq, tol, ref_sq, c_fro;
+    int method, stop_kind, tie_guard, vec2;
+    // launch geometry
+    int r_grid, r_rows_per_cta, r_chunk;
+    int yg_grid;
+    int z_nslab, z_nj, z_jrows, x_ctas;
+};
+
+// ---- launchers (axb_iter.cu) ----
+void launch_yg(const Params& P, cudaStream_t s, bool with_g);
+void launch_zx(const Params& P, cudaStream_t s);
+void launch_r(const Params& P, cudaStream_t s, bool update);
+void launch_select(const Params& P, cudaStream_t s, int method, double theta, int consume);
+void launch_query(const Params& P, cudaStream_t s, double theta, int want_set);
+void launch_rollback(const Params& P, cudaStream_t s);
+void launch_err_fresh(const Params& P, cudaStream_t s);
+// device power iteration helpers: y = M v (rows), w = Mᵀ y (cols)
+void launch_rowdot(const double* M, long long rows, long long cols, const double* v, double* out,
+                   cudaStream_t s);
+void launch_coldot(const double* M, long long rows, long long cols, const double* v, double* out,
+                   double* part, unsigned int* cnt, int nj, int jrows, cudaStream_t s);
+void launch_power_step(const double* v_in, const double* w, double* v_out, long long dim,
+                       double* out2, cudaStream_t s);
+void launch_fill(double* p, long long n, double v, cudaStream_t s);
+void launch_ctrl(DevState* st, unsigned long long k0, unsigned long long k_limit, int fin_mode,
+                 int run_mode, int reset_status, cudaStream_t s);
+void launch_set_sel(DevState* st, long long sel, double coef, cudaStream_t s);
+int sumsq_parts(long long n);
+void launch_sumsq(const double* v, long long n, double* part, cudaStream_t s);
+void launch_row_sq_seq(const double* A, long long m, long long p, double* out, cudaStream_t s);
+void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* total, cudaStream_t s);
+
+// ---- DMMA GEMM (axb_gemm.cu) ----
+// D = (Cin ? Cin − A·op(B) : A·op(B)); op(B) = B (K×N) or Bᵀ (B is N×K) when b_trans.
+// Optional per-CTA partials: sum of D² (sq_part) and of (Rold − D)² (diff_part),
+// reduced deterministically by reduce_parts().  store=0 skips writing D.
+struct GemmArgs {
+    long long M, N, K;
+    const double* A; long long lda;
+    const double* B; long long ldb;
+    int b_trans;
+    double* D; long long ldd;
+    const double* Cin; long long ldc;
+    const double* Rold; long long ldr;
+    double* sq_part;
+    double* diff_part;
+    int store;
+};
+int gemm_num_ctas(long long M, long long N);
+void launch_gemm(const GemmArgs& g, cudaStream_t s);
+void launch_reduce_parts(const double* part, long long n, double* out, cudaStream_t s);
+
+}  // namespace axb_dev

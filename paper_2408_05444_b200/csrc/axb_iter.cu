@@ -1,0 +1,903 @@
+// axb_iter.cu — the per-iteration kernels of the B200 row-action solver.
+//
+// One Kaczmarz iteration of the reference (Solver::step, solver.hpp:321-333 →
+// select_* :197-258 + update_row :264-318) is three kernels here, captured into
+// a CUDA graph by the host:
+//
+//   K4  k_yg   y = B·R_iᵀ (q row dots, solver.hpp:270) and, when G = A·Aᵀ is not
+//              cached, g = A·A_iᵀ (m row dots, the G column of :294).
+//   K4b k_zx   z = yᵀ·B (= R_i·BᵀB, :293, as two GEMVs over B — cheaper than the
+//              reference's cached n×n BᵀB) fused with K5, the X row update
+//              X_t += (coef·A_it)·y (:272-289) and the fresh ‖X−X_ref‖² sum.
+//   K2  k_r    the fused residual update: ONE pass over R with 128-bit loads,
+//              R_l −= (coef·g_l)·z, ‖R_l‖² emitted in the same pass (:294-305),
+//              per-CTA {Σ‖R_l‖², max ratio, argmax} records; the last CTA to
+//              finish reduces them, runs the stop/divergence logic (:306-307,
+//              :351-358) and — K3 — selects the next row on the device with the
+//              reference's xoshiro256** stream (rng.hpp:30-43, 84-99), so no host
+//              round trip happens between iterations.
+//
+// All reductions use fixed shapes and fixed orders: results are deterministic
+// run to run.  The R and X updates use separately rounded multiply and subtract
+// (__dmul_rn/__dsub_rn), i.e. the reference's arithmetic (no FMA contraction).
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "axb_device.cuh"
+
+namespace axb_dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ bool halted(const DevState* st) {
+    return st->status != ST_RUN || st->k >= st->k_limit;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block-wide sum (deterministic tree); result valid in all threads
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+    t = warp_sum(t);
+    return t;
+}
+
+// (max ratio, smallest index) pair reduction; valid in all threads
+__device__ __forceinline__ void maxidx_merge(double& v, long long& i, double ov, long long oi) {
+    if (ov > v || (ov == v && oi < i)) {
+        v = ov;
+        i = oi;
+    }
+}
+
+__device__ void block_maxidx(double& v, long long& i, double* redv, long long* redi) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        long long oi = __shfl_xor_sync(0xffffffffu, i, o);
+        maxidx_merge(v, i, ov, oi);
+    }
+    __syncthreads();
+    if (lane == 0) {
+        redv[w] = v;
+        redi[w] = i;
+    }
+    __syncthreads();
+    v = -INFINITY;
+    i = LLONG_MAX;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) maxidx_merge(v, i, redv[k], redi[k]);
+}
+
+// ---- xoshiro256** (rng.hpp:30-43) ----
+__device__ __forceinline__ unsigned long long rotl64(unsigned long long x, int k) {
+    return (x << k) | (x >> (64 - k));
+}
+__device__ unsigned long long rng_next(unsigned long long* s) {
+    const unsigned long long result = rotl64(s[1] * 5ull, 7) * 9ull;
+    const unsigned long long t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl64(s[3], 45);
+    return result;
+}
+__device__ double rng_unit(unsigned long long* s) {
+    return __dmul_rn((double)(rng_next(s) >> 11), 0x1.0p-53);
+}
+
+// dot of a row with a vector by one warp; lane-strided partials then a
+// shuffle tree (deterministic).  vec2: both pointers 16-byte aligned, len even.
+__device__ double warp_dot(const double* __restrict__ row, const double* __restrict__ v,
+                           long long len, int lane, bool vec2) {
+    double acc = 0.0;
+    if (vec2) {
+        const double2* r2 = reinterpret_cast<const double2*>(row);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const long long h = len >> 1;
+#pragma unroll 4
+        for (long long k = lane; k < h; k += 32) {
+            const double2 a = __ldg(r2 + k);
+            const double2 b = __ldg(v2 + k);
+            acc += a.x * b.x;
+            acc += a.y * b.y;
+        }
+    } else {
+#pragma unroll 4
+        for (long long k = lane; k < len; k += 32) acc += __ldg(row + k) * __ldg(v + k);
+    }
+    return warp_sum(acc);
+}
+
+// ------------------------------------------------------------------------
+// K4: y = B·R_iᵀ (solver.hpp:270) [+ g = A·A_iᵀ, the Gram column of :294]
+__global__ void __launch_bounds__(kThreads) k_yg(Params P, int with_g) {
+    const DevState* st = P.st;
+    if (halted(st)) return;
+    const long long il = st->sel - P.row0;
+    const double* Ri = P.R + il * P.n;
+    const double* Ai = P.A + il * P.p;
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long items = P.q + (with_g ? P.m : 0);
+    const bool vb = (P.n & 1) == 0, va = (P.p & 1) == 0;
+    for (long long it = warp; it < items; it += nwarps) {
+        double acc;
+        if (it < P.q) {
+            acc = warp_dot(P.B + it * P.n, Ri, P.n, lane, vb);
+            if (lane == 0) P.y[it] = acc;
+        } else {
+            const long long l = it - P.q;
+            acc = warp_dot(P.A + l * P.p, Ai, P.p, lane, va);
+            if (lane == 0) P.g[l] = acc;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// K4b + K5: z = yᵀ·B (column slabs × row chunks, deterministic last-block
+// combine) and the X row update with the fresh ‖X − X_ref‖² partial sums.
+__global__ void __launch_bounds__(kThreads) k_zx(Params P) {
+    __shared__ double red[kWarps];
+    __shared__ bool last;
+    DevState* st = P.st;
+    if (halted(st)) return;
+    const int nzc = P.z_nslab * P.z_nj;
+    const int tid = threadIdx.x;
+    if ((int)blockIdx.x < nzc) {
+        const int slab = blockIdx.x % P.z_nslab;
+        const int jc = blockIdx.x / P.z_nslab;
+        const long long j0 = (long long)jc * P.z_jrows;
+        const long long j1 = min(P.q, j0 + P.z_jrows);
+        const long long c = (long long)slab * (2 * kThreads) + 2 * tid;
+        double a0 = 0.0, a1 = 0.0;
+        if ((P.n & 1) == 0) {
+            if (c < P.n) {
+                const double2* Bc = reinterpret_cast<const double2*>(P.B + c);
+                const long long ld2 = P.n >> 1;
+#pragma unroll 8
+                for (long long j = j0; j < j1; ++j) {
+                    const double yj = __ldg(P.y + j);
+                    const double2 b = __ldg(Bc + j * ld2);
+                    a0 += yj * b.x;
+                    a1 += yj * b.y;
+                }
+            }
+        } else {
+            for (long long j = j0; j < j1; ++j) {
+                const double yj = __ldg(P.y + j);
+                if (c < P.n) a0 += yj * __ldg(P.B + j * P.n + c);
+                if (c + 1 < P.n) a1 += yj * __ldg(P.B + j * P.n + c + 1);
+            }
+        }
+        if (P.z_nj == 1) {
+            if (c < P.n) P.z[c] = a0;
+            if (c + 1 < P.n) P.z[c + 1] = a1;
+            return;
+        }
+        double* zp = P.zpart + (long long)jc * P.n;
+        if (c < P.n) zp[c] = a0;
+        if (c + 1 < P.n) zp[c + 1] = a1;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) last = atomicAdd(P.zcnt + slab, 1u) == (unsigned)(P.z_nj - 1);
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        for (long long cc = c; cc < c + 2 && cc < P.n; ++cc) {
+            double s = 0.0;
+            for (int k = 0; k < P.z_nj; ++k) s += __ldcg(P.zpart + (long long)k * P.n + cc);
+            P.z[cc] = s;
+        }
+        if (tid == 0) P.zcnt[slab] = 0u;
+        return;
+    }
+    // ---- X update (solver.hpp:272-290) ----
+    const int xb = blockIdx.x - nzc;
+    const long long il = st->sel - P.row0;
+    const double* Ai = P.A + il * P.p;
+    const double coef = st->coef;
+    const long long total = P.p * P.q;
+    const bool track = P.Xref != nullptr;
+    double acc = 0.0;
+    for (long long e = (long long)xb * kThreads + tid; e < total; e += (long long)P.x_ctas * kThreads) {
+        const long long t = e / P.q, j = e - t * P.q;
+        const double f = __dmul_rn(coef, __ldg(Ai + t));
+        const double x1 = __dadd_rn(P.X[e], __dmul_rn(f, __ldg(P.y + j)));
+        P.X[e] = x1;
+        if (track) {
+            const double d1 = x1 - __ldg(P.Xref + e);
+            acc += d1 * d1;
+        }
+    }
+    if (!track) return;
+    acc = block_sum(acc, red);
+    if (tid == 0) {
+        P.xpart[xb] = acc;
+        __threadfence();
+        last = atomicAdd(&st->cnt_x, 1u) == (unsigned)(P.x_ctas - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s = 0.0;
+    for (int k = tid; k < P.x_ctas; k += kThreads) s += __ldcg(P.xpart + k);
+    s = block_sum(s, red);
+    if (tid == 0) {
+        st->err_sq = s;
+        st->cnt_x = 0u;
+    }
+}
+
+// ------------------------------------------------------------------------
+// K3: row selection for the next iteration, executed by one 256-thread block.
+// Writes *out_row; returns an axb_status (0 ok).  All threads must call it.
+struct SelShared {
+    double scan[kThreads];
+    double redv[kWarps];
+    long long redi[kWarps];
+    double target;
+    double u;
+    long long cand;
+    int err;
+};
+
+__device__ int select_rows(const Params& P, DevState* st, int method, double theta,
+                           long long* out_row, SelShared& sh) {
+    const int tid = threadIdx.x;
+    const long long m = P.m;
+    if (method == 4) {  // MWRBK: smallest argmax (solver.hpp:258, 387-400)
+        if (st->argmax == LLONG_MAX) return 2;
+        *out_row = st->argmax;
+        return 0;
+    }
+    if (method == 0) {  // BK: cyclic, zero rows skipped (solver.hpp:197-206)
+        if (tid == 0) {
+            sh.err = 2;
+            for (long long tries = 0; tries < m; ++tries) {
+                const long long i = (long long)st->cyclic_pos;
+                st->cyclic_pos = (st->cyclic_pos + 1) % (unsigned long long)m;
+                if (P.a_sq[i] > 0.0) {
+                    sh.cand = i;
+                    sh.err = 0;
+                    break;
+                }
+                ++st->skipped_zero_rows;
+            }
+        }
+        __syncthreads();
+        *out_row = sh.cand;
+        return sh.err;
+    }
+    if (method == 1) {  // RBK: categorical_cdf on the static ‖A_i‖² CDF (solver.hpp:209)
+        if (tid == 0) {
+            const double* cum = P.rbk_cum;
+            const double total = cum[m - 1];
+            sh.err = 0;
+            if (!(total > 0.0)) {
+                sh.err = 2;
+            } else {
+                const double target = __dmul_rn(rng_unit(st->rng), total);
+                long long lo = 0, hi = m - 1;
+                while (lo < hi) {  // rng.hpp:88-95
+                    const long long mid = (lo + hi) / 2;
+                    if (cum[mid] <= target) lo = mid + 1;
+                    else hi = mid;
+                }
+                while (lo > 0 && cum[lo] == cum[lo - 1]) --lo;  // rng.hpp:97
+                sh.cand = lo;
+            }
+        }
+        __syncthreads();
+        *out_row = sh.cand;
+        return sh.err;
+    }
+    // GRBK / RGRBK (solver.hpp:212-254): ζ, membership, member-mass draw.
+    const double r_fro = st->r_fro_sq;
+    if (!(r_fro > 0.0)) return 2;  // "greedy threshold: zero residual"
+    const long long argmax = st->argmax;
+    const double zeta = __dadd_rn(__dmul_rn(theta, __ddiv_rn(st->max_ratio, r_fro)),
+                                  __ddiv_rn(__dsub_rn(1.0, theta), P.a_fro_sq));
+    const long long seg = (m + kThreads - 1) / kThreads;
+    const long long s0 = min(m, (long long)tid * seg), s1 = min(m, s0 + seg);
+    auto member = [&](long long i) -> bool {
+        const double as = P.a_sq[i];
+        if (as <= 0.0) return false;
+        return i == argmax || __ldcg(P.r_sq + i) >= __dmul_rn(__dmul_rn(zeta, as), r_fro);
+    };
+    double local = 0.0;
+    for (long long i = s0; i < s1; ++i)
+        if (member(i)) local = __dadd_rn(local, __ldcg(P.r_sq + i));
+    // exclusive scan of the per-thread segment sums (Hillis–Steele, fixed order)
+    sh.scan[tid] = local;
+    __syncthreads();
+    for (int off = 1; off < kThreads; off <<= 1) {
+        const double v = tid >= off ? sh.scan[tid - off] : 0.0;
+        __syncthreads();
+        sh.scan[tid] = __dadd_rn(sh.scan[tid], v);
+        __syncthreads();
+    }
+    const double total = sh.scan[kThreads - 1];
+    const double excl = tid ? sh.scan[tid - 1] : 0.0;
+    if (!(total > 0.0)) return 2;  // mass on zero rows only (solver.hpp:249-252)
+    if (tid == 0) {
+        sh.u = rng_unit(st->rng);
+        sh.target = __dmul_rn(sh.u, total);
+        sh.cand = LLONG_MAX;
+    }
+    __syncthreads();
+    const double target = sh.target;
+    // first member whose running cumulative mass exceeds the target (upper_bound)
+    long long mine = LLONG_MAX;
+    double lo_c = 0.0, hi_c = 0.0;
+    {
+        double cum = excl;
+        for (long long i = s0; i < s1; ++i) {
+            if (!member(i)) continue;
+            const double nc = __dadd_rn(cum, __ldcg(P.r_sq + i));
+            if (nc > target) {
+                mine = i;
+                lo_c = cum;
+                hi_c = nc;
+                break;
+            }
+            cum = nc;
+        }
+    }
+    if (mine != LLONG_MAX) atomicMin(reinterpret_cast<unsigned long long*>(&sh.cand),
+                                     (unsigned long long)mine);
+    __syncthreads();
+    long long pick = sh.cand;
+    const bool exact_needed = pick == LLONG_MAX;
+    __syncthreads();
+    if (tid == 0) sh.err = 0;
+    __syncthreads();
+    if (!exact_needed && P.tie_guard && mine == pick) {
+        // the parallel cumsum rounds differently from the reference's sequential
+        // one; if the draw landed within that rounding of a boundary, re-run the
+        // reference's sequential walk (rare; keeps the pick bitwise-faithful).
+        const double slack = 8.0 * (double)m * DBL_EPSILON * total;
+        if (hi_c - target <= slack || target - lo_c <= slack) sh.err = -1;
+    }
+    __syncthreads();
+    if (exact_needed || sh.err == -1) {
+        __syncthreads();
+        if (tid == 0) {
+            // Sequential replay of solver.hpp:243-253 + rng.hpp:84-99 with the same
+            // uniform u: cumulative mass in ascending member order, target = u·total,
+            // upper_bound, then walk back over a trailing zero-weight plateau.
+            const double u = sh.u;
+            double total_seq = 0.0;
+            for (long long i = 0; i < m; ++i)
+                if (member(i)) total_seq = __dadd_rn(total_seq, __ldcg(P.r_sq + i));
+            const double tseq = __dmul_rn(u, total_seq);
+            double cum = 0.0;
+            long long found = -1, first_member = -1, last_change = -1;
+            for (long long i = 0; i < m && found < 0; ++i) {
+                if (!member(i)) continue;
+                if (first_member < 0) first_member = i;
+                const double nc = __dadd_rn(cum, __ldcg(P.r_sq + i));
+                if (nc > tseq) found = i;
+                if (nc != cum) last_change = i;
+                cum = nc;
+            }
+            if (found < 0) found = last_change >= 0 ? last_change : first_member;
+            sh.cand = found;
+            sh.err = 0;
+            atomicAdd(&st->tie_guard_hits, 1);
+        }
+        __syncthreads();
+        pick = sh.cand;
+    }
+    *out_row = pick;
+    return 0;
+}
+
+// block-level finalize + selection shared by k_r's last block and k_select
+__device__ void finish_select(const Params& P, DevState* st, SelShared& sh) {
+    long long row = 0;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 4; ++k) st->rng_snap[k] = st->rng[k];
+        st->cyclic_snap = st->cyclic_pos;
+        st->skipped_snap = st->skipped_zero_rows;
+        sh.err = 0;
+    }
+    __syncthreads();
+    const int err = select_rows(P, st, P.method, P.theta, &row, sh);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (err) {
+            st->status = ST_ERROR;
+            st->err_code = err;
+            st->err_k = st->k;
+            st->sel_valid = 0;
+        } else {
+            st->sel = row;
+            st->coef = __ddiv_rn(P.alpha, P.a_sq[row - P.row0]);
+            st->sel_valid = 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// K2: fused residual update + row norms + reductions (+ finalize / K3 select)
+template <bool UPDATE, bool VEC2>
+__global__ void __launch_bounds__(kThreads) k_r(Params P) {
+    extern __shared__ double smem[];
+    __shared__ double redv[kWarps];
+    __shared__ long long redi[kWarps];
+    __shared__ bool last;
+    __shared__ SelShared sh;
+    DevState* st = P.st;
+    if (UPDATE && halted(st)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long m = P.m, n = P.n;
+    const long long r0 = (long long)blockIdx.x * P.r_rows_per_cta;
+    const long long r1 = min(m, r0 + P.r_rows_per_cta);
+    double* zs = smem;
+    double* rowacc = smem + P.r_chunk;
+    double coef = 0.0;
+    long long sel = 0;
+    if (UPDATE) {
+        coef = st->coef;
+        sel = st->sel;
+    }
+    for (long long t = tid; t < r1 - r0; t += kThreads) rowacc[t] = 0.0;
+    for (long long c0 = 0; c0 < n; c0 += P.r_chunk) {
+        const long long cw = min((long long)P.r_chunk, n - c0);
+        __syncthreads();
+        if (UPDATE)
+            for (long long t = tid; t < cw; t += kThreads) zs[t] = __ldg(P.z + c0 + t);
+        __syncthreads();
+        for (long long l = r0 + warp; l < r1; l += kWarps) {
+            double f = 0.0;
+            if (UPDATE) {
+                const double gl = P.G ? __ldg(P.G + sel * m + l) : __ldg(P.g + l);
+                f = __dmul_rn(coef, gl);  // solver.hpp:296
+            }
+            double* row = P.R + l * n + c0;
+            double acc = 0.0;
+            if (VEC2) {
+                double2* r2 = reinterpret_cast<double2*>(row);
+                const double2* z2 = reinterpret_cast<const double2*>(zs);
+                const long long h = cw >> 1;
+#pragma unroll 8
+                for (long long k = lane; k < h; k += 32) {
+                    double2 r = __ldcs(r2 + k);
+                    if (UPDATE) {
+                        const double2 zz = z2[k];
+                        r.x = __dsub_rn(r.x, __dmul_rn(f, zz.x));  // solver.hpp:300
+                        r.y = __dsub_rn(r.y, __dmul_rn(f, zz.y));
+                        __stcs(r2 + k, r);
+                    }
+                    acc += r.x * r.x;  // solver.hpp:301 (tree order here)
+                    acc += r.y * r.y;
+                }
+            } else {
+#pragma unroll 4
+                for (long long k = lane; k < cw; k += 32) {
+                    double r = row[k];
+                    if (UPDATE) {
+                        r = __dsub_rn(r, __dmul_rn(f, zs[k]));
+                        row[k] = r;
+                    }
+                    acc += r * r;
+                }
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) rowacc[l - r0] += acc;
+        }
+    }
+    __syncthreads();
+    double bsum = 0.0, bmax = -INFINITY;
+    long long barg = LLONG_MAX;
+    for (long long t = tid; t < r1 - r0; t += kThreads) {
+        const long long l = r0 + t;
+        const double rs = rowacc[t];
+        P.r_sq[l] = rs;
+        bsum += rs;
+        const double as = P.a_sq[l];
+        if (as > 0.0) maxidx_merge(bmax, barg, __ddiv_rn(rs, as), P.row0 + l);
+    }
+    bsum = block_sum(bsum, redv);
+    block_maxidx(bmax, barg, redv, redi);
+    if (tid == 0) {
+        P.rrec[blockIdx.x] = RowRecord{bsum, bmax, barg, 0.0};
+        __threadfence();
+        last = atomicAdd(&st->cnt_r, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    // ---- last CTA: reduce the records (fixed order), finalize the iteration ----
+    __threadfence();
+    double s = 0.0, mx = -INFINITY;
+    long long ax = LLONG_MAX;
+    for (int k = tid; k < (int)gridDim.x; k += kThreads) {
+        const double* rp = reinterpret_cast<const double*>(P.rrec + k);
+        const RowRecord rc{__ldcg(rp), __ldcg(rp + 1), __ldcg(reinterpret_cast<const long long*>(rp + 2)), 0.0};
+        s += rc.sum;
+        maxidx_merge(mx, ax, rc.max_ratio, rc.argmax);
+    }
+    s = block_sum(s, redv);
+    block_maxidx(mx, ax, redv, redi);
+    const int mode = UPDATE ? st->fin_mode : FIN_NORMS;
+    __syncthreads();
+    if (tid == 0) {
+        st->cnt_r = 0u;
+        st->r_fro_sq = s;
+        st->max_ratio = mx;
+        st->argmax = ax;
+        st->sel_valid = 0;
+        const double cf = P.c_fro > 0.0 ? P.c_fro : 1.0;
+        const double rel = sqrt(s > 0.0 ? s : 0.0) / cf;
+        if (mode != FIN_NORMS && !isfinite(s)) {  // solver.hpp:306-307
+            st->status = ST_ERROR;
+            st->err_code = 4;
+            st->err_k = st->k;
+            st->err_val = sqrt(fabs(s));
+        } else if (mode == FIN_ITERATION) {
+            const unsigned long long k = st->k;
+            const double metric = P.stop_kind == 0 ? st->err_sq / P.ref_sq : rel;
+            const unsigned long long slot = k - st->k0;
+            if (slot < P.trace_cap) {
+                P.trace_row[slot] = st->sel;
+                P.trace_metric[slot] = metric;
+                P.trace_rel[slot] = rel;
+            }
+            st->k = k + 1;
+            st->metric = metric;
+            if (st->run_mode && metric <= P.tol) st->status = ST_PAUSE;        // :351
+            else if (st->run_mode && !(s > 0.0)) st->status = ST_ZERO;         // :347
+        } else {
+            st->metric = P.stop_kind == 0 ? st->err_sq / P.ref_sq : rel;
+        }
+    }
+    __syncthreads();
+    if (mode == FIN_ITERATION && st->status == ST_RUN && st->k < st->k_limit)
+        finish_select(P, st, sh);
+}
+
+// K3 standalone: (re)select with the configured rule (consume=0: speculative,
+// snapshot kept) or run a public select_*(θ) that consumes the stream (consume=1).
+__global__ void __launch_bounds__(kThreads) k_select(Params P, int method, double theta,
+                                                    int consume) {
+    __shared__ SelShared sh;
+    DevState* st = P.st;
+    if (!consume) {
+        finish_select(P, st, sh);
+        return;
+    }
+    long long row = 0;
+    if (threadIdx.x == 0) sh.err = 0;
+    __syncthreads();
+    const int err = select_rows(P, st, method, theta, &row, sh);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st->sel_valid = 0;
+        st->q_row = row;
+        if (err) {
+            st->status = ST_ERROR;
+            st->err_code = err;
+        }
+    }
+}
+
+// greedy_threshold / greedy_index_set / max_residual_ratio queries (no RNG use)
+__global__ void __launch_bounds__(kThreads) k_query(Params P, double theta, int want_set) {
+    __shared__ double red[kWarps];
+    DevState* st = P.st;
+    const double r_fro = st->r_fro_sq;
+    const long long argmax = st->argmax;
+    const bool zero = !(r_fro > 0.0);
+    const double zeta = zero ? 0.0
+                             : __dadd_rn(__dmul_rn(theta, __ddiv_rn(st->max_ratio, r_fro)),
+                                         __ddiv_rn(__dsub_rn(1.0, theta), P.a_fro_sq));
+    long long cnt = 0;
+    if (want_set && !zero) {
+        for (long long i = threadIdx.x; i < P.m; i += kThreads) {
+            const double as = P.a_sq[i];
+            const int mem = as > 0.0 &&
+                            (i == argmax || P.r_sq[i] >= __dmul_rn(__dmul_rn(zeta, as), r_fro));
+            P.member_flags[i] = mem;
+            cnt += mem;
+        }
+    }
+    const double c = block_sum((double)cnt, red);
+    if (threadIdx.x == 0) {
+        st->q_zeta = zeta;
+        st->q_row = argmax;
+        st->q_count = (long long)c;
+        if (zero) {
+            st->status = ST_ERROR;
+            st->err_code = 2;
+        }
+    }
+}
+
+__global__ void k_rollback(DevState* st) {
+    if (st->sel_valid) {
+        for (int k = 0; k < 4; ++k) st->rng[k] = st->rng_snap[k];
+        st->cyclic_pos = st->cyclic_snap;
+        st->skipped_zero_rows = st->skipped_snap;
+        st->sel_valid = 0;
+    }
+}
+
+// fresh ‖X − X_ref‖² (solver.hpp:188, :414, :475) and the all-finite check (:428)
+__global__ void __launch_bounds__(kThreads) k_err_fresh(Params P) {
+    __shared__ double red[kWarps];
+    __shared__ bool last;
+    DevState* st = P.st;
+    const long long total = P.p * P.q;
+    double acc = 0.0, bad = 0.0;
+    for (long long e = (long long)blockIdx.x * kThreads + threadIdx.x; e < total;
+         e += (long long)gridDim.x * kThreads) {
+        const double x = P.X[e];
+        if (!isfinite(x)) bad += 1.0;
+        if (P.Xref) {
+            const double d = x - P.Xref[e];
+            acc += d * d;
+        }
+    }
+    acc = block_sum(acc, red);
+    bad = block_sum(bad, red);
+    if (threadIdx.x == 0) {
+        P.xpart[2 * blockIdx.x] = acc;
+        P.xpart[2 * blockIdx.x + 1] = bad;
+        __threadfence();
+        last = atomicAdd(&st->cnt_red, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s = 0.0, b = 0.0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += kThreads) {
+        s += __ldcg(P.xpart + 2 * k);
+        b += __ldcg(P.xpart + 2 * k + 1);
+    }
+    s = block_sum(s, red);
+    b = block_sum(b, red);
+    if (threadIdx.x == 0) {
+        st->err_sq = s;
+        st->x_finite = b == 0.0;
+        st->cnt_red = 0u;
+        if (P.stop_kind == 0) st->metric = s / P.ref_sq;
+    }
+}
+
+// ---- power iteration helpers (decomp.hpp:207-239 on the device) ----
+__global__ void __launch_bounds__(kThreads) k_rowdot(const double* M, long long rows,
+                                                    long long cols, const double* v, double* out) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const bool v2 = (cols & 1) == 0;
+    for (long long r = warp; r < rows; r += nw) {
+        const double a = warp_dot(M + r * cols, v, cols, lane, v2);
+        if (lane == 0) out[r] = a;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_coldot(const double* M, long long rows,
+                                                    long long cols, const double* v, double* out,
+                                                    double* part, unsigned int* cnt, int nslab,
+                                                    int nj, int jrows) {
+    __shared__ bool last;
+    const int slab = blockIdx.x % nslab, jc = blockIdx.x / nslab;
+    const long long j0 = (long long)jc * jrows, j1 = min(rows, j0 + jrows);
+    const long long c = (long long)slab * kThreads + threadIdx.x;
+    double a = 0.0;
+    if (c < cols)
+        for (long long j = j0; j < j1; ++j) a += __ldg(v + j) * __ldg(M + j * cols + c);
+    if (nj == 1) {
+        if (c < cols) out[c] = a;
+        return;
+    }
+    if (c < cols) part[(long long)jc * cols + c] = a;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cnt + slab, 1u) == (unsigned)(nj - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (c < cols) {
+        double s = 0.0;
+        for (int k = 0; k < nj; ++k) s += __ldcg(part + (long long)k * cols + c);
+        out[c] = s;
+    }
+    if (threadIdx.x == 0) cnt[slab] = 0u;
+}
+
+// rayleigh = v·w, wn = ‖w‖, v_out = w / wn   (decomp.hpp:227-231)
+__global__ void __launch_bounds__(1024) k_power_step(const double* v, const double* w,
+                                                     double* v_out, long long dim, double* out2) {
+    __shared__ double red[32];
+    __shared__ double wn_s;
+    double a = 0.0, b = 0.0;
+    for (long long i = threadIdx.x; i < dim; i += blockDim.x) {
+        a += v[i] * w[i];
+        b += w[i] * w[i];
+    }
+    a = block_sum(a, red);
+    b = block_sum(b, red);
+    if (threadIdx.x == 0) {
+        wn_s = sqrt(b);
+        out2[0] = a;
+        out2[1] = wn_s;
+    }
+    __syncthreads();
+    const double wn = wn_s;
+    if (wn != 0.0)
+        for (long long i = threadIdx.x; i < dim; i += blockDim.x) v_out[i] = w[i] / wn;
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// host → device control writes for a batch (one launch instead of several memcpys)
+__global__ void k_ctrl(DevState* st, unsigned long long k0, unsigned long long k_limit,
+                       int fin_mode, int run_mode, int reset_status) {
+    st->k0 = k0;
+    st->k_limit = k_limit;
+    st->fin_mode = fin_mode;
+    st->run_mode = run_mode;
+    if (reset_status) {
+        st->status = ST_RUN;
+        st->err_code = 0;
+    }
+}
+
+__global__ void k_set_sel(DevState* st, long long sel, double coef) {
+    st->sel = sel;
+    st->coef = coef;
+    st->sel_valid = 0;
+}
+
+// per-CTA Σ v² partials (deterministic), reduced by k_reduce_parts (axb_gemm.cu)
+__global__ void __launch_bounds__(kThreads) k_sumsq(const double* v, long long n, double* part) {
+    __shared__ double red[kWarps];
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n;
+         i += (long long)gridDim.x * kThreads) {
+        const double x = v[i];
+        acc += x * x;
+    }
+    acc = block_sum(acc, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// ‖A_i‖² per row with the reference's sequential order and rounding
+// (matrix.hpp:300-306 via RowView::sq_norm :199-203): one thread per row.
+__global__ void k_row_sq_seq(const double* A, long long m, long long p, double* out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double* row = A + i * p;
+        double s = 0.0;
+        for (long long j = 0; j < p; ++j) {
+            const double v = row[j];
+            s = __dadd_rn(s, __dmul_rn(v, v));
+        }
+        out[i] = s;
+    }
+}
+
+// a_fro_sq and the RBK inclusive cumsum, sequential as solver.hpp:157-166
+__global__ void k_cumsum_seq(const double* a_sq, long long m, double* cum, double* total) {
+    double c = 0.0;
+    for (long long i = 0; i < m; ++i) {
+        c = __dadd_rn(c, a_sq[i]);
+        cum[i] = c;
+    }
+    *total = c;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------
+// launchers
+
+void launch_yg(const Params& P, cudaStream_t s, bool with_g) {
+    k_yg<<<P.yg_grid, kThreads, 0, s>>>(P, with_g ? 1 : 0);
+}
+
+void launch_zx(const Params& P, cudaStream_t s) {
+    k_zx<<<P.z_nslab * P.z_nj + P.x_ctas, kThreads, 0, s>>>(P);
+}
+
+void launch_r(const Params& P, cudaStream_t s, bool update) {
+    const size_t smem = sizeof(double) * (size_t)(P.r_chunk + P.r_rows_per_cta);
+    const bool v2 = (P.n & 1) == 0;
+    if (update) {
+        if (v2) k_r<true, true><<<P.r_grid, kThreads, smem, s>>>(P);
+        else k_r<true, false><<<P.r_grid, kThreads, smem, s>>>(P);
+    } else {
+        if (v2) k_r<false, true><<<P.r_grid, kThreads, smem, s>>>(P);
+        else k_r<false, false><<<P.r_grid, kThreads, smem, s>>>(P);
+    }
+}
+
+void launch_select(const Params& P, cudaStream_t s, int method, double theta, int consume) {
+    k_select<<<1, kThreads, 0, s>>>(P, method, theta, consume);
+}
+
+void launch_query(const Params& P, cudaStream_t s, double theta, int want_set) {
+    k_query<<<1, kThreads, 0, s>>>(P, theta, want_set);
+}
+
+void launch_rollback(const Params& P, cudaStream_t s) { k_rollback<<<1, 1, 0, s>>>(P.st); }
+
+void launch_err_fresh(const Params& P, cudaStream_t s) {
+    long long total = P.p * P.q;
+    int grid = (int)std::min<long long>(296, (total + kThreads * 4 - 1) / (kThreads * 4));
+    if (grid < 1) grid = 1;
+    k_err_fresh<<<grid, kThreads, 0, s>>>(P);
+}
+
+void launch_rowdot(const double* M, long long rows, long long cols, const double* v, double* out,
+                   cudaStream_t s) {
+    int grid = (int)std::min<long long>(148 * 8, (rows + kWarps - 1) / kWarps);
+    k_rowdot<<<grid, kThreads, 0, s>>>(M, rows, cols, v, out);
+}
+
+void launch_coldot(const double* M, long long rows, long long cols, const double* v, double* out,
+                   double* part, unsigned int* cnt, int nj, int jrows, cudaStream_t s) {
+    const int nslab = (int)((cols + kThreads - 1) / kThreads);
+    k_coldot<<<nslab * nj, kThreads, 0, s>>>(M, rows, cols, v, out, part, cnt, nslab, nj, jrows);
+}
+
+void launch_power_step(const double* v_in, const double* w, double* v_out, long long dim,
+                       double* out2, cudaStream_t s) {
+    k_power_step<<<1, 1024, 0, s>>>(v_in, w, v_out, dim, out2);
+}
+
+void launch_ctrl(DevState* st, unsigned long long k0, unsigned long long k_limit, int fin_mode,
+                 int run_mode, int reset_status, cudaStream_t s) {
+    k_ctrl<<<1, 1, 0, s>>>(st, k0, k_limit, fin_mode, run_mode, reset_status);
+}
+
+void launch_set_sel(DevState* st, long long sel, double coef, cudaStream_t s) {
+    k_set_sel<<<1, 1, 0, s>>>(st, sel, coef);
+}
+
+int sumsq_parts(long long n) { return (int)std::max<long long>(1, std::min<long long>(1184, (n + 1023) / 1024)); }
+
+void launch_sumsq(const double* v, long long n, double* part, cudaStream_t s) {
+    k_sumsq<<<sumsq_parts(n), kThreads, 0, s>>>(v, n, part);
+}
+
+void launch_row_sq_seq(const double* A, long long m, long long p, double* out, cudaStream_t s) {
+    int grid = (int)std::max<long long>(1, std::min<long long>(148 * 8, (m + 127) / 128));
+    k_row_sq_seq<<<grid, 128, 0, s>>>(A, m, p, out);
+}
+
+void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* total, cudaStream_t s) {
+    k_cumsum_seq<<<1, 1, 0, s>>>(a_sq, m, cum, total);
+}
+
+void launch_fill(double* p, long long n, double v, cudaStream_t s) {
+    int grid = (int)std::min<long long>(1184, (n + 255) / 256);
+    if (grid < 1) grid = 1;
+    k_fill<<<grid, 256, 0, s>>>(p, n, v);
+}
+
+}  // namespace axb_dev

@@ -1,0 +1,996 @@
+// axb_solver.cu — host C++ engine behind the C-ABI (include/axb_b200.h).
+//
+// Mirrors axb::Solver<DenseMatrix,DenseMatrix> (solver.hpp:143-515): the same
+// constructor checks and initialisation order (:146-192), the same run() loop
+// with its confirm/resync and refresh-checkpoint schedule (:337-372), the same
+// public selection and metric methods.  The iteration itself runs on the
+// device (axb_iter.cu), batched into CUDA graphs; the host only intervenes at
+// batch boundaries, refresh checkpoints and stop confirmations.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/axb_b200.h"
+#include "axb_device.cuh"
+
+using namespace axb_dev;
+
+namespace {
+
+struct AxbError {
+    int code;
+    std::string msg;
+    uint64_t k = 0;
+    double val = 0.0;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw AxbError{code, buf};
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation)
+            fail(AXB_CAPACITY_ERROR, "%s: out of device memory (%s)", what, cudaGetErrorString(e));
+        fail(AXB_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
+    }
+}
+
+// ---- host restatement of decomp.hpp:207-239 (bitwise α for small B) ----
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+std::vector<double> power_start(size_t dim) {
+    std::vector<double> v(dim);
+    uint64_t h = 0x6b8f9a37c1d2e4f5ULL;
+    for (size_t i = 0; i < dim; ++i) {
+        h = splitmix64(h);
+        v[i] = 1.0 + 1e-3 * (static_cast<double>(h >> 11) * 0x1.0p-53 - 0.5);
+    }
+    double nrm = 0.0;
+    for (size_t i = 0; i < dim; ++i) nrm = nrm + v[i] * v[i];
+    nrm = std::sqrt(nrm);
+    for (double& x : v) x /= nrm;
+    return v;
+}
+
+double spectral_norm_host(const std::vector<double>& b, size_t rows, size_t cols, double tol,
+                          size_t max_iter) {
+    double fro = 0.0;
+    for (double v : b) fro += v * v;
+    if (fro == 0.0) fail(AXB_DOMAIN_ERROR, "spectral_norm: zero matrix");
+    const bool use_mtm = cols <= rows;
+    const size_t dim = use_mtm ? cols : rows, other = use_mtm ? rows : cols;
+    std::vector<double> v = power_start(dim), w(dim), t(other);
+    auto matvec = [&](const double* x, double* y) {  // matrix.hpp:400-410
+        for (size_t i = 0; i < rows; ++i) {
+            const double* ri = b.data() + i * cols;
+            double s = 0.0;
+            for (size_t j = 0; j < cols; ++j) s += ri[j] * x[j];
+            y[i] = s;
+        }
+    };
+    auto matvec_t = [&](const double* x, double* y) {  // matrix.hpp:420-430
+        for (size_t j = 0; j < cols; ++j) y[j] = 0.0;
+        for (size_t i = 0; i < rows; ++i) {
+            const double xv = x[i];
+            if (xv == 0.0) continue;
+            const double* ri = b.data() + i * cols;
+            for (size_t j = 0; j < cols; ++j) y[j] += xv * ri[j];
+        }
+    };
+    double lambda = 0.0;
+    for (size_t it = 0; it < max_iter; ++it) {
+        if (use_mtm) {
+            matvec(v.data(), t.data());
+            matvec_t(t.data(), w.data());
+        } else {
+            matvec_t(v.data(), t.data());
+            matvec(t.data(), w.data());
+        }
+        double rayleigh = 0.0, wn = 0.0;
+        for (size_t i = 0; i < dim; ++i) rayleigh = rayleigh + v[i] * w[i];
+        for (size_t i = 0; i < dim; ++i) wn = wn + w[i] * w[i];
+        wn = std::sqrt(wn);
+        if (wn == 0.0) return 0.0;
+        for (size_t i = 0; i < dim; ++i) v[i] = w[i] / wn;
+        if (it > 0 && std::abs(rayleigh - lambda) <= 0.5 * tol * std::abs(rayleigh))
+            return std::sqrt(rayleigh);
+        lambda = rayleigh;
+    }
+    AxbError e{AXB_CONVERGENCE_ERROR, "spectral_norm: power iteration did not converge"};
+    e.val = std::sqrt(std::abs(lambda));
+    throw e;
+}
+
+bool trace_point_due(uint64_t k) { return k < 10000 || k % 10 == 0; }  // solver.hpp:136
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count, const char* what) {
+        n = count;
+        ck(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)), what);
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+}  // namespace
+
+struct axb_solver {
+    uint64_t m = 0, p = 0, q = 0, n = 0;
+    axb_config cfg{};
+    axb_options opt{};
+    cudaStream_t stream = nullptr;
+    DevBuf<double> A, B, C, R, X, Xref, a_sq, rbk_cum, r_sq, G, g, y, z, zpart, xpart, T,
+        gemm_sq, gemm_diff, scal, tr_metric, tr_rel, sq_part;
+    DevBuf<unsigned int> zcnt;
+    DevBuf<RowRecord> rrec;
+    DevBuf<long long> tr_row;
+    DevBuf<int> flags;
+    DevBuf<DevState> st;
+    DevState* hs = nullptr;  // pinned host mirror
+    std::vector<double> a_sq_h;
+    double a_fro_sq = 0.0, b_spec = 0.0, alpha = 0.0, c_fro = 0.0, ref_sq = 0.0;
+    bool alpha_outside = false, gram_cached = false;
+    uint64_t k = 0;
+    bool sel_valid = false;
+    Params P{};
+    cudaGraphExec_t graph = nullptr;
+    int graph_iters = 32;
+    uint64_t trace_cap = 4096;
+    long long* h_trace_row = nullptr;
+    double* h_trace_metric = nullptr;
+    double* h_trace_rel = nullptr;
+    std::string err;
+    // timing
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool profiling = false;
+    std::vector<cudaEvent_t> prof_ev;
+    double loop_ms = 0.0, k2_ms = 0.0;
+    uint64_t k2_launches = 0, kernel_launches = 0;
+
+    ~axb_solver() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (hs) cudaFreeHost(hs);
+        if (h_trace_row) cudaFreeHost(h_trace_row);
+        if (h_trace_metric) cudaFreeHost(h_trace_metric);
+        if (h_trace_rel) cudaFreeHost(h_trace_rel);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        for (auto e : prof_ev) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    // ---------------------------------------------------------------- utils
+    void sync(const char* what) { ck(cudaStreamSynchronize(stream), what); }
+
+    void pull_state() {
+        ck(cudaMemcpyAsync(hs, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, stream), "state");
+        sync("state sync");
+    }
+
+    [[noreturn]] void raise_state() {
+        const int code = hs->err_code ? hs->err_code : AXB_CUDA_ERROR;
+        AxbError e{code, ""};
+        char buf[256];
+        switch (code) {
+            case AXB_DIVERGENCE_ERROR:
+                snprintf(buf, sizeof buf, "divergence at iteration %llu, residual frobenius norm %f",
+                         (unsigned long long)hs->err_k, hs->err_val);
+                e.k = hs->err_k;
+                e.val = hs->err_val;
+                break;
+            case AXB_DOMAIN_ERROR:
+                if (cfg.method == AXB_GRBK || cfg.method == AXB_RGRBK)
+                    snprintf(buf, sizeof buf,
+                             !(hs->r_fro_sq > 0.0)
+                                 ? "greedy threshold: zero residual"
+                                 : "greedy selection: residual mass sits on zero rows of A only; "
+                                   "the system is inconsistent");
+                else if (cfg.method == AXB_BK)
+                    snprintf(buf, sizeof buf, "select_cyclic: no nonzero row");
+                else
+                    snprintf(buf, sizeof buf, "categorical: no positive weight");
+                break;
+            default: snprintf(buf, sizeof buf, "device error %d", code);
+        }
+        e.msg = buf;
+        // leave the device state runnable for a caller that catches and continues
+        launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 1, stream);
+        sync("reset");
+        throw e;
+    }
+
+    double reduce_sumsq(const double* v, uint64_t len) {
+        launch_sumsq(v, (long long)len, sq_part.p, stream);
+        launch_reduce_parts(sq_part.p, sumsq_parts((long long)len), scal.p, stream);
+        double out = 0.0;
+        ck(cudaMemcpyAsync(&out, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "sumsq");
+        sync("sumsq");
+        return out;
+    }
+
+    // ---------------------------------------------------------------- init
+    void create(const double* A_in, const double* B_in, const double* C_in, const double* X0_in) {
+        // Method::validate (solver.hpp:30-38)
+        if (cfg.method < AXB_BK || cfg.method > AXB_MWRBK) fail(AXB_CONFIG_ERROR, "unknown method");
+        if (cfg.method == AXB_RGRBK) {
+            if (!cfg.has_theta) fail(AXB_CONFIG_ERROR, "rgrbk requires theta");
+            if (!(cfg.theta > 0.0 && cfg.theta < 1.0))
+                fail(AXB_CONFIG_ERROR, "theta must lie strictly in (0, 1)");
+        } else if (cfg.has_theta) {
+            fail(AXB_CONFIG_ERROR, "theta is only valid for rgrbk");
+        }
+        if (cfg.alpha_rule < AXB_ALPHA_SAFE || cfg.alpha_rule > AXB_ALPHA_FIXED)
+            fail(AXB_CONFIG_ERROR, "unknown alpha rule");
+        if (m == 0 || p == 0) fail(AXB_SHAPE_ERROR, "row_sq_norms: empty matrix");
+        if (q == 0 || n == 0) fail(AXB_SHAPE_ERROR, "spectral_norm: empty matrix");
+        if (opt.nccl_comm || opt.world_size > 1)
+            fail(AXB_CONFIG_ERROR, "row sharding needs the sharded build (axb_shard)");
+        if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN && !cfg.reference)
+            fail(AXB_CONFIG_ERROR, "solution_rrn stopping needs a reference solution");
+
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            fail(AXB_CUDA_ERROR, "no CUDA device visible (this build has no CPU fallback)");
+        ck(cudaSetDevice(opt.device), "cudaSetDevice");
+        cudaDeviceProp prop{};
+        ck(cudaGetDeviceProperties(&prop, opt.device), "cudaGetDeviceProperties");
+        if (prop.major < 10)
+            fail(AXB_CUDA_ERROR, "device %d is sm_%d%d; the kernels are built for sm_100a",
+                 opt.device, prop.major, prop.minor);
+        ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreate(&ev0), "event");
+        ck(cudaEventCreate(&ev1), "event");
+        ck(cudaMallocHost(&hs, sizeof(DevState)), "pinned state");
+        if (opt.graph_iters > 0) graph_iters = opt.graph_iters;
+        ck(cudaMallocHost(&h_trace_row, sizeof(long long) * trace_cap), "pinned trace");
+        ck(cudaMallocHost(&h_trace_metric, sizeof(double) * trace_cap), "pinned trace");
+        ck(cudaMallocHost(&h_trace_rel, sizeof(double) * trace_cap), "pinned trace");
+
+        const cudaMemcpyKind kind =
+            opt.inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        A.alloc(m * p, "A");
+        B.alloc(q * n, "B");
+        C.alloc(m * n, "C");
+        R.alloc(m * n, "R");
+        X.alloc(p * q, "X");
+        ck(cudaMemcpyAsync(A.p, A_in, sizeof(double) * m * p, kind, stream), "copy A");
+        ck(cudaMemcpyAsync(B.p, B_in, sizeof(double) * q * n, kind, stream), "copy B");
+        ck(cudaMemcpyAsync(C.p, C_in, sizeof(double) * m * n, kind, stream), "copy C");
+        if (X0_in)
+            ck(cudaMemcpyAsync(X.p, X0_in, sizeof(double) * p * q, kind, stream), "copy X0");
+        else
+            ck(cudaMemsetAsync(X.p, 0, sizeof(double) * p * q, stream), "zero X0");
+        if (cfg.reference) {
+            Xref.alloc(p * q, "Xref");
+            ck(cudaMemcpyAsync(Xref.p, cfg.reference, sizeof(double) * p * q, kind, stream),
+               "copy reference");
+        }
+        a_sq.alloc(m, "a_sq");
+        rbk_cum.alloc(m, "rbk_cum");
+        r_sq.alloc(m, "r_sq");
+        scal.alloc(4, "scalars");
+        sq_part.alloc(sumsq_parts((long long)std::max({m * n, q * n, p * q, m * p})), "parts");
+
+        // a_sq_ = row_sq_norms(A); a_fro_sq_; rbk_cumsum_ (solver.hpp:156-166), sequential
+        launch_row_sq_seq(A.p, (long long)m, (long long)p, a_sq.p, stream);
+        launch_cumsum_seq(a_sq.p, (long long)m, rbk_cum.p, scal.p, stream);
+        a_sq_h.resize(m);
+        ck(cudaMemcpyAsync(a_sq_h.data(), a_sq.p, sizeof(double) * m, cudaMemcpyDeviceToHost,
+                           stream), "a_sq");
+        ck(cudaMemcpyAsync(&a_fro_sq, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream),
+           "a_fro");
+        sync("init norms");
+        if (a_fro_sq == 0.0) fail(AXB_DOMAIN_ERROR, "solve: A is the zero matrix");
+
+        // b_spec_ = spectral_norm(B); resolve_alpha() (solver.hpp:168-169, :439-456)
+        if (opt.alpha_override > 0.0) {
+            alpha = opt.alpha_override;
+            b_spec = 0.0;
+        } else {
+            const size_t cap = opt.spectral_max_iter ? opt.spectral_max_iter : 5000;
+            bool on_dev = opt.spectral_on_device == 1 ||
+                          (opt.spectral_on_device < 0 && q * n > (1ull << 20));
+            if (on_dev) {
+                b_spec = spectral_norm_device(1e-10, cap);
+            } else {
+                std::vector<double> bh(q * n);
+                ck(cudaMemcpyAsync(bh.data(), B.p, sizeof(double) * q * n, cudaMemcpyDeviceToHost,
+                                   stream), "B to host");
+                sync("B to host");
+                b_spec = spectral_norm_host(bh, q, n, 1e-10, cap);
+            }
+            const double b2 = b_spec * b_spec;
+            switch (cfg.alpha_rule) {
+                case AXB_ALPHA_SAFE: alpha = 1.0 / b2; break;
+                case AXB_ALPHA_PAPER:
+                    alpha = 1.0 / b_spec;
+                    alpha_outside = !(alpha < 2.0 / b2);
+                    break;
+                default:
+                    alpha = cfg.alpha_value;
+                    if (!(alpha > 0.0) || !(alpha < 2.0 / b2))
+                        fail(AXB_CONFIG_ERROR, "fixed alpha %f outside (0, 2/‖B‖₂²)", alpha);
+            }
+        }
+
+        // gram_ = gram_mmt(A) (solver.hpp:171): cached when it fits in HBM
+        size_t free_b = 0, total_b = 0;
+        ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
+        const double gbytes = 8.0 * (double)m * (double)m;
+        gram_cached = opt.cache_gram == 1 ||
+                      (opt.cache_gram < 0 && gbytes < 0.45 * (double)free_b &&
+                       gbytes <= 48e9);
+        T.alloc(m * q, "T");
+        const int gparts = gemm_num_ctas((long long)m, (long long)std::max(n, m));
+        gemm_sq.alloc(gparts, "gemm parts");
+        gemm_diff.alloc(gparts, "gemm parts");
+        if (gram_cached) {
+            G.alloc(m * m, "G");
+            GemmArgs ga{};
+            ga.M = m; ga.N = m; ga.K = p;
+            ga.A = A.p; ga.lda = p;
+            ga.B = A.p; ga.ldb = p; ga.b_trans = 1;
+            ga.D = G.p; ga.ldd = m;
+            ga.store = 1;
+            launch_gemm(ga, stream);
+        } else {
+            g.alloc(m, "g");
+        }
+
+        // r_ = C − (A·X0)·B (solver.hpp:173)
+        if (X0_in) {
+            exact_residual_into(R.p, nullptr, nullptr, true);
+        } else {
+            ck(cudaMemcpyAsync(R.p, C.p, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, stream),
+               "R = C");
+        }
+        c_fro = std::sqrt(reduce_sumsq(C.p, m * n));  // :179
+        if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) {   // :180-189
+            ref_sq = reduce_sumsq(Xref.p, p * q);
+            if (ref_sq == 0.0) fail(AXB_DOMAIN_ERROR, "solution_rrn: zero reference");
+        }
+
+        // iteration buffers and launch geometry
+        y.alloc(q, "y");
+        z.alloc(n, "z");
+        P.m = (long long)m; P.p = (long long)p; P.q = (long long)q; P.n = (long long)n;
+        P.row0 = 0;
+        P.m_global = (long long)m;
+        const int target = 148 * 4;
+        int rgrid = (int)std::min<uint64_t>((uint64_t)target, std::max<uint64_t>(1, (m + 7) / 8));
+        P.r_rows_per_cta = (int)((m + rgrid - 1) / rgrid);
+        P.r_grid = (int)((m + P.r_rows_per_cta - 1) / P.r_rows_per_cta);
+        P.r_chunk = (int)std::min<uint64_t>(n, 4096);
+        if (P.r_chunk & 1) P.r_chunk += (n > (uint64_t)P.r_chunk) ? 1 : 0;
+        const uint64_t items = q + (gram_cached ? 0 : m);
+        P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(148 * 8, (items + 7) / 8));
+        P.z_nslab = (int)((n + 511) / 512);
+        int nj = (int)std::max<uint64_t>(1, std::min<uint64_t>((target + P.z_nslab - 1) / P.z_nslab,
+                                                                (q + 7) / 8));
+        P.z_jrows = (int)((q + nj - 1) / nj);
+        P.z_nj = (int)((q + P.z_jrows - 1) / P.z_jrows);
+        P.x_ctas = (int)std::max<uint64_t>(1, std::min<uint64_t>(296, (p * q + 1023) / 1024));
+        zpart.alloc((size_t)P.z_nj * n, "zpart");
+        zcnt.alloc(P.z_nslab, "zcnt");
+        ck(cudaMemsetAsync(zcnt.p, 0, sizeof(unsigned) * P.z_nslab, stream), "zcnt");
+        xpart.alloc(2 * 1184, "xpart");
+        rrec.alloc(P.r_grid, "rrec");
+        tr_row.alloc(trace_cap, "trace");
+        tr_metric.alloc(trace_cap, "trace");
+        tr_rel.alloc(trace_cap, "trace");
+        flags.alloc(m, "flags");
+        st.alloc(1, "state");
+
+        P.A = A.p; P.B = B.p; P.R = R.p; P.X = X.p; P.Xref = Xref.p;
+        P.a_sq = a_sq.p; P.rbk_cum = rbk_cum.p; P.r_sq = r_sq.p;
+        P.G = gram_cached ? G.p : nullptr;
+        P.g = g.p; P.y = y.p; P.z = z.p; P.zpart = zpart.p; P.zcnt = zcnt.p; P.xpart = xpart.p;
+        P.rrec = rrec.p; P.trace_row = tr_row.p; P.trace_metric = tr_metric.p;
+        P.trace_rel = tr_rel.p; P.trace_cap = trace_cap; P.member_flags = flags.p; P.st = st.p;
+        P.alpha = alpha;
+        P.theta = cfg.method == AXB_RGRBK ? cfg.theta : 0.5;
+        P.a_fro_sq = a_fro_sq;
+        P.tol = cfg.tol;
+        P.ref_sq = ref_sq > 0.0 ? ref_sq : 1.0;
+        P.c_fro = c_fro;
+        P.method = cfg.method;
+        P.stop_kind = cfg.stop_kind;
+        P.tie_guard = opt.tie_guard ? 1 : 0;
+        P.vec2 = (n % 2) == 0;
+
+        // DevState: RngStream(cfg.seed) (rng.hpp:20-25), k = 0
+        DevState s0{};
+        uint64_t x = cfg.seed;
+        for (int i = 0; i < 4; ++i) {
+            x += 0x9e3779b97f4a7c15ULL;
+            uint64_t zz = x;
+            zz = (zz ^ (zz >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            zz = (zz ^ (zz >> 27)) * 0x94d049bb133111ebULL;
+            s0.rng[i] = zz ^ (zz >> 31);
+        }
+        if (!s0.rng[0] && !s0.rng[1] && !s0.rng[2] && !s0.rng[3]) s0.rng[0] = 1;
+        s0.status = ST_RUN;
+        s0.fin_mode = FIN_ITERATION;
+        s0.argmax = -1;
+        *hs = s0;
+        ck(cudaMemcpyAsync(st.p, hs, sizeof(DevState), cudaMemcpyHostToDevice, stream), "state");
+        adopt_norms();
+        sync("init");
+        pull_state();
+    }
+
+    double spectral_norm_device(double tol, size_t max_iter) {
+        if (reduce_sumsq(B.p, q * n) == 0.0) fail(AXB_DOMAIN_ERROR, "spectral_norm: zero matrix");
+        const bool use_mtm = n <= q;
+        const size_t dim = use_mtm ? n : q, other = use_mtm ? q : n;
+        std::vector<double> v0 = power_start(dim);
+        DevBuf<double> v, vn, w, t, part, out2;
+        DevBuf<unsigned int> cnt;
+        v.alloc(dim, "power v");
+        vn.alloc(dim, "power v");
+        w.alloc(dim, "power w");
+        t.alloc(other, "power t");
+        out2.alloc(2, "power out");
+        const int nslab = (int)((n + 255) / 256);
+        const int nj = (int)std::max<size_t>(1, std::min<size_t>((592 + nslab - 1) / nslab, (q + 7) / 8));
+        const int jrows = (int)((q + nj - 1) / nj);
+        const int nj2 = (int)((q + jrows - 1) / jrows);
+        part.alloc((size_t)nj2 * n, "power part");
+        cnt.alloc(nslab, "power cnt");
+        ck(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned) * nslab, stream), "cnt");
+        ck(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * dim, cudaMemcpyHostToDevice, stream),
+           "v0");
+        double lambda = 0.0, h2[2];
+        for (size_t it = 0; it < max_iter; ++it) {
+            if (use_mtm) {  // w = Bᵀ(B v)
+                launch_rowdot(B.p, (long long)q, (long long)n, v.p, t.p, stream);
+                launch_coldot(B.p, (long long)q, (long long)n, t.p, w.p, part.p, cnt.p, nj2, jrows,
+                              stream);
+            } else {        // w = B(Bᵀ v)
+                launch_coldot(B.p, (long long)q, (long long)n, v.p, t.p, part.p, cnt.p, nj2, jrows,
+                              stream);
+                launch_rowdot(B.p, (long long)q, (long long)n, t.p, w.p, stream);
+            }
+            launch_power_step(v.p, w.p, vn.p, (long long)dim, out2.p, stream);
+            ck(cudaMemcpyAsync(h2, out2.p, sizeof h2, cudaMemcpyDeviceToHost, stream), "power");
+            sync("power");
+            const double rayleigh = h2[0], wn = h2[1];
+            if (wn == 0.0) return 0.0;
+            std::swap(v.p, vn.p);
+            if (it > 0 && std::abs(rayleigh - lambda) <= 0.5 * tol * std::abs(rayleigh))
+                return std::sqrt(rayleigh);
+            lambda = rayleigh;
+        }
+        AxbError e{AXB_CONVERGENCE_ERROR, "spectral_norm: power iteration did not converge"};
+        e.val = std::sqrt(std::abs(lambda));
+        throw e;
+    }
+
+    // D = C − (A·X)·B into out (store) with optional Σ D² and Σ (Rold − D)² partials
+    void exact_residual_into(double* out, double* sq, const double* rold, bool store) {
+        GemmArgs t1{};
+        t1.M = m; t1.N = q; t1.K = p;
+        t1.A = A.p; t1.lda = p;
+        t1.B = X.p; t1.ldb = q;
+        t1.D = T.p; t1.ldd = q;
+        t1.store = 1;
+        launch_gemm(t1, stream);
+        GemmArgs t2{};
+        t2.M = m; t2.N = n; t2.K = q;
+        t2.A = T.p; t2.lda = q;
+        t2.B = B.p; t2.ldb = n;
+        t2.D = out; t2.ldd = n;
+        t2.Cin = C.p; t2.ldc = n;
+        t2.Rold = rold; t2.ldr = n;
+        t2.sq_part = sq;
+        t2.diff_part = rold ? gemm_diff.p : nullptr;
+        t2.store = store ? 1 : 0;
+        launch_gemm(t2, stream);
+    }
+
+    // r_sq_, r_fro_sq_, reductions of the current R (solver.hpp:174-177, :468-476)
+    void adopt_norms() {
+        launch_r(P, stream, false);
+        if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) launch_err_fresh(P, stream);
+        sel_valid = false;
+    }
+
+    // ---------------------------------------------------------------- selection
+    void rollback() {
+        launch_rollback(P, stream);
+        sel_valid = false;
+    }
+
+    void ensure_selection() {
+        if (!sel_valid) {
+            launch_select(P, stream, cfg.method, P.theta, 0);
+            sel_valid = true;  // confirmed (or error) at the next state pull
+        }
+    }
+
+    // ---------------------------------------------------------------- iteration
+    void launch_iteration() {
+        launch_yg(P, stream, !gram_cached);
+        launch_zx(P, stream);
+        launch_r(P, stream, true);
+        kernel_launches += 3;
+    }
+
+    void build_graph() {
+        cudaGraph_t g0 = nullptr;
+        ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+        for (int i = 0; i < graph_iters; ++i) {
+            launch_yg(P, stream, !gram_cached);
+            launch_zx(P, stream);
+            launch_r(P, stream, true);
+        }
+        ck(cudaStreamEndCapture(stream, &g0), "capture end");
+        ck(cudaGraphInstantiate(&graph, g0, 0), "graph instantiate");
+        cudaGraphDestroy(g0);
+    }
+
+    // runs up to nb iterations from the current k; returns iterations executed
+    uint64_t batch(uint64_t nb, int run_mode) {
+        launch_ctrl(st.p, k, k + nb, FIN_ITERATION, run_mode, 0, stream);
+        ensure_selection();
+        if (profiling) {
+            if (prof_ev.size() < 2 * nb) {
+                size_t have = prof_ev.size();
+                prof_ev.resize(2 * nb);
+                for (size_t i = have; i < prof_ev.size(); ++i) ck(cudaEventCreate(&prof_ev[i]), "ev");
+            }
+            for (uint64_t i = 0; i < nb; ++i) {
+                launch_yg(P, stream, !gram_cached);
+                launch_zx(P, stream);
+                ck(cudaEventRecord(prof_ev[2 * i], stream), "ev");
+                launch_r(P, stream, true);
+                ck(cudaEventRecord(prof_ev[2 * i + 1], stream), "ev");
+                kernel_launches += 3;
+            }
+        } else if (nb < (uint64_t)graph_iters) {
+            for (uint64_t i = 0; i < nb; ++i) launch_iteration();
+        } else {
+            if (!graph) build_graph();
+            const uint64_t launches = (nb + graph_iters - 1) / graph_iters;
+            for (uint64_t i = 0; i < launches; ++i) ck(cudaGraphLaunch(graph, stream), "graph launch");
+            kernel_launches += 3 * nb;
+        }
+        pull_state();
+        if (profiling) {
+            const uint64_t done = hs->k - k;
+            for (uint64_t i = 0; i < done; ++i) {
+                float ms = 0.f;
+                ck(cudaEventElapsedTime(&ms, prof_ev[2 * i], prof_ev[2 * i + 1]), "elapsed");
+                k2_ms += ms;
+                ++k2_launches;
+            }
+        }
+        sel_valid = hs->sel_valid != 0;
+        const uint64_t done = hs->k - k;
+        if (done) {
+            ck(cudaMemcpyAsync(h_trace_row, tr_row.p, sizeof(long long) * done,
+                               cudaMemcpyDeviceToHost, stream), "trace");
+            ck(cudaMemcpyAsync(h_trace_metric, tr_metric.p, sizeof(double) * done,
+                               cudaMemcpyDeviceToHost, stream), "trace");
+            ck(cudaMemcpyAsync(h_trace_rel, tr_rel.p, sizeof(double) * done,
+                               cudaMemcpyDeviceToHost, stream), "trace");
+            sync("trace");
+        }
+        k = hs->k;
+        if (hs->status == ST_ERROR) raise_state();
+        return done;
+    }
+
+    void reset_status() { launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 1, stream); }
+
+    // k step() calls (acceptance.cpp:128-141), optional run()-style refresh
+    void steps(uint64_t count, uint64_t* rows, bool mirror_refresh) {
+        reset_status();
+        uint64_t got = 0;
+        cudaEventRecord(ev0, stream);
+        while (got < count) {
+            uint64_t nb = std::min<uint64_t>(count - got, trace_cap);
+            const uint64_t ri = cfg.refresh_interval;
+            if (mirror_refresh && ri > 0) nb = std::min<uint64_t>(nb, ri - k % ri);
+            const uint64_t done = batch(nb, 0);
+            if (rows)
+                for (uint64_t t = 0; t < done; ++t) rows[got + t] = (uint64_t)h_trace_row[t];
+            got += done;
+            if (done != nb) fail(AXB_CUDA_ERROR, "batch stopped early (%llu of %llu)",
+                                 (unsigned long long)done, (unsigned long long)nb);
+            if (mirror_refresh && ri > 0 && k % ri == 0) checkpoint();
+        }
+        cudaEventRecord(ev1, stream);
+        sync("steps");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        loop_ms = ms;
+    }
+
+    void update_row(uint64_t i) {  // solver.hpp:264-318
+        if (i >= m) fail(AXB_SHAPE_ERROR, "update_row: row %llu out of range", (unsigned long long)i);
+        if (!(a_sq_h[i] > 0.0)) fail(AXB_DOMAIN_ERROR, "update_row: zero row selected");
+        rollback();
+        launch_set_sel(st.p, (long long)i, alpha / a_sq_h[i], stream);
+        launch_ctrl(st.p, k, k + 1, FIN_UPDATE_ROW, 0, 1, stream);
+        launch_iteration();
+        launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 0, stream);
+        pull_state();
+        sel_valid = false;
+        if (hs->status == ST_ERROR) raise_state();
+    }
+
+    // ---------------------------------------------------------------- metrics
+    double current_metric() {
+        pull_state();
+        if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) return hs->err_sq / ref_sq;
+        return current_residual_rel();
+    }
+    double current_residual_rel() {
+        pull_state();
+        const double s = hs->r_fro_sq;
+        return std::sqrt(std::max(s, 0.0)) / (c_fro > 0.0 ? c_fro : 1.0);
+    }
+    double exact_residual_rel() {  // solver.hpp:417-419
+        exact_residual_into(nullptr, gemm_sq.p, nullptr, false);
+        launch_reduce_parts(gemm_sq.p, gemm_num_ctas((long long)m, (long long)n), scal.p, stream);
+        double s = 0.0;
+        ck(cudaMemcpyAsync(&s, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "exact");
+        sync("exact residual");
+        return std::sqrt(s) / (c_fro > 0.0 ? c_fro : 1.0);
+    }
+    double exact_metric() {  // solver.hpp:412-416
+        if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) {
+            launch_err_fresh(P, stream);
+            pull_state();
+            return hs->err_sq / ref_sq;
+        }
+        return exact_residual_rel();
+    }
+    double residual_drift() {  // solver.hpp:423
+        exact_residual_into(nullptr, nullptr, R.p, false);
+        launch_reduce_parts(gemm_diff.p, gemm_num_ctas((long long)m, (long long)n), scal.p, stream);
+        double s = 0.0;
+        ck(cudaMemcpyAsync(&s, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "drift");
+        sync("drift");
+        return std::sqrt(s);
+    }
+    void checkpoint() {  // solver.hpp:427-436
+        launch_err_fresh(P, stream);
+        pull_state();
+        if (!hs->x_finite) {
+            AxbError e{AXB_DIVERGENCE_ERROR, ""};
+            e.k = k;
+            e.val = std::sqrt(std::max(hs->r_fro_sq, 0.0));
+            char buf[160];
+            snprintf(buf, sizeof buf, "divergence at iteration %llu, residual frobenius norm %f",
+                     (unsigned long long)k, e.val);
+            e.msg = buf;
+            throw e;
+        }
+        rollback();
+        // exact residual written in place over R; the epilogue reads R_old first
+        exact_residual_into(R.p, nullptr, R.p, true);
+        launch_reduce_parts(gemm_diff.p, gemm_num_ctas((long long)m, (long long)n), scal.p, stream);
+        double d2 = 0.0;
+        ck(cudaMemcpyAsync(&d2, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "drift");
+        adopt_norms();
+        sync("checkpoint");
+        const double drift = std::sqrt(d2);
+        if (drift > 1e-8 * (1.0 + c_fro))
+            fail(AXB_INVARIANT_ERROR, "residual drift guard tripped at iteration %llu",
+                 (unsigned long long)k);
+    }
+    void resync() {  // solver.hpp:478
+        rollback();
+        exact_residual_into(R.p, nullptr, nullptr, true);
+        adopt_norms();
+    }
+
+    // ---------------------------------------------------------------- run()
+    void run(axb_report* rep, uint64_t* trace_k, double* trace_rrn, double* trace_rel,
+             uint64_t* trace_row, uint64_t trace_cap_out, double* x_out) {
+        std::memset(rep, 0, sizeof *rep);
+        rep->alpha = alpha;
+        rep->seed = cfg.seed;
+        rep->alpha_outside_bound = alpha_outside;
+        reset_status();
+        uint64_t ntrace = 0;
+        bool converged = exact_metric() <= cfg.tol;  // :344
+        const auto t0 = std::chrono::steady_clock::now();
+        cudaEventRecord(ev0, stream);
+        try {
+            while (!converged && k < cfg.max_iter) {
+                pull_state();
+                if (!(hs->r_fro_sq > 0.0)) break;  // :347
+                uint64_t nb = std::min<uint64_t>(cfg.max_iter - k, trace_cap);
+                const uint64_t ri = cfg.refresh_interval;
+                if (ri > 0) nb = std::min<uint64_t>(nb, ri - k % ri);
+                const uint64_t k_before = k;
+                const uint64_t done = batch(nb, 1);
+                if (cfg.record_trace) {
+                    for (uint64_t t = 0; t < done; ++t) {
+                        const uint64_t kk = k_before + t;
+                        if (!trace_point_due(kk)) continue;  // :349-350
+                        if (ntrace < trace_cap_out) {
+                            if (trace_k) trace_k[ntrace] = kk;
+                            if (trace_rrn) trace_rrn[ntrace] = h_trace_metric[t];
+                            if (trace_rel) trace_rel[ntrace] = h_trace_rel[t];
+                            if (trace_row) trace_row[ntrace] = (uint64_t)h_trace_row[t];
+                        }
+                        ++ntrace;
+                    }
+                }
+                if (hs->status == ST_ZERO) {
+                    launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 1, stream);
+                    break;
+                }
+                if (hs->status == ST_PAUSE) {  // :351-358
+                    launch_ctrl(st.p, k, k, FIN_ITERATION, 1, 1, stream);
+                    if (exact_metric() <= cfg.tol) converged = true;
+                    else resync();
+                }
+                if (!converged && ri > 0 && k % ri == 0) checkpoint();  // :359-360
+            }
+        } catch (AxbError& e) {
+            rep->iterations = k;
+            rep->diverged_iteration = e.k;
+            rep->diverged_residual = e.val;
+            throw;
+        }
+        cudaEventRecord(ev1, stream);
+        sync("run");
+        const auto t1 = std::chrono::steady_clock::now();
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        loop_ms = ms;
+        rep->iterations = k;
+        rep->wall_seconds = std::chrono::duration<double>(t1 - t0).count();
+        rep->terminated_by = converged ? AXB_TERMINATED_TOLERANCE : AXB_TERMINATED_MAX_ITER;
+        rep->final_rrn = exact_metric();
+        rep->final_residual_rel = exact_residual_rel();
+        pull_state();
+        rep->skipped_zero_rows = hs->skipped_zero_rows;
+        rep->trace_len = ntrace;
+        if (x_out) {
+            ck(cudaMemcpyAsync(x_out, X.p, sizeof(double) * p * q, cudaMemcpyDeviceToHost, stream),
+               "X out");
+            sync("X out");
+        }
+    }
+
+    // ---------------------------------------------------------------- public selects
+    uint64_t select_consume(int method, double theta) {
+        rollback();
+        reset_status();
+        launch_select(P, stream, method, theta, 1);
+        pull_state();
+        if (hs->status == ST_ERROR) {
+            const int save = cfg.method;
+            cfg.method = method;
+            try {
+                raise_state();
+            } catch (...) {
+                cfg.method = save;
+                throw;
+            }
+        }
+        return (uint64_t)hs->q_row;
+    }
+    void query(double theta, bool want_set) {
+        reset_status();
+        launch_query(P, stream, theta, want_set ? 1 : 0);
+        pull_state();
+        if (hs->status == ST_ERROR) {
+            launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 1, stream);
+            fail(AXB_DOMAIN_ERROR, "greedy threshold: zero residual");
+        }
+    }
+};
+
+// =========================================================================
+// C-ABI
+namespace {
+thread_local std::string g_create_err;
+
+template <class F>
+int guarded(axb_solver* s, F&& f) {
+    try {
+        f();
+        return AXB_OK;
+    } catch (const AxbError& e) {
+        if (s) s->err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        if (s) s->err = e.what();
+        return AXB_CUDA_ERROR;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+void axb_options_default(axb_options* o) {
+    std::memset(o, 0, sizeof *o);
+    o->cache_gram = -1;
+    o->spectral_on_device = -1;
+    o->tie_guard = 1;
+    o->world_size = 1;
+}
+
+int axb_abi_version(void) { return AXB_B200_ABI_VERSION; }
+
+int axb_device_available(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return 0;
+    cudaDeviceProp p{};
+    if (cudaGetDeviceProperties(&p, 0) != cudaSuccess) return 0;
+    return p.major >= 10 ? 1 : 0;
+}
+
+const char* axb_last_create_error(void) { return g_create_err.c_str(); }
+
+int axb_solver_create(const double* A, uint64_t m, uint64_t p, const double* B, uint64_t q,
+                      uint64_t n, const double* C, const double* X0, const axb_config* cfg,
+                      const axb_options* opt, axb_solver** out) {
+    *out = nullptr;
+    auto s = std::make_unique<axb_solver>();
+    s->m = m; s->p = p; s->q = q; s->n = n;
+    s->cfg = *cfg;
+    if (opt) s->opt = *opt;
+    else axb_options_default(&s->opt);
+    int st = guarded(s.get(), [&] { s->create(A, B, C, X0); });
+    if (st != AXB_OK) {
+        g_create_err = s->err;
+        return st;
+    }
+    g_create_err.clear();
+    *out = s.release();
+    return AXB_OK;
+}
+
+void axb_solver_destroy(axb_solver* s) { delete s; }
+const char* axb_solver_last_error(const axb_solver* s) { return s->err.c_str(); }
+
+int axb_solver_step(axb_solver* s, uint64_t* row) {
+    return guarded(s, [&] { s->steps(1, row, false); });
+}
+int axb_solver_steps(axb_solver* s, uint64_t k, uint64_t* rows, int32_t mirror_refresh) {
+    return guarded(s, [&] { s->steps(k, rows, mirror_refresh != 0); });
+}
+int axb_solver_update_row(axb_solver* s, uint64_t i) {
+    return guarded(s, [&] { s->update_row(i); });
+}
+int axb_solver_run(axb_solver* s, axb_report* rep, uint64_t* trace_k, double* trace_rrn,
+                   double* trace_rel, uint64_t* trace_row, uint64_t trace_cap, double* x_out) {
+    return guarded(s, [&] { s->run(rep, trace_k, trace_rrn, trace_rel, trace_row, trace_cap, x_out); });
+}
+int axb_solver_select_cyclic(axb_solver* s, uint64_t* row) {
+    return guarded(s, [&] { *row = s->select_consume(AXB_BK, 0.5); });
+}
+int axb_solver_select_rbk(axb_solver* s, uint64_t* row) {
+    return guarded(s, [&] { *row = s->select_consume(AXB_RBK, 0.5); });
+}
+int axb_solver_select_greedy(axb_solver* s, double theta, uint64_t* row) {
+    return guarded(s, [&] { *row = s->select_consume(AXB_GRBK, theta); });
+}
+int axb_solver_select_mwrbk(axb_solver* s, uint64_t* row) {
+    return guarded(s, [&] { *row = s->select_consume(AXB_MWRBK, 0.5); });
+}
+int axb_solver_greedy_threshold(axb_solver* s, double theta, double* out) {
+    return guarded(s, [&] {
+        s->query(theta, false);
+        *out = s->hs->q_zeta;
+    });
+}
+int axb_solver_rgrbk_threshold(axb_solver* s, double theta, double* out) {
+    return guarded(s, [&] {
+        if (!(theta > 0.0 && theta < 1.0)) fail(AXB_CONFIG_ERROR, "theta must lie in (0, 1)");
+        s->query(theta, false);
+        *out = s->hs->q_zeta;
+    });
+}
+int axb_solver_greedy_index_set(axb_solver* s, double theta, uint64_t* out, uint64_t* count) {
+    return guarded(s, [&] {
+        s->query(theta, true);
+        std::vector<int> f(s->m);
+        ck(cudaMemcpy(f.data(), s->flags.p, sizeof(int) * s->m, cudaMemcpyDeviceToHost), "flags");
+        uint64_t c = 0;
+        for (uint64_t i = 0; i < s->m; ++i)
+            if (f[i]) out[c++] = i;
+        if (c == 0) fail(AXB_INVARIANT_ERROR, "greedy index set is empty");
+        *count = c;
+    });
+}
+int axb_solver_max_residual_ratio(axb_solver* s, uint64_t* row, double* ratio) {
+    return guarded(s, [&] {
+        s->pull_state();
+        if (s->hs->argmax < 0 || s->hs->argmax >= (long long)s->m)
+            fail(AXB_DOMAIN_ERROR, "no nonzero row in A");
+        *row = (uint64_t)s->hs->argmax;
+        *ratio = s->hs->max_ratio;
+    });
+}
+int axb_solver_current_metric(axb_solver* s, double* out) {
+    return guarded(s, [&] { *out = s->current_metric(); });
+}
+int axb_solver_current_residual_rel(axb_solver* s, double* out) {
+    return guarded(s, [&] { *out = s->current_residual_rel(); });
+}
+int axb_solver_exact_metric(axb_solver* s, double* out) {
+    return guarded(s, [&] { *out = s->exact_metric(); });
+}
+int axb_solver_exact_residual_rel(axb_solver* s, double* out) {
+    return guarded(s, [&] { *out = s->exact_residual_rel(); });
+}
+int axb_solver_residual_drift(axb_solver* s, double* out) {
+    return guarded(s, [&] { *out = s->residual_drift(); });
+}
+int axb_solver_checkpoint(axb_solver* s) {
+    return guarded(s, [&] { s->checkpoint(); });
+}
+uint64_t axb_solver_iteration(const axb_solver* s) { return s->k; }
+double axb_solver_alpha(const axb_solver* s) { return s->alpha; }
+double axb_solver_spectral_norm_b(const axb_solver* s) { return s->b_spec; }
+int axb_solver_alpha_outside_bound(const axb_solver* s) { return s->alpha_outside ? 1 : 0; }
+double axb_solver_a_fro_sq(const axb_solver* s) { return s->a_fro_sq; }
+int axb_solver_residual_fro_sq(axb_solver* s, double* out) {
+    return guarded(s, [&] {
+        s->pull_state();
+        *out = s->hs->r_fro_sq;
+    });
+}
+static int copy_out(axb_solver* s, double* dst, const double* src, size_t count) {
+    return guarded(s, [&] {
+        ck(cudaMemcpy(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost), "copy out");
+    });
+}
+int axb_solver_get_X(axb_solver* s, double* out) { return copy_out(s, out, s->X.p, s->p * s->q); }
+int axb_solver_get_R(axb_solver* s, double* out) { return copy_out(s, out, s->R.p, s->m * s->n); }
+int axb_solver_get_r_sq(axb_solver* s, double* out) { return copy_out(s, out, s->r_sq.p, s->m); }
+int axb_solver_get_a_sq(axb_solver* s, double* out) { return copy_out(s, out, s->a_sq.p, s->m); }
+int axb_solver_dims(const axb_solver* s, uint64_t dims[4]) {
+    dims[0] = s->m; dims[1] = s->p; dims[2] = s->q; dims[3] = s->n;
+    return AXB_OK;
+}
+int axb_solver_last_timing(const axb_solver* s, double* loop_ms, double* k2_ms,
+                           uint64_t* k2_launches, uint64_t* kernel_launches) {
+    if (loop_ms) *loop_ms = s->loop_ms;
+    if (k2_ms) *k2_ms = s->k2_ms;
+    if (k2_launches) *k2_launches = s->k2_launches;
+    if (kernel_launches) *kernel_launches = s->kernel_launches;
+    return AXB_OK;
+}
+int axb_solver_set_profiling(axb_solver* s, int32_t on) {
+    s->profiling = on != 0;
+    s->k2_ms = 0.0;
+    s->k2_launches = 0;
+    s->kernel_launches = 0;
+    return AXB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): deterministic MWRBK — same index sequence and
+iterates within 1e-10 relative; randomized variants replaying the reference's
+xoshiro256** stream — same index sequence (the oracle's) and iterates within
+1e-10 relative; every variant reaches the same relative error.
+Oracle = oracle/axb_oracle.c, bitwise-pinned to the unmodified reference.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL_X = 1e-10
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def axb_method(axb, tag, theta=None):
+    return {O.BK: axb.Method.bk(), O.RBK: axb.Method.rbk(), O.GRBK: axb.Method.grbk(),
+            O.RGRBK: axb.Method.rgrbk(theta if theta is not None else 0.5),
+            O.MWRBK: axb.Method.mwrbk()}[tag]
+
+
+def pair(axb, orc, A, B, Cm, X0, tag, theta=None, seed=0, Xref=None, refresh=0, tol=0.0,
+         max_iter=200000, options=None, stop_rrn=True):
+    if stop_rrn:
+        stop_o = dict(stop_kind=O.SOLUTION_RRN, tol=tol, reference=Xref)
+        stop = axb.StopRule.solution_rrn(tol, Xref)
+    else:
+        stop_o = dict(stop_kind=O.RESIDUAL_REL, tol=tol)
+        stop = axb.StopRule.residual_rel(tol)
+    cfg_o = O.make_config(method=tag, theta=theta, seed=seed, max_iter=max_iter,
+                          refresh_interval=refresh, **stop_o)
+    so = O.Solver(orc, A, B, Cm, X0, cfg_o)
+    cfg = axb.SolveConfig(method=axb_method(axb, tag, theta), stop=stop, max_iter=max_iter,
+                          seed=seed, refresh_interval=refresh)
+    sg = axb.Solver(A, B, Cm, X0, cfg, options)
+    return so, sg
+
+
+@pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.MWRBK, None), (O.RGRBK, 0.25),
+                                       (O.RGRBK, 0.75), (O.RBK, None), (O.BK, None)])
+def test_config1_step_sequence(axb, orc, tag, theta):
+    """Config-1 shape (A 500×100, B 80×400): 3000 steps, identical rows, X within 1e-10."""
+    A, B, X, Cm = O.generate(orc, 7, 500, 100, 80, 400)
+    so, sg = pair(axb, orc, A, B, Cm, None, tag, theta, seed=42, Xref=X)
+    assert so.alpha == sg.alpha(), "host α must be the reference's bit for bit"
+    np.testing.assert_array_equal(sg.a_row_sq(), so.a_sq())
+    ro = so.steps(3000)
+    rg = sg.steps(3000)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
+    assert rel(sg.R(), so.R()) <= 1e-9
+
+
+def test_config1_run_to_tolerance(axb, orc):
+    """Config 1 end to end: ‖X−X*‖/‖X*‖ < 1e-6 ⇔ squared RRN ≤ 1e-12, refresh every 1000."""
+    A, B, X, Cm = O.generate(orc, 7, 500, 100, 80, 400)
+    so, sg = pair(axb, orc, A, B, Cm, None, O.GRBK, seed=42, Xref=X, refresh=1000, tol=1e-12)
+    rep_o, rows_o, _, Xo = so.run(20000)
+    rep = sg.run()
+    assert rep_o.iterations == 13483
+    assert abs(rep.iterations - rep_o.iterations) <= 2
+    assert rep.terminated_by == axb.Terminated.Tolerance
+    assert rep.final_rrn <= 1e-12
+    assert rel(rep.X, Xo) <= 1e-8
+
+
+def test_update_row_kat(axb):
+    """test_solver.cpp:37-44 — A=[2], B=[1], C=[4], α=1: one step gives X=2, R=0."""
+    A = np.array([[2.0]]); B = np.array([[1.0]]); Cm = np.array([[4.0]])
+    cfg = axb.SolveConfig(method=axb.Method.bk(), alpha_rule=axb.AlphaRule.Fixed, alpha_value=1.0,
+                          stop=axb.StopRule.residual_rel(0.0), max_iter=1000, refresh_interval=0)
+    s = axb.Solver(A, B, Cm, np.zeros((1, 1)), cfg)
+    assert s.R()[0, 0] == 4.0
+    s.update_row(0)
+    assert s.X()[0, 0] == 2.0
+    assert s.R()[0, 0] == 0.0
+
+
+def test_greedy_threshold_kats(axb):
+    """test_solver.cpp:136-151: ζ=0.75, ξ(0.8)=0.9, θ=½ bitwise GRBK."""
+    A = np.eye(2); B = np.array([[1.0]]); Cm = np.array([[1.0], [0.0]])
+    cfg = axb.SolveConfig(method=axb.Method.grbk(), alpha_rule=axb.AlphaRule.Fixed, alpha_value=0.5,
+                          stop=axb.StopRule.residual_rel(0.0), max_iter=1000, refresh_interval=0)
+    s = axb.Solver(A, B, Cm, np.zeros((2, 1)), cfg)
+    assert s.grbk_threshold() == pytest.approx(0.75, rel=1e-15)
+    assert s.rgrbk_threshold(0.8) == pytest.approx(0.9, rel=1e-15)
+    assert s.rgrbk_threshold(0.5) == s.grbk_threshold()
+    with pytest.raises(axb.ConfigError):
+        s.rgrbk_threshold(1.5)
+    assert s.greedy_index_set(0.5) == [0]
+    for _ in range(20):
+        assert s.select_grbk() == 0
+    assert s.select_mwrbk() == 0
+
+
+def test_mwrbk_tie_smallest_index(axb):
+    A = np.eye(3); B = np.array([[1.0]]); Cm = np.full((3, 1), np.sqrt(2.0))
+    cfg = axb.SolveConfig(method=axb.Method.mwrbk(), alpha_rule=axb.AlphaRule.Fixed,
+                          alpha_value=0.5, stop=axb.StopRule.residual_rel(0.0), refresh_interval=0)
+    s = axb.Solver(A, B, Cm, np.zeros((3, 1)), cfg)
+    assert s.select_mwrbk() == 0
+
+
+def test_residual_init_with_x0(axb, orc):
+    """R0 = C − (A·X0)·B on the DMMA path vs the oracle (X0 random)."""
+    A, B, X, Cm = O.generate(orc, 3, 300, 64, 48, 200)
+    X0 = np.random.default_rng(0).standard_normal((64, 48))
+    so, sg = pair(axb, orc, A, B, Cm, X0, O.MWRBK, Xref=X)
+    assert rel(sg.R(), so.R()) <= 1e-13
+    np.testing.assert_allclose(sg.residual_row_sq(), so.r_sq(), rtol=1e-12)
+    ro = so.steps(500)
+    rg = sg.steps(500)
+    np.testing.assert_array_equal(ro, rg)
+    assert rel(sg.X(), so.X()) <= RTOL_X
