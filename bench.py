@@ -1,0 +1,431 @@
+#!/usr/bin/env python3
+"""Benchmark: Kaczmarz iterations/s of the B200 solver (BASELINE.json metric).
+
+Workload (default --config 3, BASELINE.json configs[2], the HBM-bound case):
+ME-GRBK (θ=½, i.e. RGRBK θ=0.5) fp64, A 8192×2048 and B 2048×8192 iid N(0,1),
+X* 2048×2048 N(0,1), C = A·X*·B, X0 N(0,1), stop solution_rrn(1e-12, X*) (never met
+within the timed window), refresh checkpoints every 1000 iterations as the reference
+defaults.  One "step" = one Kaczmarz iteration (select → y → z/X → fused R update).
+Inputs are synthetic (seeded torch RNG on the device); R (537 MB) exceeds the 126 MB
+L2, so no explicit flush is needed between iterations.
+
+N > 1 (torchrun): one process per GPU, each solving its own independent system of
+the same shape (independent right-hand sides) — weak scaling, no
+data-path collective; value = Σ iterations / max-over-ranks device time.
+
+--impl reference: the reference's per-iteration algorithm on the host cores (the
+oracle C port, bitwise-pinned to the reference; kind "port"), one solver per core
+as the reference's benchmark pool runs trials (analysis.hpp:295-313).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(m=500, p=100, q=80, n=400, x0="zero", scale_a=1.0, scale_b=1.0,
+            desc="config1: ME-GRBK fp64 A 500x100, B 80x400 iid N(0,1), X0=0"),
+    3: dict(m=8192, p=2048, q=2048, n=8192, x0="randn", scale_a=1.0, scale_b=1.0,
+            desc="config3: ME-GRBK(theta=1/2) fp64 A 8192x2048, B 2048x8192 iid N(0,1), "
+                 "X0 N(0,1), X* N(0,1), C=A.X*.B"),
+    5: dict(m=65536, p=8192, q=8192, n=32768, x0="zero", scale_a=8192 ** -0.5,
+            scale_b=32768 ** -0.5,
+            desc="config5: ME-GRBK fp64 A 65536x8192 N(0,1/8192), B 8192x32768 N(0,1/32768), "
+                 "X* 8192x8192 N(0,1), X0=0"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- workload
+def make_inputs_device(cfg, seed, device):
+    import torch
+
+    g = torch.Generator(device=f"cuda:{device}").manual_seed(seed)
+    kw = dict(dtype=torch.float64, device=f"cuda:{device}", generator=g)
+    A = torch.randn(cfg["m"], cfg["p"], **kw) * cfg["scale_a"]
+    B = torch.randn(cfg["q"], cfg["n"], **kw) * cfg["scale_b"]
+    Xs = torch.randn(cfg["p"], cfg["q"], **kw)
+    C = (A @ Xs) @ B
+    X0 = torch.randn(cfg["p"], cfg["q"], **kw) if cfg["x0"] == "randn" else None
+    torch.cuda.synchronize(device)
+    return A, B, C, X0, Xs
+
+
+def solver_config(axb, Xs, max_iter):
+    return axb.SolveConfig(method=axb.Method.grbk(), alpha_rule=axb.AlphaRule.Safe,
+                           stop=axb.StopRule.solution_rrn(1e-12, Xs), max_iter=max_iter,
+                           seed=42, refresh_interval=1000)
+
+
+def k2_bytes(cfg):
+    """Algorithmic bytes of one fused residual-update launch:
+    read+write R (16·m·n), read the G column and z, write ‖R_l‖² (8·(2m+n))."""
+    m, n = cfg["m"], cfg["n"]
+    return 16 * m * n + 8 * (2 * m + n)
+
+
+def iteration_bytes(cfg, gram_cached=True):
+    m, p, q, n = cfg["m"], cfg["p"], cfg["q"], cfg["n"]
+    return k2_bytes(cfg) + 16 * q * n + 16 * p * q + (8 * m if gram_cached else 8 * m * p)
+
+
+# --------------------------------------------------------------------- CPU legs
+def cpu_prepared_state(cfg, seed):
+    """Host inputs + the reference constructor's caches (numpy BLAS: setup only)."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    m, p, q, n = cfg["m"], cfg["p"], cfg["q"], cfg["n"]
+    A = rng.standard_normal((m, p)) * cfg["scale_a"]
+    B = rng.standard_normal((q, n)) * cfg["scale_b"]
+    Xs = rng.standard_normal((p, q))
+    X0 = rng.standard_normal((p, q)) if cfg["x0"] == "randn" else np.zeros((p, q))
+    C = (A @ Xs) @ B
+    R0 = C - (A @ X0) @ B
+    G = A @ A.T
+    BtB = B.T @ B
+    bbt = B @ B.T if q <= n else B.T @ B
+    alpha = 1.0 / float(np.linalg.eigvalsh(bbt).max())
+    return dict(A=A, B=B, C=C, X0=X0, Xs=Xs, R0=R0, G=G, BtB=BtB, alpha=alpha)
+
+
+def cpu_solver(O, orc, state, seed):
+    cfg_o = O.make_config(method=O.GRBK, stop_kind=O.SOLUTION_RRN, tol=1e-12,
+                          reference=state["Xs"], seed=seed, refresh_interval=0)
+    return O.PreparedSolver(orc, state["A"], state["B"], state["C"], state["X0"], state["R0"],
+                            state["G"], state["BtB"], state["alpha"], cfg_o), cfg_o
+
+
+def cpu_baseline(cfg, budget_s=15.0):
+    """The oracle port (bitwise the reference's per-iteration algorithm), 1 core."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+
+    orc = O.oracle()
+    state = cpu_prepared_state(cfg, 7)
+    s, _keep = cpu_solver(O, orc, state, 42)
+    s.steps(1)  # warm
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        s.steps(1)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s or done >= 2000:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "iter/s", "cores": 1, "kind": "port",
+            "sample": f"{done} ME-GRBK iterations of one {cfg['m']}x{cfg['p']}.{cfg['q']}x{cfg['n']} "
+                      f"solve (oracle C port of solver.hpp step(); constructor caches "
+                      f"precomputed with numpy), {dt:.1f}s on 1 core"}
+
+
+def reference_arm(args, cfg):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+
+    orc = O.oracle()
+    T = max(1, min(os.cpu_count() or 1, args.ref_threads))
+    log(f"[reference] preparing {cfg['desc']} on the host; {T} solver threads")
+    state = cpu_prepared_state(cfg, 7)
+    solvers = [cpu_solver(O, orc, state, 42 + t) for t in range(T)]
+    per = max(1, math.ceil(args.steps / T))
+    budget = args.ref_budget_s
+    # warmup (W iterations spread over the pool)
+    wper = max(1, math.ceil(args.warmup / T))
+    for s, _ in solvers:
+        s.steps(wper)
+    # calibrate: bound the sample so the run stays within the budget
+    t0 = time.perf_counter()
+    solvers[0][0].steps(1)
+    one = time.perf_counter() - t0
+    per = max(1, min(per, int(budget / max(one, 1e-9) / 1.5)))
+    counts = [0] * T
+
+    def work(t):
+        s = solvers[t][0]
+        s.steps(per)
+        counts[t] = per
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(T)]
+    t0 = time.perf_counter()
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    dt = time.perf_counter() - t0
+    total = sum(counts)
+    value = total / dt
+    cores = T
+    line = {
+        "impl": "reference",
+        "metric": "kaczmarz_iterations_per_sec", "value": value, "unit": "iter/s",
+        "n_gpus": args.gpus, "steps": total, "warmup": wper * T, "ms_per_step": 1000.0 * dt / total,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (numpy seeded N(0,1))",
+        "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
+                   "n": cfg["n"], "method": "grbk", "parallelism": f"{T} independent solves"},
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port",
+                         "sample": f"{T} concurrent solves x {per} iterations (reference "
+                                   f"benchmark-pool pattern), oracle C port of solver.hpp "
+                                   f"step(), {dt:.1f}s wall"},
+        "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tol", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=50)
+    ap.add_argument("--ref-threads", type=int, default=16)
+    ap.add_argument("--ref-budget-s", type=float, default=60.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_05444_b200 as axb
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    seed = 1000 + rank
+    max_iter = 10 ** 9
+    log(f"[rank {rank}] generating {cfg['desc']}")
+    A, B, C, X0, Xs = make_inputs_device(cfg, seed, local)
+    opts = axb.Options(device=local, spectral_max_iter=200000)
+    t0 = time.perf_counter()
+    s = axb.Solver(A, B, C, X0, solver_config(axb, Xs, max_iter), opts)
+    setup_s = time.perf_counter() - t0
+    del A, B, C, X0
+    torch.cuda.empty_cache()
+    log(f"[rank {rank}] solver ready in {setup_s:.2f}s, alpha={s.alpha():.6e}")
+
+    # warmup, then exactly K timed steps (device events on the solver stream)
+    s.steps(args.warmup, mirror_refresh=True)
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    barrier()
+    s.steps(args.steps, mirror_refresh=True)
+    barrier()
+    ck = clocks.stop()
+    tm = s.last_timing()
+    ms = allmax(tm["loop_ms"])
+    launches = tm["kernel_launches"]
+    value = world * args.steps / (ms / 1000.0)
+    log(f"[rank {rank}] {args.steps} iterations in {tm['loop_ms']:.2f} ms -> "
+        f"{args.steps / (tm['loop_ms'] / 1000):.1f} it/s")
+
+    # dominant kernel K2 (fused residual update): CUDA events around each launch
+    s.set_profiling(True)
+    s.steps(args.profile_steps, mirror_refresh=False)
+    pt = s.last_timing()
+    s.set_profiling(False)
+    k2_ms = pt["k2_ms"] / max(pt["k2_launches"], 1)
+    peak, peak_kind = peaks()
+    kb = k2_bytes(cfg)
+    achieved = kb / (k2_ms / 1000.0) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"k2_traffic_config{args.config}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    per_iter_ms = ms / args.steps
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "k_r<true,true> (fused R update + row norms + select)",
+                "algorithmic_bytes_per_launch": kb, "k2_ms": round(k2_ms, 5),
+                "peak_kind": peak_kind,
+                "k2_share_of_step": round(k2_ms / per_iter_ms, 4),
+                "iteration_bytes": iteration_bytes(cfg),
+                "iteration_achieved_gbs": round(iteration_bytes(cfg) / (per_iter_ms / 1000) / 1e9, 1)}
+    del s
+    torch.cuda.empty_cache()
+
+    # e2e: the public API from pinned host buffers (H2D of the system, device init,
+    # K iterations, D2H of X), wall clock, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        Ad, Bd, Cd, X0d, Xsd = make_inputs_device(cfg, seed + 7919, local)
+        host = {}
+        for name, t in (("A", Ad), ("B", Bd), ("C", Cd), ("X0", X0d), ("Xs", Xsd)):
+            if t is None:
+                host[name] = None
+                continue
+            h = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+            h.copy_(t)
+            host[name] = h.numpy()
+        del Ad, Bd, Cd, X0d, Xsd
+        torch.cuda.empty_cache()
+        h2d = sum(v.nbytes for v in host.values() if v is not None)
+        barrier()
+        t0 = time.perf_counter()
+        s2 = axb.Solver(host["A"], host["B"], host["C"], host["X0"],
+                        solver_config(axb, host["Xs"], max_iter), opts)
+        s2.steps(args.steps, mirror_refresh=True)
+        Xout = s2.X()
+        torch.cuda.synchronize(local)
+        e2e_s = allmax(time.perf_counter() - t0)
+        d2h = Xout.nbytes + 8 * args.steps
+        e2e = {"value": world * args.steps / e2e_s, "unit": "iter/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "seconds": round(e2e_s, 4),
+               "what": "Solver(host A,B,C,X0,X*) -> steps(K) -> X() through the C-ABI; "
+                       "includes H2D of the system, device ||B||_2, G=A.A^T, R0 (DMMA), D2H of X"}
+        del s2
+        host = None
+
+    # time-to-tolerance on config 1 (the reference's CPU-runnable case)
+    ttt = None
+    if rank == 0 and not args.no_tol:
+        c1 = CONFIGS[1]
+        A1, B1, C1, _, X1 = make_inputs_device(c1, 7, local)
+        s1 = axb.Solver(A1, B1, C1, None, solver_config(axb, X1, 10 ** 6), axb.Options(device=local))
+        s1.cfg.max_iter = 10 ** 6
+        t0 = time.perf_counter()
+        rep = s1.run()
+        ttt = {"config": "config1 (A 500x100, B 80x400, GRBK, ||X-X*||/||X*|| < 1e-6)",
+               "iterations": rep.iterations, "seconds": round(rep.wall_seconds, 4),
+               "device_loop_ms": round(s1.last_timing()["loop_ms"], 3),
+               "final_rel_error": math.sqrt(rep.final_rrn),
+               "terminated_by": rep.terminated_by.name}
+        del s1
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": "kaczmarz_iterations_per_sec", "value": round(value, 2), "unit": "iter/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded torch N(0,1) on device)",
+            "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
+                       "n": cfg["n"], "method": "grbk", "refresh_interval": 1000,
+                       "parallelism": f"{world} independent systems (one per GPU)" if world > 1
+                       else "single GPU",
+                       "l2": "R is 8*m*n bytes > 126 MB L2: inputs larger than L2, no flush"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": ck,
+            "time_to_tol": ttt,
+            "setup_s": round(setup_s, 3),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

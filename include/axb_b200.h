@@ -121,6 +121,9 @@ int axb_solver_create(const double* A, uint64_t m, uint64_t p, const double* B, 
                       const axb_options* opt, axb_solver** out);
 void axb_solver_destroy(axb_solver* s);
 const char* axb_solver_last_error(const axb_solver* s);
+/* payload of the last DivergenceError (iteration, residual norm) or
+ * ConvergenceError (last estimate in *value) raised on this handle */
+int axb_solver_last_error_info(const axb_solver* s, uint64_t* iteration, double* value);
 /* message for failures of axb_solver_create (handle-less), thread-local */
 const char* axb_last_create_error(void);
 
@@ -131,6 +134,13 @@ int axb_solver_step(axb_solver* s, uint64_t* row);
  * mirror_refresh is set, checkpoint() runs every cfg.refresh_interval
  * iterations exactly as run() schedules it (solver.hpp:359-360). */
 int axb_solver_steps(axb_solver* s, uint64_t k, uint64_t* rows, int32_t mirror_refresh);
+/* k iterations on a GIVEN index stream (e.g. the reference's, from its trace):
+ * each step applies update_row(rows[t]) and advances k, the RNG draw / cyclic
+ * position and the refresh schedule exactly as step() would, so a randomized
+ * run can be replayed and its iterates compared (north star: "randomized
+ * variants, replaying the reference's index stream").  A zero row of A yields
+ * AXB_DOMAIN_ERROR as update_row does. */
+int axb_solver_replay(axb_solver* s, uint64_t k, const uint64_t* rows, int32_t mirror_refresh);
 /* Solver::update_row(i) — solver.hpp:264-318. */
 int axb_solver_update_row(axb_solver* s, uint64_t i);
 /* Solver::run() — solver.hpp:337-372.  trace_* (may be NULL) receive up to

@@ -134,6 +134,13 @@ typedef struct {
 int orc_solver_run(orc_solver* s, orc_report* rep, uint64_t* trace_k, double* trace_rrn,
                    double* trace_rel, uint64_t* trace_row, uint64_t trace_cap, double* x_out);
 
+/* benchmark-only prepared state: caches borrowed from the caller (see .c) */
+orc_solver* orc_solver_create_prepared(const double* A, size_t m, size_t p, const double* B,
+                                       size_t q, size_t n, const double* C, const double* X0,
+                                       const double* R0, const double* G, const double* BtB,
+                                       double alpha, const orc_config* cfg, int* status);
+int orc_solver_steps(orc_solver* s, uint64_t k, uint64_t* rows);
+
 /* accessors (solver.hpp:376-385) */
 uint64_t orc_solver_iteration(const orc_solver* s);
 double orc_solver_alpha(const orc_solver* s);

@@ -87,8 +87,10 @@ SIGNATURES = [
     ("axb_solver_destroy", None, [_H]),
     ("axb_solver_last_error", C.c_char_p, [_H]),
     ("axb_last_create_error", C.c_char_p, []),
+    ("axb_solver_last_error_info", C.c_int, [_H, _u64p, _dp]),
     ("axb_solver_step", C.c_int, [_H, _u64p]),
     ("axb_solver_steps", C.c_int, [_H, C.c_uint64, _u64p, C.c_int32]),
+    ("axb_solver_replay", C.c_int, [_H, C.c_uint64, _u64p, C.c_int32]),
     ("axb_solver_update_row", C.c_int, [_H, C.c_uint64]),
     ("axb_solver_run", C.c_int,
      [_H, C.POINTER(AxbReport), _u64p, _dp, _dp, _u64p, C.c_uint64, _dp]),

@@ -69,6 +69,9 @@ struct alignas(16) DevState {
     unsigned int cnt_x;
     unsigned int cnt_red;
     unsigned int _pad1;
+    unsigned long long r_next;   // dynamic row counter of the TMA residual kernel
+    int32_t replay;              // 1: select from Params::forced_rows (index-stream replay)
+    int32_t _pad2;
 };
 
 struct RowRecord {   // per-CTA partial of the residual reduction
@@ -105,11 +108,12 @@ struct Params {
     double* trace_rel;           // batch trace of ‖R‖/‖C‖
     unsigned long long trace_cap;
     int* member_flags;           // m (greedy_index_set query)
+    const long long* forced_rows;  // replayed index stream, slot = k − k0
     DevState* st;
     double alpha, theta, a_fro_sq, tol, ref_sq, c_fro;
     int method, stop_kind, tie_guard, vec2;
     // launch geometry
-    int r_grid, r_rows_per_cta, r_chunk;
+    int r_grid, r_rows_per_cta, r_chunk, r_tma, r_stages;
     int yg_grid;
     int z_nslab, z_nj, z_jrows, x_ctas;
 };
@@ -133,6 +137,7 @@ void launch_fill(double* p, long long n, double v, cudaStream_t s);
 void launch_ctrl(DevState* st, unsigned long long k0, unsigned long long k_limit, int fin_mode,
                  int run_mode, int reset_status, cudaStream_t s);
 void launch_set_sel(DevState* st, long long sel, double coef, cudaStream_t s);
+void launch_set_replay(DevState* st, int on, cudaStream_t s);
 int sumsq_parts(long long n);
 void launch_sumsq(const double* v, long long n, double* part, cudaStream_t s);
 void launch_row_sq_seq(const double* A, long long m, long long p, double* out, cudaStream_t s);

@@ -45,7 +45,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // block-wide sum (deterministic tree); result valid in all threads
-__device__ double block_sum(double v, double* red) {
+__device__ double block_sum(double v, double* red) {  // red: ≥ blockDim.x/32 slots
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = warp_sum(v);
     __syncthreads();
@@ -126,28 +126,55 @@ __device__ double warp_dot(const double* __restrict__ row, const double* __restr
 }
 
 // ------------------------------------------------------------------------
-// K4: y = B·R_iᵀ (solver.hpp:270) [+ g = A·A_iᵀ, the Gram column of :294]
-__global__ void __launch_bounds__(kThreads) k_yg(Params P, int with_g) {
+// K4: y = B·R_iᵀ (solver.hpp:270) [+ g = A·A_iᵀ, the Gram column of :294].
+// One 128-thread CTA per output row (grid-stride): 4 warps share a row so the
+// B stream has enough loads in flight even when q is small; fixed-order
+// lane/warp reduction (deterministic).
+constexpr int kYgThreads = 128;
+__global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
+    __shared__ double red[kYgThreads / 32];
     const DevState* st = P.st;
     if (halted(st)) return;
     const long long il = st->sel - P.row0;
     const double* Ri = P.R + il * P.n;
     const double* Ai = P.A + il * P.p;
-    const int lane = threadIdx.x & 31;
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const long long items = P.q + (with_g ? P.m : 0);
-    const bool vb = (P.n & 1) == 0, va = (P.p & 1) == 0;
-    for (long long it = warp; it < items; it += nwarps) {
-        double acc;
+    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        const double* row;
+        const double* v;
+        long long len;
         if (it < P.q) {
-            acc = warp_dot(P.B + it * P.n, Ri, P.n, lane, vb);
-            if (lane == 0) P.y[it] = acc;
+            row = P.B + it * P.n; v = Ri; len = P.n;
         } else {
-            const long long l = it - P.q;
-            acc = warp_dot(P.A + l * P.p, Ai, P.p, lane, va);
-            if (lane == 0) P.g[l] = acc;
+            row = P.A + (it - P.q) * P.p; v = Ai; len = P.p;
         }
+        double a0 = 0.0, a1 = 0.0;
+        if ((len & 1) == 0) {
+            const double2* r2 = reinterpret_cast<const double2*>(row);
+            const double2* v2 = reinterpret_cast<const double2*>(v);
+            const long long h = len >> 1;
+#pragma unroll 8
+            for (long long k = tid; k < h; k += kYgThreads) {
+                const double2 a = __ldcs(r2 + k);
+                const double2 b = __ldg(v2 + k);
+                a0 += a.x * b.x;
+                a1 += a.y * b.y;
+            }
+        } else {
+#pragma unroll 8
+            for (long long k = tid; k < len; k += kYgThreads) a0 += __ldcs(row + k) * __ldg(v + k);
+        }
+        double acc = warp_sum(a0 + a1);
+        if (lane == 0) red[w] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int k = 0; k < kYgThreads / 32; ++k) t += red[k];
+            if (it < P.q) P.y[it] = t;
+            else P.g[it - P.q] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -209,22 +236,46 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
         if (tid == 0) P.zcnt[slab] = 0u;
         return;
     }
-    // ---- X update (solver.hpp:272-290) ----
+    // ---- X update (solver.hpp:272-290): one warp per row t of X ----
     const int xb = blockIdx.x - nzc;
     const long long il = st->sel - P.row0;
     const double* Ai = P.A + il * P.p;
     const double coef = st->coef;
-    const long long total = P.p * P.q;
     const bool track = P.Xref != nullptr;
+    const int lane = tid & 31, warp = tid >> 5;
+    const long long q = P.q;
     double acc = 0.0;
-    for (long long e = (long long)xb * kThreads + tid; e < total; e += (long long)P.x_ctas * kThreads) {
-        const long long t = e / P.q, j = e - t * P.q;
+    for (long long t = (long long)xb * kWarps + warp; t < P.p; t += (long long)P.x_ctas * kWarps) {
         const double f = __dmul_rn(coef, __ldg(Ai + t));
-        const double x1 = __dadd_rn(P.X[e], __dmul_rn(f, __ldg(P.y + j)));
-        P.X[e] = x1;
-        if (track) {
-            const double d1 = x1 - __ldg(P.Xref + e);
-            acc += d1 * d1;
+        double* xr = P.X + t * q;
+        const double* rr = track ? P.Xref + t * q : nullptr;
+        if ((q & 1) == 0) {
+            double2* x2 = reinterpret_cast<double2*>(xr);
+            const double2* y2 = reinterpret_cast<const double2*>(P.y);
+            const double2* f2 = reinterpret_cast<const double2*>(rr);
+            const long long h = q >> 1;
+#pragma unroll 4
+            for (long long k = lane; k < h; k += 32) {
+                double2 x = x2[k];
+                const double2 yy = __ldg(y2 + k);
+                x.x = __dadd_rn(x.x, __dmul_rn(f, yy.x));
+                x.y = __dadd_rn(x.y, __dmul_rn(f, yy.y));
+                x2[k] = x;
+                if (track) {
+                    const double2 rf = __ldg(f2 + k);
+                    const double d0 = x.x - rf.x, d1 = x.y - rf.y;
+                    acc += d0 * d0 + d1 * d1;
+                }
+            }
+        } else {
+            for (long long k = lane; k < q; k += 32) {
+                const double x1 = __dadd_rn(xr[k], __dmul_rn(f, __ldg(P.y + k)));
+                xr[k] = x1;
+                if (track) {
+                    const double d1 = x1 - __ldg(rr + k);
+                    acc += d1 * d1;
+                }
+            }
         }
     }
     if (!track) return;
@@ -260,9 +311,24 @@ struct SelShared {
 };
 
 __device__ int select_rows(const Params& P, DevState* st, int method, double theta,
-                           long long* out_row, SelShared& sh) {
+                           long long* out_row, SelShared& sh, double* scratch,
+                           long long scratch_cap) {
     const int tid = threadIdx.x;
     const long long m = P.m;
+    if (st->replay) {
+        // replay of a given index stream (the reference's): consume the same
+        // RNG draw / cyclic advance the reference's select_* would, take the row
+        if (tid == 0) {
+            const long long row = P.forced_rows[st->k - st->k0];
+            sh.err = (row < 0 || row >= m || !(P.a_sq[row] > 0.0)) ? 2 : 0;
+            sh.cand = row;
+            if (method == 1 || method == 2 || method == 3) (void)rng_next(st->rng);
+            if (method == 0 && !sh.err) st->cyclic_pos = (unsigned long long)((row + 1) % m);
+        }
+        __syncthreads();
+        *out_row = sh.cand;
+        return sh.err;
+    }
     if (method == 4) {  // MWRBK: smallest argmax (solver.hpp:258, 387-400)
         if (st->argmax == LLONG_MAX) return 2;
         *out_row = st->argmax;
@@ -317,25 +383,36 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
                                   __ddiv_rn(__dsub_rn(1.0, theta), P.a_fro_sq));
     const long long seg = (m + kThreads - 1) / kThreads;
     const long long s0 = min(m, (long long)tid * seg), s1 = min(m, s0 + seg);
-    auto member = [&](long long i) -> bool {
+    auto member_g = [&](long long i) -> double {  // member mass, or −1 for non-members
         const double as = P.a_sq[i];
-        if (as <= 0.0) return false;
-        return i == argmax || __ldcg(P.r_sq + i) >= __dmul_rn(__dmul_rn(zeta, as), r_fro);
+        if (as <= 0.0) return -1.0;
+        const double rs = __ldcg(P.r_sq + i);
+        return (i == argmax || rs >= __dmul_rn(__dmul_rn(zeta, as), r_fro)) ? rs : -1.0;
     };
+    // one coalesced pass stages the member masses in shared memory, so the
+    // ordered segment scans below run at smem latency instead of L2 latency
+    const bool staged = scratch != nullptr && m <= scratch_cap;
+    if (staged) {
+        for (long long i = tid; i < m; i += blockDim.x) scratch[i] = member_g(i);
+        __syncthreads();
+    }
+    auto mass_of = [&](long long i) -> double { return staged ? scratch[i] : member_g(i); };
     double local = 0.0;
-    for (long long i = s0; i < s1; ++i)
-        if (member(i)) local = __dadd_rn(local, __ldcg(P.r_sq + i));
-    // exclusive scan of the per-thread segment sums (Hillis–Steele, fixed order)
-    sh.scan[tid] = local;
+    for (long long i = s0; i < s1; ++i) {
+        const double w = mass_of(i);
+        if (w >= 0.0) local = __dadd_rn(local, w);
+    }
+    const bool scan_lane = tid < kThreads;  // blocks may carry an extra producer warp
+    if (scan_lane) sh.scan[tid] = local;
     __syncthreads();
     for (int off = 1; off < kThreads; off <<= 1) {
-        const double v = tid >= off ? sh.scan[tid - off] : 0.0;
+        const double v = (scan_lane && tid >= off) ? sh.scan[tid - off] : 0.0;
         __syncthreads();
-        sh.scan[tid] = __dadd_rn(sh.scan[tid], v);
+        if (scan_lane) sh.scan[tid] = __dadd_rn(sh.scan[tid], v);
         __syncthreads();
     }
     const double total = sh.scan[kThreads - 1];
-    const double excl = tid ? sh.scan[tid - 1] : 0.0;
+    const double excl = (scan_lane && tid) ? sh.scan[tid - 1] : 0.0;
     if (!(total > 0.0)) return 2;  // mass on zero rows only (solver.hpp:249-252)
     if (tid == 0) {
         sh.u = rng_unit(st->rng);
@@ -350,8 +427,9 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
     {
         double cum = excl;
         for (long long i = s0; i < s1; ++i) {
-            if (!member(i)) continue;
-            const double nc = __dadd_rn(cum, __ldcg(P.r_sq + i));
+            const double w = mass_of(i);
+            if (w < 0.0) continue;
+            const double nc = __dadd_rn(cum, w);
             if (nc > target) {
                 mine = i;
                 lo_c = cum;
@@ -385,15 +463,18 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
             // upper_bound, then walk back over a trailing zero-weight plateau.
             const double u = sh.u;
             double total_seq = 0.0;
-            for (long long i = 0; i < m; ++i)
-                if (member(i)) total_seq = __dadd_rn(total_seq, __ldcg(P.r_sq + i));
+            for (long long i = 0; i < m; ++i) {
+                const double w = mass_of(i);
+                if (w >= 0.0) total_seq = __dadd_rn(total_seq, w);
+            }
             const double tseq = __dmul_rn(u, total_seq);
             double cum = 0.0;
             long long found = -1, first_member = -1, last_change = -1;
             for (long long i = 0; i < m && found < 0; ++i) {
-                if (!member(i)) continue;
+                const double w = mass_of(i);
+                if (w < 0.0) continue;
                 if (first_member < 0) first_member = i;
-                const double nc = __dadd_rn(cum, __ldcg(P.r_sq + i));
+                const double nc = __dadd_rn(cum, w);
                 if (nc > tseq) found = i;
                 if (nc != cum) last_change = i;
                 cum = nc;
@@ -411,7 +492,8 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
 }
 
 // block-level finalize + selection shared by k_r's last block and k_select
-__device__ void finish_select(const Params& P, DevState* st, SelShared& sh) {
+__device__ void finish_select(const Params& P, DevState* st, SelShared& sh, double* scratch,
+                              long long scratch_cap) {
     long long row = 0;
     if (threadIdx.x == 0) {
         for (int k = 0; k < 4; ++k) st->rng_snap[k] = st->rng[k];
@@ -420,7 +502,7 @@ __device__ void finish_select(const Params& P, DevState* st, SelShared& sh) {
         sh.err = 0;
     }
     __syncthreads();
-    const int err = select_rows(P, st, P.method, P.theta, &row, sh);
+    const int err = select_rows(P, st, P.method, P.theta, &row, sh, scratch, scratch_cap);
     __syncthreads();
     if (threadIdx.x == 0) {
         if (err) {
@@ -436,107 +518,17 @@ __device__ void finish_select(const Params& P, DevState* st, SelShared& sh) {
     }
 }
 
-// ------------------------------------------------------------------------
-// K2: fused residual update + row norms + reductions (+ finalize / K3 select)
-template <bool UPDATE, bool VEC2>
-__global__ void __launch_bounds__(kThreads) k_r(Params P) {
-    extern __shared__ double smem[];
-    __shared__ double redv[kWarps];
-    __shared__ long long redi[kWarps];
-    __shared__ bool last;
+// Everything after the streaming pass of K2: write ‖R_l‖², per-CTA records, and
+// in the last CTA to finish the fixed-order reduction, the stop / divergence
+// logic (solver.hpp:306-307, :347, :351) and K3 for the next iteration.
+// rowacc[t] holds ‖R_{r0+t}‖²; all threads of the block must call it.
+// Last-CTA finalize of an iteration (or of a norms pass): publish ‖R‖², max ratio
+// and argmax, run the divergence / stop logic and pre-select the next row.
+template <bool UPDATE>
+__device__ void finalize(const Params& P, DevState* st, double s, double mx, long long ax,
+                         double* scratch, long long scratch_cap) {
     __shared__ SelShared sh;
-    DevState* st = P.st;
-    if (UPDATE && halted(st)) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long m = P.m, n = P.n;
-    const long long r0 = (long long)blockIdx.x * P.r_rows_per_cta;
-    const long long r1 = min(m, r0 + P.r_rows_per_cta);
-    double* zs = smem;
-    double* rowacc = smem + P.r_chunk;
-    double coef = 0.0;
-    long long sel = 0;
-    if (UPDATE) {
-        coef = st->coef;
-        sel = st->sel;
-    }
-    for (long long t = tid; t < r1 - r0; t += kThreads) rowacc[t] = 0.0;
-    for (long long c0 = 0; c0 < n; c0 += P.r_chunk) {
-        const long long cw = min((long long)P.r_chunk, n - c0);
-        __syncthreads();
-        if (UPDATE)
-            for (long long t = tid; t < cw; t += kThreads) zs[t] = __ldg(P.z + c0 + t);
-        __syncthreads();
-        for (long long l = r0 + warp; l < r1; l += kWarps) {
-            double f = 0.0;
-            if (UPDATE) {
-                const double gl = P.G ? __ldg(P.G + sel * m + l) : __ldg(P.g + l);
-                f = __dmul_rn(coef, gl);  // solver.hpp:296
-            }
-            double* row = P.R + l * n + c0;
-            double acc = 0.0;
-            if (VEC2) {
-                double2* r2 = reinterpret_cast<double2*>(row);
-                const double2* z2 = reinterpret_cast<const double2*>(zs);
-                const long long h = cw >> 1;
-#pragma unroll 8
-                for (long long k = lane; k < h; k += 32) {
-                    double2 r = __ldcs(r2 + k);
-                    if (UPDATE) {
-                        const double2 zz = z2[k];
-                        r.x = __dsub_rn(r.x, __dmul_rn(f, zz.x));  // solver.hpp:300
-                        r.y = __dsub_rn(r.y, __dmul_rn(f, zz.y));
-                        __stcs(r2 + k, r);
-                    }
-                    acc += r.x * r.x;  // solver.hpp:301 (tree order here)
-                    acc += r.y * r.y;
-                }
-            } else {
-#pragma unroll 4
-                for (long long k = lane; k < cw; k += 32) {
-                    double r = row[k];
-                    if (UPDATE) {
-                        r = __dsub_rn(r, __dmul_rn(f, zs[k]));
-                        row[k] = r;
-                    }
-                    acc += r * r;
-                }
-            }
-            acc = warp_sum(acc);
-            if (lane == 0) rowacc[l - r0] += acc;
-        }
-    }
-    __syncthreads();
-    double bsum = 0.0, bmax = -INFINITY;
-    long long barg = LLONG_MAX;
-    for (long long t = tid; t < r1 - r0; t += kThreads) {
-        const long long l = r0 + t;
-        const double rs = rowacc[t];
-        P.r_sq[l] = rs;
-        bsum += rs;
-        const double as = P.a_sq[l];
-        if (as > 0.0) maxidx_merge(bmax, barg, __ddiv_rn(rs, as), P.row0 + l);
-    }
-    bsum = block_sum(bsum, redv);
-    block_maxidx(bmax, barg, redv, redi);
-    if (tid == 0) {
-        P.rrec[blockIdx.x] = RowRecord{bsum, bmax, barg, 0.0};
-        __threadfence();
-        last = atomicAdd(&st->cnt_r, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last) return;
-    // ---- last CTA: reduce the records (fixed order), finalize the iteration ----
-    __threadfence();
-    double s = 0.0, mx = -INFINITY;
-    long long ax = LLONG_MAX;
-    for (int k = tid; k < (int)gridDim.x; k += kThreads) {
-        const double* rp = reinterpret_cast<const double*>(P.rrec + k);
-        const RowRecord rc{__ldcg(rp), __ldcg(rp + 1), __ldcg(reinterpret_cast<const long long*>(rp + 2)), 0.0};
-        s += rc.sum;
-        maxidx_merge(mx, ax, rc.max_ratio, rc.argmax);
-    }
-    s = block_sum(s, redv);
-    block_maxidx(mx, ax, redv, redi);
+    const int tid = threadIdx.x;
     const int mode = UPDATE ? st->fin_mode : FIN_NORMS;
     __syncthreads();
     if (tid == 0) {
@@ -571,23 +563,357 @@ __global__ void __launch_bounds__(kThreads) k_r(Params P) {
     }
     __syncthreads();
     if (mode == FIN_ITERATION && st->status == ST_RUN && st->k < st->k_limit)
-        finish_select(P, st, sh);
+        finish_select(P, st, sh, scratch, scratch_cap);
+}
+
+template <bool UPDATE>
+__device__ void r_tail(const Params& P, DevState* st, long long r0, long long r1,
+                       const double* rowacc, double* scratch, long long scratch_cap) {
+    __shared__ double redv[32];
+    __shared__ long long redi[32];
+    __shared__ bool last;
+    const int tid = threadIdx.x;
+    double bsum = 0.0, bmax = -INFINITY;
+    long long barg = LLONG_MAX;
+    for (long long t = tid; t < r1 - r0; t += blockDim.x) {
+        const long long l = r0 + t;
+        const double rs = rowacc[t];
+        P.r_sq[l] = rs;
+        bsum += rs;
+        const double as = P.a_sq[l];
+        if (as > 0.0) maxidx_merge(bmax, barg, __ddiv_rn(rs, as), P.row0 + l);
+    }
+    bsum = block_sum(bsum, redv);
+    block_maxidx(bmax, barg, redv, redi);
+    if (tid == 0) {
+        P.rrec[blockIdx.x] = RowRecord{bsum, bmax, barg, 0.0};
+        __threadfence();
+        last = atomicAdd(&st->cnt_r, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    // ---- last CTA: reduce the records (fixed order), finalize the iteration ----
+    __threadfence();
+    double s = 0.0, mx = -INFINITY;
+    long long ax = LLONG_MAX;
+    for (int k = tid; k < (int)gridDim.x; k += blockDim.x) {
+        const double* rp = reinterpret_cast<const double*>(P.rrec + k);
+        const RowRecord rc{__ldcg(rp), __ldcg(rp + 1), __ldcg(reinterpret_cast<const long long*>(rp + 2)), 0.0};
+        s += rc.sum;
+        maxidx_merge(mx, ax, rc.max_ratio, rc.argmax);
+    }
+    s = block_sum(s, redv);
+    block_maxidx(mx, ax, redv, redi);
+    finalize<UPDATE>(P, st, s, mx, ax, scratch, scratch_cap);
+}
+
+// ------------------------------------------------------------------------
+// K2: fused residual update + row norms + reductions (+ finalize / K3 select)
+template <bool UPDATE, bool VEC2>
+__global__ void __launch_bounds__(kThreads) k_r(Params P) {
+    extern __shared__ double smem[];
+    DevState* st = P.st;
+    if (UPDATE && halted(st)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long m = P.m, n = P.n;
+    const long long r0 = (long long)blockIdx.x * P.r_rows_per_cta;
+    const long long r1 = min(m, r0 + P.r_rows_per_cta);
+    double* zs = smem;
+    double* rowacc = smem + P.r_chunk;
+    double coef = 0.0;
+    long long sel = 0;
+    if (UPDATE) {
+        coef = st->coef;
+        sel = st->sel;
+    }
+    for (long long t = tid; t < r1 - r0; t += kThreads) rowacc[t] = 0.0;
+    for (long long c0 = 0; c0 < n; c0 += P.r_chunk) {
+        const long long cw = min((long long)P.r_chunk, n - c0);
+        __syncthreads();
+        if (UPDATE)
+            for (long long t = tid; t < cw; t += kThreads) zs[t] = __ldg(P.z + c0 + t);
+        __syncthreads();
+        for (long long l = r0 + warp; l < r1; l += kWarps) {
+            double f = 0.0;
+            if (UPDATE) {
+                const double gl = P.G ? __ldg(P.G + sel * m + l) : __ldg(P.g + l);
+                f = __dmul_rn(coef, gl);  // solver.hpp:296
+            }
+            double* row = P.R + l * n + c0;
+            double acc = 0.0;
+            // explicit batches of kU independent 128-bit loads per lane before any
+            // store, so each warp keeps kU×512 B of R in flight (the compiler will
+            // not hoist loads across the streaming stores on its own)
+            constexpr int kU = 8;
+            if (VEC2) {
+                double2* r2 = reinterpret_cast<double2*>(row);
+                const double2* z2 = reinterpret_cast<const double2*>(zs);
+                const long long h = cw >> 1;
+                for (long long kb = lane; kb < h; kb += 32 * kU) {
+                    double2 rv[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u)
+                        if (kb + 32 * u < h) rv[u] = __ldcs(r2 + kb + 32 * u);
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const long long k = kb + 32 * u;
+                        if (k < h) {
+                            double2 r = rv[u];
+                            if (UPDATE) {
+                                const double2 zz = z2[k];
+                                r.x = __dsub_rn(r.x, __dmul_rn(f, zz.x));  // solver.hpp:300
+                                r.y = __dsub_rn(r.y, __dmul_rn(f, zz.y));
+                                __stcs(r2 + k, r);
+                            }
+                            acc += r.x * r.x;  // solver.hpp:301 (tree order here)
+                            acc += r.y * r.y;
+                        }
+                    }
+                }
+            } else {
+                for (long long kb = lane; kb < cw; kb += 32 * kU) {
+                    double rv[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u)
+                        if (kb + 32 * u < cw) rv[u] = row[kb + 32 * u];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const long long k = kb + 32 * u;
+                        if (k < cw) {
+                            double r = rv[u];
+                            if (UPDATE) {
+                                r = __dsub_rn(r, __dmul_rn(f, zs[k]));
+                                row[k] = r;
+                            }
+                            acc += r * r;
+                        }
+                    }
+                }
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) rowacc[l - r0] += acc;
+        }
+    }
+    __syncthreads();
+    r_tail<UPDATE>(P, st, r0, r1, rowacc, smem, P.r_chunk);
+}
+
+// ------------------------------------------------------------------------
+// K2 (even n, the production path): the same fused update, with R streamed
+// through shared memory by 1-D bulk TMA copies (cp.async.bulk, SASS UBLKCP) in a
+// kTmaStages-deep mbarrier ring.  One producer warp issues the copies; eight
+// consumer warps apply R_l −= (coef·g_l)·z from shared memory, write the result
+// straight back with streaming stores and accumulate ‖R_l‖².  Each CTA owns a
+// contiguous block of rows and walks it in row-major tiles of r_chunk columns,
+// so DRAM sees one sequential read stream and one write stream per CTA, and the
+// bytes in flight per SM (stages × tile × CTAs) do not depend on registers.
+constexpr int kTmaConsumerWarps = 8;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+
+__device__ __forceinline__ unsigned smem_u32(const void* ptr) {
+    return (unsigned)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    while (!mbar_try(b, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <bool UPDATE>
+__global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ long long stage_row[32];
+    __shared__ double rp[2][kTmaConsumerWarps];
+    __shared__ double redv[32];
+    __shared__ long long redi[32];
+    __shared__ bool last;
+    DevState* st = P.st;
+    if (UPDATE && halted(st)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long m = P.m, n = P.n;
+    const int TW = P.r_chunk;
+    const int tpr = (int)((n + TW - 1) / TW);
+    const int S = P.r_stages;
+    double* stage = reinterpret_cast<double*>(dsm);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(dsm + (size_t)S * TW * 8);
+    unsigned long long* empty = full + S;
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kTmaConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    double cmax = -INFINITY;
+    long long carg = LLONG_MAX;
+    if (warp == kTmaConsumerWarps) {
+        // ---- producer: grab rows dynamically, stream their tiles into the ring ----
+        if (lane == 0) {
+            int s = 0;
+            unsigned round = 0;
+            for (;;) {
+                const long long row = (long long)atomicAdd(&st->r_next, 1ull);
+                const bool done = row >= m;
+                const long long ntiles = done ? 1 : tpr;
+                const double* src = P.R + row * n;
+                for (long long seg = 0; seg < ntiles; ++seg, src += TW) {
+                    if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+                    stage_row[s] = done ? -1 : row;
+                    if (done) {
+                        mbar_arrive(&full[s]);  // sentinel: no bytes
+                    } else {
+                        const unsigned bytes = (unsigned)(min((long long)TW, n - seg * TW) * 8);
+                        mbar_expect_tx(&full[s], bytes);
+                        tma_load_1d(stage + (size_t)s * TW, src, bytes, &full[s]);
+                    }
+                    if (++s == S) {
+                        s = 0;
+                        ++round;
+                    }
+                }
+                if (done) break;
+            }
+        }
+    } else {
+        // ---- 8 consumer warps ----
+        double coef = 0.0;
+        long long sel = 0;
+        if (UPDATE) {
+            coef = st->coef;
+            sel = st->sel;
+        }
+        int s = 0, buf = 0;
+        unsigned round = 0;
+        for (;;) {
+            mbar_wait(&full[s], round & 1);
+            const long long row = stage_row[s];
+            if (row < 0) break;
+            double f = 0.0;
+            if (UPDATE) {
+                const double gl = P.G ? __ldg(P.G + sel * m + row) : __ldg(P.g + row);
+                f = __dmul_rn(coef, gl);  // solver.hpp:296
+            }
+            double acc = 0.0;
+            long long c0 = 0;
+            for (int seg = 0; seg < tpr; ++seg, c0 += TW) {
+                if (seg > 0) mbar_wait(&full[s], round & 1);
+                const int h = (int)(min((long long)TW, n - c0) >> 1);
+                const double2* src = reinterpret_cast<const double2*>(stage + (size_t)s * TW);
+                double2* dst = reinterpret_cast<double2*>(P.R + row * n + c0);
+                const double2* z2 = reinterpret_cast<const double2*>(P.z + c0);
+#pragma unroll 4
+                for (int k = tid; k < h; k += kTmaConsumerWarps * 32) {
+                    double2 r = src[k];
+                    if (UPDATE) {
+                        const double2 zz = __ldg(z2 + k);
+                        r.x = __dsub_rn(r.x, __dmul_rn(f, zz.x));  // solver.hpp:300
+                        r.y = __dsub_rn(r.y, __dmul_rn(f, zz.y));
+                        __stcs(dst + k, r);
+                    }
+                    acc += r.x * r.x;  // solver.hpp:301 (tree order here)
+                    acc += r.y * r.y;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (++s == S) {
+                    s = 0;
+                    ++round;
+                }
+            }
+            // ‖R_row‖²: fixed-order combine of the 8 warp partials
+            acc = warp_sum(acc);
+            if (lane == 0) rp[buf][warp] = acc;
+            asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+            if (tid == 0) {
+                double a = 0.0;
+                for (int w = 0; w < kTmaConsumerWarps; ++w) a += rp[buf][w];
+                P.r_sq[row] = a;
+                const double as = P.a_sq[row];
+                if (as > 0.0) maxidx_merge(cmax, carg, __ddiv_rn(a, as), P.row0 + row);
+            }
+            buf ^= 1;
+        }
+    }
+    // records: max/argmax only (order-independent); ‖R‖² is summed over the
+    // rows in fixed order by the last CTA, so the dynamic row-to-CTA mapping
+    // cannot change its rounding.
+    __syncthreads();
+    if (tid == 0) {
+        P.rrec[blockIdx.x] = RowRecord{0.0, cmax, carg, 0.0};
+        __threadfence();
+        last = atomicAdd(&st->cnt_r, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double sum = 0.0, mx = -INFINITY;
+    long long ax = LLONG_MAX;
+    {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const long long T = blockDim.x;
+        long long l = tid;
+        for (; l + 3 * T < m; l += 4 * T) {
+            a0 += __ldcg(P.r_sq + l);
+            a1 += __ldcg(P.r_sq + l + T);
+            a2 += __ldcg(P.r_sq + l + 2 * T);
+            a3 += __ldcg(P.r_sq + l + 3 * T);
+        }
+        for (; l < m; l += T) a0 += __ldcg(P.r_sq + l);
+        sum = (a0 + a1) + (a2 + a3);
+    }
+    for (int k = tid; k < (int)gridDim.x; k += blockDim.x) {
+        const double* rpp = reinterpret_cast<const double*>(P.rrec + k);
+        maxidx_merge(mx, ax, __ldcg(rpp + 1), __ldcg(reinterpret_cast<const long long*>(rpp + 2)));
+    }
+    sum = block_sum(sum, redv);
+    block_maxidx(mx, ax, redv, redi);
+    if (tid == 0) st->r_next = 0ull;
+    // the TMA ring is idle now: reuse it as selection scratch
+    finalize<UPDATE>(P, st, sum, mx, ax, stage, (long long)S * TW);
+}
+
+size_t tma_smem_bytes(const Params& P) {
+    return (size_t)P.r_stages * P.r_chunk * 8 + 2 * P.r_stages * 8;
 }
 
 // K3 standalone: (re)select with the configured rule (consume=0: speculative,
 // snapshot kept) or run a public select_*(θ) that consumes the stream (consume=1).
 __global__ void __launch_bounds__(kThreads) k_select(Params P, int method, double theta,
-                                                    int consume) {
+                                                    int consume, long long scratch_cap) {
+    extern __shared__ double scratch[];
     __shared__ SelShared sh;
     DevState* st = P.st;
     if (!consume) {
-        finish_select(P, st, sh);
+        finish_select(P, st, sh, scratch, scratch_cap);
         return;
     }
     long long row = 0;
     if (threadIdx.x == 0) sh.err = 0;
     __syncthreads();
-    const int err = select_rows(P, st, method, theta, &row, sh);
+    const int err = select_rows(P, st, method, theta, &row, sh, scratch, scratch_cap);
     __syncthreads();
     if (threadIdx.x == 0) {
         st->sel_valid = 0;
@@ -767,6 +1093,8 @@ __global__ void k_ctrl(DevState* st, unsigned long long k0, unsigned long long k
     }
 }
 
+__global__ void k_set_replay(DevState* st, int on) { st->replay = on; }
+
 __global__ void k_set_sel(DevState* st, long long sel, double coef) {
     st->sel = sel;
     st->coef = coef;
@@ -817,7 +1145,7 @@ __global__ void k_cumsum_seq(const double* a_sq, long long m, double* cum, doubl
 // launchers
 
 void launch_yg(const Params& P, cudaStream_t s, bool with_g) {
-    k_yg<<<P.yg_grid, kThreads, 0, s>>>(P, with_g ? 1 : 0);
+    k_yg<<<P.yg_grid, kYgThreads, 0, s>>>(P, with_g ? 1 : 0);
 }
 
 void launch_zx(const Params& P, cudaStream_t s) {
@@ -825,6 +1153,31 @@ void launch_zx(const Params& P, cudaStream_t s) {
 }
 
 void launch_r(const Params& P, cudaStream_t s, bool update) {
+    if (P.r_tma) {
+        const size_t smem = tma_smem_bytes(P);
+        static size_t attr_set = 0;
+        if (attr_set < smem) {  // opt in up to (device limit − static smem)
+            int dev = 0, optin = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, k_r_tma<true>);
+            const int dyn = optin - (int)fa.sharedSizeBytes;
+            cudaFuncSetAttribute(k_r_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            // carve out only the shared memory the resident CTAs need, so the
+            // rest of the 256 KB stays L1 for the z vector (read via __ldg)
+            const int cps = std::max(1, (P.r_grid + 147) / 148);
+            int pct = (int)((100.0 * cps * (smem + fa.sharedSizeBytes + 1024)) / optin + 0.999);
+            pct = std::min(100, std::max(pct, 1));
+            cudaFuncSetAttribute(k_r_tma<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            attr_set = (size_t)dyn;
+        }
+        if (update) k_r_tma<true><<<P.r_grid, kTmaThreads, smem, s>>>(P);
+        else k_r_tma<false><<<P.r_grid, kTmaThreads, smem, s>>>(P);
+        return;
+    }
     const size_t smem = sizeof(double) * (size_t)(P.r_chunk + P.r_rows_per_cta);
     const bool v2 = (P.n & 1) == 0;
     if (update) {
@@ -837,7 +1190,8 @@ void launch_r(const Params& P, cudaStream_t s, bool update) {
 }
 
 void launch_select(const Params& P, cudaStream_t s, int method, double theta, int consume) {
-    k_select<<<1, kThreads, 0, s>>>(P, method, theta, consume);
+    const long long cap = P.m <= 6144 ? P.m : 0;  // ≤48 KB static-limit scratch
+    k_select<<<1, kThreads, (size_t)cap * 8, s>>>(P, method, theta, consume, cap);
 }
 
 void launch_query(const Params& P, cudaStream_t s, double theta, int want_set) {
@@ -874,6 +1228,8 @@ void launch_ctrl(DevState* st, unsigned long long k0, unsigned long long k_limit
                  int run_mode, int reset_status, cudaStream_t s) {
     k_ctrl<<<1, 1, 0, s>>>(st, k0, k_limit, fin_mode, run_mode, reset_status);
 }
+
+void launch_set_replay(DevState* st, int on, cudaStream_t s) { k_set_replay<<<1, 1, 0, s>>>(st, on); }
 
 void launch_set_sel(DevState* st, long long sel, double coef, cudaStream_t s) {
     k_set_sel<<<1, 1, 0, s>>>(st, sel, coef);

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -123,6 +124,17 @@ double spectral_norm_host(const std::vector<double>& b, size_t rows, size_t cols
 
 bool trace_point_due(uint64_t k) { return k < 10000 || k % 10 == 0; }  // solver.hpp:136
 
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// AXB_R_KERNEL=simple selects the register-streaming K2 (A/B comparisons)
+bool opt_r_tma() {
+    const char* e = std::getenv("AXB_R_KERNEL");
+    return !(e && std::strcmp(e, "simple") == 0);
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -147,7 +159,7 @@ struct axb_solver {
         gemm_sq, gemm_diff, scal, tr_metric, tr_rel, sq_part;
     DevBuf<unsigned int> zcnt;
     DevBuf<RowRecord> rrec;
-    DevBuf<long long> tr_row;
+    DevBuf<long long> tr_row, forced;
     DevBuf<int> flags;
     DevBuf<DevState> st;
     DevState* hs = nullptr;  // pinned host mirror
@@ -164,6 +176,8 @@ struct axb_solver {
     double* h_trace_metric = nullptr;
     double* h_trace_rel = nullptr;
     std::string err;
+    uint64_t err_k = 0;
+    double err_val = 0.0;
     // timing
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool profiling = false;
@@ -184,9 +198,13 @@ struct axb_solver {
     }
 
     // ---------------------------------------------------------------- utils
-    void sync(const char* what) { ck(cudaStreamSynchronize(stream), what); }
+    void sync(const char* what) {
+        ck(cudaGetLastError(), what);
+        ck(cudaStreamSynchronize(stream), what);
+    }
 
     void pull_state() {
+        ck(cudaGetLastError(), "kernel launch");
         ck(cudaMemcpyAsync(hs, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, stream), "state");
         sync("state sync");
     }
@@ -381,25 +399,38 @@ struct axb_solver {
         P.row0 = 0;
         P.m_global = (long long)m;
         const int target = 148 * 4;
-        int rgrid = (int)std::min<uint64_t>((uint64_t)target, std::max<uint64_t>(1, (m + 7) / 8));
-        P.r_rows_per_cta = (int)((m + rgrid - 1) / rgrid);
-        P.r_grid = (int)((m + P.r_rows_per_cta - 1) / P.r_rows_per_cta);
-        P.r_chunk = (int)std::min<uint64_t>(n, 4096);
-        if (P.r_chunk & 1) P.r_chunk += (n > (uint64_t)P.r_chunk) ? 1 : 0;
+        P.r_tma = (n % 2 == 0) && opt_r_tma();
+        if (P.r_tma) {
+            // TMA ring: 2 CTAs per SM, rows split evenly, tiles of ≤2048 columns
+            // (tunable for sweeps: AXB_R_CPS, AXB_R_STAGES, AXB_R_TILE)
+            const int cps = env_int("AXB_R_CPS", 2), stages = env_int("AXB_R_STAGES", 4);
+            const int tile = env_int("AXB_R_TILE", 2048);
+            P.r_grid = (int)std::min<uint64_t>((uint64_t)148 * cps, m);
+            P.r_rows_per_cta = (int)((m + P.r_grid - 1) / P.r_grid);
+            P.r_chunk = (int)std::min<uint64_t>(n, (uint64_t)tile);
+            P.r_stages = std::max(2, std::min(stages, 16));
+        } else {
+            int rgrid = (int)std::min<uint64_t>((uint64_t)target, std::max<uint64_t>(1, (m + 7) / 8));
+            P.r_rows_per_cta = (int)((m + rgrid - 1) / rgrid);
+            P.r_grid = (int)((m + P.r_rows_per_cta - 1) / P.r_rows_per_cta);
+            P.r_chunk = (int)std::min<uint64_t>(n, 4096);
+            if (P.r_chunk & 1) P.r_chunk += (n > (uint64_t)P.r_chunk) ? 1 : 0;
+        }
         const uint64_t items = q + (gram_cached ? 0 : m);
-        P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(148 * 8, (items + 7) / 8));
+        P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(148 * 16, items));
         P.z_nslab = (int)((n + 511) / 512);
         int nj = (int)std::max<uint64_t>(1, std::min<uint64_t>((target + P.z_nslab - 1) / P.z_nslab,
                                                                 (q + 7) / 8));
         P.z_jrows = (int)((q + nj - 1) / nj);
         P.z_nj = (int)((q + P.z_jrows - 1) / P.z_jrows);
-        P.x_ctas = (int)std::max<uint64_t>(1, std::min<uint64_t>(296, (p * q + 1023) / 1024));
+        P.x_ctas = (int)std::max<uint64_t>(1, std::min<uint64_t>(296, (p + 7) / 8));
         zpart.alloc((size_t)P.z_nj * n, "zpart");
         zcnt.alloc(P.z_nslab, "zcnt");
         ck(cudaMemsetAsync(zcnt.p, 0, sizeof(unsigned) * P.z_nslab, stream), "zcnt");
         xpart.alloc(2 * 1184, "xpart");
         rrec.alloc(P.r_grid, "rrec");
         tr_row.alloc(trace_cap, "trace");
+        forced.alloc(trace_cap, "forced rows");
         tr_metric.alloc(trace_cap, "trace");
         tr_rel.alloc(trace_cap, "trace");
         flags.alloc(m, "flags");
@@ -411,6 +442,7 @@ struct axb_solver {
         P.g = g.p; P.y = y.p; P.z = z.p; P.zpart = zpart.p; P.zcnt = zcnt.p; P.xpart = xpart.p;
         P.rrec = rrec.p; P.trace_row = tr_row.p; P.trace_metric = tr_metric.p;
         P.trace_rel = tr_rel.p; P.trace_cap = trace_cap; P.member_flags = flags.p; P.st = st.p;
+        P.forced_rows = forced.p;
         P.alpha = alpha;
         P.theta = cfg.method == AXB_RGRBK ? cfg.theta : 0.5;
         P.a_fro_sq = a_fro_sq;
@@ -528,6 +560,7 @@ struct axb_solver {
     void ensure_selection() {
         if (!sel_valid) {
             launch_select(P, stream, cfg.method, P.theta, 0);
+            ++kernel_launches;
             sel_valid = true;  // confirmed (or error) at the next state pull
         }
     }
@@ -556,6 +589,7 @@ struct axb_solver {
     // runs up to nb iterations from the current k; returns iterations executed
     uint64_t batch(uint64_t nb, int run_mode) {
         launch_ctrl(st.p, k, k + nb, FIN_ITERATION, run_mode, 0, stream);
+        ++kernel_launches;
         ensure_selection();
         if (profiling) {
             if (prof_ev.size() < 2 * nb) {
@@ -626,6 +660,44 @@ struct axb_solver {
         }
         cudaEventRecord(ev1, stream);
         sync("steps");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        loop_ms = ms;
+    }
+
+    // k iterations on a given index stream (the reference's), e.g. to replay a
+    // randomized run: X, R and the metrics follow exactly as step() would
+    void replay(uint64_t count, const uint64_t* rows_in, bool mirror_refresh) {
+        reset_status();
+        rollback();
+        launch_set_replay(st.p, 1, stream);
+        std::vector<long long> chunk(trace_cap);
+        uint64_t got = 0;
+        cudaEventRecord(ev0, stream);
+        try {
+            while (got < count) {
+                uint64_t nb = std::min<uint64_t>(count - got, trace_cap);
+                const uint64_t ri = cfg.refresh_interval;
+                if (mirror_refresh && ri > 0) nb = std::min<uint64_t>(nb, ri - k % ri);
+                for (uint64_t t = 0; t < nb; ++t) chunk[t] = (long long)rows_in[got + t];
+                ck(cudaMemcpyAsync(forced.p, chunk.data(), sizeof(long long) * nb,
+                                   cudaMemcpyHostToDevice, stream), "forced rows");
+                sel_valid = false;  // the first selection of the batch reads slot 0
+                const uint64_t done = batch(nb, 0);
+                got += done;
+                if (done != nb) fail(AXB_CUDA_ERROR, "replay stopped early");
+                if (mirror_refresh && ri > 0 && k % ri == 0) checkpoint();
+                sync("replay chunk");  // chunk buffer reuse
+            }
+        } catch (...) {
+            launch_set_replay(st.p, 0, stream);
+            sel_valid = false;
+            throw;
+        }
+        cudaEventRecord(ev1, stream);
+        launch_set_replay(st.p, 0, stream);
+        sel_valid = false;
+        sync("replay");
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev0, ev1);
         loop_ms = ms;
@@ -823,7 +895,11 @@ int guarded(axb_solver* s, F&& f) {
         f();
         return AXB_OK;
     } catch (const AxbError& e) {
-        if (s) s->err = e.msg;
+        if (s) {
+            s->err = e.msg;
+            s->err_k = e.k;
+            s->err_val = e.val;
+        }
         return e.code;
     } catch (const std::exception& e) {
         if (s) s->err = e.what();
@@ -881,6 +957,9 @@ int axb_solver_step(axb_solver* s, uint64_t* row) {
 }
 int axb_solver_steps(axb_solver* s, uint64_t k, uint64_t* rows, int32_t mirror_refresh) {
     return guarded(s, [&] { s->steps(k, rows, mirror_refresh != 0); });
+}
+int axb_solver_replay(axb_solver* s, uint64_t k, const uint64_t* rows, int32_t mirror_refresh) {
+    return guarded(s, [&] { s->replay(k, rows, mirror_refresh != 0); });
 }
 int axb_solver_update_row(axb_solver* s, uint64_t i) {
     return guarded(s, [&] { s->update_row(i); });
@@ -983,6 +1062,11 @@ int axb_solver_last_timing(const axb_solver* s, double* loop_ms, double* k2_ms,
     if (k2_ms) *k2_ms = s->k2_ms;
     if (k2_launches) *k2_launches = s->k2_launches;
     if (kernel_launches) *kernel_launches = s->kernel_launches;
+    return AXB_OK;
+}
+int axb_solver_last_error_info(const axb_solver* s, uint64_t* iteration, double* value) {
+    if (iteration) *iteration = s->err_k;
+    if (value) *value = s->err_val;
     return AXB_OK;
 }
 int axb_solver_set_profiling(axb_solver* s, int32_t on) {

@@ -274,6 +274,10 @@ class Solver:
 
     def _chk(self, st, **kw):
         if st:
+            if not kw:
+                k = C.c_uint64(); v = C.c_double()
+                self._lib.axb_solver_last_error_info(self._h, C.byref(k), C.byref(v))
+                kw = {"iteration": k.value, "residual_norm": v.value}
             raise_status(st, self._lib.axb_solver_last_error(self._h).decode(), **kw)
 
     # -- selection rules (solver.hpp:197-258) --
@@ -329,6 +333,12 @@ class Solver:
         self._chk(self._lib.axb_solver_steps(self._h, int(k), rows.ctypes.data_as(_u64p),
                                              1 if mirror_refresh else 0))
         return rows[: int(k)]
+
+    def replay(self, rows, mirror_refresh=False):
+        """Iterate on a given index stream (e.g. the reference's trace)."""
+        r = np.ascontiguousarray(rows, dtype=np.uint64)
+        self._chk(self._lib.axb_solver_replay(self._h, int(r.size), r.ctypes.data_as(_u64p),
+                                              1 if mirror_refresh else 0))
 
     def run(self) -> SolveReport:
         cap = 0

@@ -170,6 +170,11 @@ class OracleLib(_Lib):
         self.get_r_sq = self._f("solver_get_r_sq", None, [C.c_void_p, _dp])
         self.get_a_sq = self._f("solver_get_a_sq", None, [C.c_void_p, _dp])
         self.rng_state = self._f("solver_rng_state", None, [C.c_void_p, _u64p])
+        self.create_prepared = self._f(
+            "solver_create_prepared", C.c_void_p,
+            [_dp, S, S, _dp, S, S, _dp, _dp, _dp, _dp, _dp, C.c_double, C.POINTER(Config),
+             C.POINTER(C.c_int)])
+        self.steps_c = self._f("solver_steps", C.c_int, [C.c_void_p, C.c_uint64, _u64p])
 
 
 class RefLib(_Lib):
@@ -379,3 +384,36 @@ class Solver:
 
     def a_sq(self):
         out = np.empty(self.m); self.lib.get_a_sq(self.h, _ptr(out)); return out
+
+
+class PreparedSolver:
+    """Oracle solver over host-precomputed caches (benchmark CPU baseline only).
+
+    A, B, C, G = A·Aᵀ and BtB = BᵀB are borrowed (must outlive this object);
+    R0 and X0 are copied.  step timing is the reference's per-iteration algorithm.
+    """
+
+    def __init__(self, lib, A, B, Cm, X0, R0, G, BtB, alpha, cfg):
+        self.lib = lib
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (A, B, Cm, X0, R0, G, BtB)]
+        A, B, Cm, X0, R0, G, BtB = self._keep
+        m, p = A.shape
+        q, n = B.shape
+        st = C.c_int(0)
+        self.h = lib.create_prepared(_ptr(A), m, p, _ptr(B), q, n, _ptr(Cm), _ptr(X0), _ptr(R0),
+                                     _ptr(G), _ptr(BtB), alpha, C.byref(cfg), C.byref(st))
+        if not self.h:
+            raise OracleError(st.value, "prepared create failed")
+        self.cfg = cfg
+
+    def steps(self, k):
+        rows = np.empty(max(k, 1), dtype=np.uint64)
+        code = self.lib.steps_c(self.h, k, rows.ctypes.data_as(_u64p))
+        if code:
+            raise OracleError(code, self.lib.last_error(self.h).decode())
+        return rows[:k]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.destroy(self.h)
+            self.h = None
