@@ -170,6 +170,12 @@ class OracleLib(_Lib):
         self.get_r_sq = self._f("solver_get_r_sq", None, [C.c_void_p, _dp])
         self.get_a_sq = self._f("solver_get_a_sq", None, [C.c_void_p, _dp])
         self.rng_state = self._f("solver_rng_state", None, [C.c_void_p, _u64p])
+        self.rng_init = self._f("rng_init", None, [C.c_void_p, C.c_uint64])
+        self.rng_next_u64 = self._f("rng_next_u64", C.c_uint64, [C.c_void_p])
+        self.rng_gauss = self._f("rng_gauss", C.c_double, [C.c_void_p])
+        self.rng_substream = self._f("rng_substream", None, [C.c_void_p, C.c_uint64, C.c_void_p])
+        self.rng_categorical_cdf = self._f("rng_categorical_cdf", C.c_size_t,
+                                           [C.c_void_p, _dp, C.c_size_t, C.POINTER(C.c_int)])
         self.create_prepared = self._f(
             "solver_create_prepared", C.c_void_p,
             [_dp, S, S, _dp, S, S, _dp, _dp, _dp, _dp, _dp, C.c_double, C.POINTER(Config),
@@ -417,3 +423,10 @@ class PreparedSolver:
         if getattr(self, "h", None):
             self.lib.destroy(self.h)
             self.h = None
+
+
+class Rng(C.Structure):
+    """orc_rng — RngStream state (rng.hpp:18-123)."""
+
+    _fields_ = [("s", C.c_uint64 * 4), ("seed", C.c_uint64), ("spare", C.c_double),
+                ("has_spare", C.c_int32)]
