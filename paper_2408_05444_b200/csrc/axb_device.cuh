@@ -109,6 +109,7 @@ struct Params {
     unsigned long long trace_cap;
     int* member_flags;           // m (greedy_index_set query)
     const long long* forced_rows;  // replayed index stream, slot = k − k0
+    double* gsum;                // ⌈m/32⌉ group member masses (selection scratch)
     DevState* st;
     double alpha, theta, a_fro_sq, tol, ref_sq, c_fro;
     int method, stop_kind, tie_guard, vec2;

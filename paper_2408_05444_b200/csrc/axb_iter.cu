@@ -34,6 +34,15 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
+// Programmatic dependent launch: the iteration kernels are launched with the
+// programmatic-stream-serialization attribute so the next kernel's CTAs are
+// scheduled while this one drains; griddepcontrol.wait then blocks until the
+// predecessor grid has completed and its writes are visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ bool halted(const DevState* st) {
     return st->status != ST_RUN || st->k >= st->k_limit;
 }
@@ -133,6 +142,8 @@ __device__ double warp_dot(const double* __restrict__ row, const double* __restr
 constexpr int kYgThreads = 128;
 __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
     __shared__ double red[kYgThreads / 32];
+    pdl_wait();
+    pdl_trigger();
     const DevState* st = P.st;
     if (halted(st)) return;
     const long long il = st->sel - P.row0;
@@ -156,14 +167,14 @@ __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
             const long long h = len >> 1;
 #pragma unroll 8
             for (long long k = tid; k < h; k += kYgThreads) {
-                const double2 a = __ldcs(r2 + k);
+                const double2 a = __ldg(r2 + k);  // keep B in L2 for the z pass
                 const double2 b = __ldg(v2 + k);
                 a0 += a.x * b.x;
                 a1 += a.y * b.y;
             }
         } else {
 #pragma unroll 8
-            for (long long k = tid; k < len; k += kYgThreads) a0 += __ldcs(row + k) * __ldg(v + k);
+            for (long long k = tid; k < len; k += kYgThreads) a0 += __ldg(row + k) * __ldg(v + k);
         }
         double acc = warp_sum(a0 + a1);
         if (lane == 0) red[w] = acc;
@@ -184,6 +195,8 @@ __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
 __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
     __shared__ double red[kWarps];
     __shared__ bool last;
+    pdl_wait();
+    pdl_trigger();
     DevState* st = P.st;
     if (halted(st)) return;
     const int nzc = P.z_nslab * P.z_nj;
@@ -202,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
 #pragma unroll 8
                 for (long long j = j0; j < j1; ++j) {
                     const double yj = __ldg(P.y + j);
-                    const double2 b = __ldg(Bc + j * ld2);
+                    const double2 b = __ldcs(Bc + j * ld2);  // last use of B this iteration
                     a0 += yj * b.x;
                     a1 += yj * b.y;
                 }
@@ -376,33 +389,49 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
         return sh.err;
     }
     // GRBK / RGRBK (solver.hpp:212-254): ζ, membership, member-mass draw.
+    // Two-level scan: member masses of 32-row groups (coalesced, warp trees),
+    // an ordered prefix over the group sums, then only the chosen group is
+    // reloaded and scanned lane by lane.
     const double r_fro = st->r_fro_sq;
     if (!(r_fro > 0.0)) return 2;  // "greedy threshold: zero residual"
     const long long argmax = st->argmax;
     const double zeta = __dadd_rn(__dmul_rn(theta, __ddiv_rn(st->max_ratio, r_fro)),
                                   __ddiv_rn(__dsub_rn(1.0, theta), P.a_fro_sq));
-    const long long seg = (m + kThreads - 1) / kThreads;
-    const long long s0 = min(m, (long long)tid * seg), s1 = min(m, s0 + seg);
     auto member_g = [&](long long i) -> double {  // member mass, or −1 for non-members
         const double as = P.a_sq[i];
         if (as <= 0.0) return -1.0;
         const double rs = __ldcg(P.r_sq + i);
         return (i == argmax || rs >= __dmul_rn(__dmul_rn(zeta, as), r_fro)) ? rs : -1.0;
     };
-    // one coalesced pass stages the member masses in shared memory, so the
-    // ordered segment scans below run at smem latency instead of L2 latency
-    const bool staged = scratch != nullptr && m <= scratch_cap;
-    if (staged) {
-        for (long long i = tid; i < m; i += blockDim.x) scratch[i] = member_g(i);
-        __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5;
+    const long long ng = (m + 31) / 32;
+    double* gs = (scratch != nullptr && ng <= scratch_cap) ? scratch : P.gsum;
+    if (warp < kWarps) {
+        constexpr int kG = 4;  // groups in flight per warp
+        for (long long gb = warp; gb < ng; gb += (long long)kWarps * kG) {
+            double w[kG];
+#pragma unroll
+            for (int u = 0; u < kG; ++u) {
+                const long long i = (gb + (long long)u * kWarps) * 32 + lane;
+                w[u] = (i < m) ? member_g(i) : -1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kG; ++u) {
+                const long long g = gb + (long long)u * kWarps;
+                const double v = warp_sum(w[u] > 0.0 ? w[u] : 0.0);
+                if (lane == 0 && g < ng) gs[g] = v;
+            }
+        }
     }
-    auto mass_of = [&](long long i) -> double { return staged ? scratch[i] : member_g(i); };
-    double local = 0.0;
-    for (long long i = s0; i < s1; ++i) {
-        const double w = mass_of(i);
-        if (w >= 0.0) local = __dadd_rn(local, w);
-    }
+    __syncthreads();
+    // ordered inclusive prefix over the group sums: contiguous runs per thread,
+    // Hillis–Steele across the runs (fixed order → deterministic)
     const bool scan_lane = tid < kThreads;  // blocks may carry an extra producer warp
+    const long long gseg = (ng + kThreads - 1) / kThreads;
+    const long long g0 = scan_lane ? min(ng, (long long)tid * gseg) : ng;
+    const long long g1 = min(ng, g0 + gseg);
+    double local = 0.0;
+    for (long long g = g0; g < g1; ++g) local = __dadd_rn(local, gs[g]);
     if (scan_lane) sh.scan[tid] = local;
     __syncthreads();
     for (int off = 1; off < kThreads; off <<= 1) {
@@ -418,44 +447,64 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
         sh.u = rng_unit(st->rng);
         sh.target = __dmul_rn(sh.u, total);
         sh.cand = LLONG_MAX;
+        sh.err = 0;
     }
     __syncthreads();
     const double target = sh.target;
-    // first member whose running cumulative mass exceeds the target (upper_bound)
-    long long mine = LLONG_MAX;
-    double lo_c = 0.0, hi_c = 0.0;
-    {
+    long long my_g = LLONG_MAX;
+    double my_before = 0.0;
+    {  // first group whose cumulative mass exceeds the target
         double cum = excl;
-        for (long long i = s0; i < s1; ++i) {
-            const double w = mass_of(i);
-            if (w < 0.0) continue;
-            const double nc = __dadd_rn(cum, w);
+        for (long long g = g0; g < g1; ++g) {
+            const double nc = __dadd_rn(cum, gs[g]);
             if (nc > target) {
-                mine = i;
-                lo_c = cum;
-                hi_c = nc;
+                my_g = g;
+                my_before = cum;
                 break;
             }
             cum = nc;
         }
+        if (my_g != LLONG_MAX)
+            atomicMin(reinterpret_cast<unsigned long long*>(&sh.cand), (unsigned long long)my_g);
     }
-    if (mine != LLONG_MAX) atomicMin(reinterpret_cast<unsigned long long*>(&sh.cand),
-                                     (unsigned long long)mine);
+    __syncthreads();
+    const long long G = sh.cand;
+    if (my_g == G && G != LLONG_MAX) sh.redv[0] = my_before;  // unique owner of G
+    __syncthreads();
+    if (G != LLONG_MAX && warp == 0) {
+        // within group G: lane-inclusive scan of the member masses
+        const long long i = G * 32 + lane;
+        const double w = (i < m) ? member_g(i) : -1.0;
+        double v = w > 0.0 ? w : 0.0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off) v = __dadd_rn(v, t);
+        }
+        const double before = sh.redv[0];  // cumulative mass before group G
+        const double cum = __dadd_rn(before, v);
+        double prev = __shfl_up_sync(0xffffffffu, cum, 1);
+        if (lane == 0) prev = before;
+        const unsigned hit = __ballot_sync(0xffffffffu, w >= 0.0 && cum > target);
+        if (hit == 0u) {
+            if (lane == 0) sh.err = -1;  // inconsistent rounding: exact replay below
+        } else {
+            const int first = __ffs(hit) - 1;
+            const double hi = __shfl_sync(0xffffffffu, cum, first);
+            const double lo = __shfl_sync(0xffffffffu, prev, first);
+            if (lane == 0) {
+                sh.cand = G * 32 + first;
+                // the ordered prefix rounds differently from the reference's
+                // sequential cumsum; a draw within that rounding of a boundary
+                // re-runs the reference's sequential walk (rare)
+                const double slack = 8.0 * (double)m * DBL_EPSILON * total;
+                if (P.tie_guard && (hi - target <= slack || target - lo <= slack)) sh.err = -1;
+            }
+        }
+    }
     __syncthreads();
     long long pick = sh.cand;
-    const bool exact_needed = pick == LLONG_MAX;
-    __syncthreads();
-    if (tid == 0) sh.err = 0;
-    __syncthreads();
-    if (!exact_needed && P.tie_guard && mine == pick) {
-        // the parallel cumsum rounds differently from the reference's sequential
-        // one; if the draw landed within that rounding of a boundary, re-run the
-        // reference's sequential walk (rare; keeps the pick bitwise-faithful).
-        const double slack = 8.0 * (double)m * DBL_EPSILON * total;
-        if (hi_c - target <= slack || target - lo_c <= slack) sh.err = -1;
-    }
-    __syncthreads();
-    if (exact_needed || sh.err == -1) {
+    if (G == LLONG_MAX || sh.err == -1) {
         __syncthreads();
         if (tid == 0) {
             // Sequential replay of solver.hpp:243-253 + rng.hpp:84-99 with the same
@@ -463,20 +512,20 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
             // upper_bound, then walk back over a trailing zero-weight plateau.
             const double u = sh.u;
             double total_seq = 0.0;
-            for (long long i = 0; i < m; ++i) {
-                const double w = mass_of(i);
+            for (long long r = 0; r < m; ++r) {
+                const double w = member_g(r);
                 if (w >= 0.0) total_seq = __dadd_rn(total_seq, w);
             }
             const double tseq = __dmul_rn(u, total_seq);
             double cum = 0.0;
             long long found = -1, first_member = -1, last_change = -1;
-            for (long long i = 0; i < m && found < 0; ++i) {
-                const double w = mass_of(i);
+            for (long long r = 0; r < m && found < 0; ++r) {
+                const double w = member_g(r);
                 if (w < 0.0) continue;
-                if (first_member < 0) first_member = i;
+                if (first_member < 0) first_member = r;
                 const double nc = __dadd_rn(cum, w);
-                if (nc > tseq) found = i;
-                if (nc != cum) last_change = i;
+                if (nc > tseq) found = r;
+                if (nc != cum) last_change = r;
                 cum = nc;
             }
             if (found < 0) found = last_change >= 0 ? last_change : first_member;
@@ -612,6 +661,8 @@ __device__ void r_tail(const Params& P, DevState* st, long long r0, long long r1
 template <bool UPDATE, bool VEC2>
 __global__ void __launch_bounds__(kThreads) k_r(Params P) {
     extern __shared__ double smem[];
+    pdl_wait();
+    pdl_trigger();
     DevState* st = P.st;
     if (UPDATE && halted(st)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -749,6 +800,8 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
     __shared__ double redv[32];
     __shared__ long long redi[32];
     __shared__ bool last;
+    pdl_wait();
+    pdl_trigger();
     DevState* st = P.st;
     if (UPDATE && halted(st)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1144,12 +1197,28 @@ __global__ void k_cumsum_seq(const double* a_sq, long long m, double* cum, doubl
 // ------------------------------------------------------------------------
 // launchers
 
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 void launch_yg(const Params& P, cudaStream_t s, bool with_g) {
-    k_yg<<<P.yg_grid, kYgThreads, 0, s>>>(P, with_g ? 1 : 0);
+    launch_pdl(k_yg, P.yg_grid, kYgThreads, 0, s, P, with_g ? 1 : 0);
 }
 
 void launch_zx(const Params& P, cudaStream_t s) {
-    k_zx<<<P.z_nslab * P.z_nj + P.x_ctas, kThreads, 0, s>>>(P);
+    launch_pdl(k_zx, P.z_nslab * P.z_nj + P.x_ctas, kThreads, 0, s, P);
 }
 
 void launch_r(const Params& P, cudaStream_t s, bool update) {
@@ -1174,7 +1243,7 @@ void launch_r(const Params& P, cudaStream_t s, bool update) {
             cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             attr_set = (size_t)dyn;
         }
-        if (update) k_r_tma<true><<<P.r_grid, kTmaThreads, smem, s>>>(P);
+        if (update) launch_pdl(k_r_tma<true>, P.r_grid, kTmaThreads, smem, s, P);
         else k_r_tma<false><<<P.r_grid, kTmaThreads, smem, s>>>(P);
         return;
     }
@@ -1190,7 +1259,8 @@ void launch_r(const Params& P, cudaStream_t s, bool update) {
 }
 
 void launch_select(const Params& P, cudaStream_t s, int method, double theta, int consume) {
-    const long long cap = P.m <= 6144 ? P.m : 0;  // ≤48 KB static-limit scratch
+    const long long ng = (P.m + 31) / 32;
+    const long long cap = ng <= 4096 ? ng : 0;  // group sums in ≤32 KB of smem, else P.gsum
     k_select<<<1, kThreads, (size_t)cap * 8, s>>>(P, method, theta, consume, cap);
 }
 

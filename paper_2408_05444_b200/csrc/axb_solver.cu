@@ -156,7 +156,7 @@ struct axb_solver {
     axb_options opt{};
     cudaStream_t stream = nullptr;
     DevBuf<double> A, B, C, R, X, Xref, a_sq, rbk_cum, r_sq, G, g, y, z, zpart, xpart, T,
-        gemm_sq, gemm_diff, scal, tr_metric, tr_rel, sq_part;
+        gemm_sq, gemm_diff, scal, tr_metric, tr_rel, sq_part, gsum;
     DevBuf<unsigned int> zcnt;
     DevBuf<RowRecord> rrec;
     DevBuf<long long> tr_row, forced;
@@ -431,6 +431,7 @@ struct axb_solver {
         rrec.alloc(P.r_grid, "rrec");
         tr_row.alloc(trace_cap, "trace");
         forced.alloc(trace_cap, "forced rows");
+        gsum.alloc((m + 31) / 32, "group sums");
         tr_metric.alloc(trace_cap, "trace");
         tr_rel.alloc(trace_cap, "trace");
         flags.alloc(m, "flags");
@@ -443,6 +444,7 @@ struct axb_solver {
         P.rrec = rrec.p; P.trace_row = tr_row.p; P.trace_metric = tr_metric.p;
         P.trace_rel = tr_rel.p; P.trace_cap = trace_cap; P.member_flags = flags.p; P.st = st.p;
         P.forced_rows = forced.p;
+        P.gsum = gsum.p;
         P.alpha = alpha;
         P.theta = cfg.method == AXB_RGRBK ? cfg.theta : 0.5;
         P.a_fro_sq = a_fro_sq;
