@@ -114,7 +114,7 @@ struct Params {
     double alpha, theta, a_fro_sq, tol, ref_sq, c_fro;
     int method, stop_kind, tie_guard, vec2;
     // launch geometry
-    int r_grid, r_rows_per_cta, r_chunk, r_tma, r_stages;
+    int r_grid, r_rows_per_cta, r_chunk, r_tma, r_stages, r_zstage;
     int yg_grid;
     int z_nslab, z_nj, z_jrows, x_ctas;
 };

@@ -792,11 +792,30 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// rows whose warp partials a CTA keeps before a combine flush
+constexpr int kRowsKept = 128;
+
+// Fixed-order combine of the kept rows' 8 warp partials (consumer threads only,
+// after a consumer barrier): ‖R_l‖² → r_sq, running max / argmax of the ratio.
+__device__ void combine_rows(const Params& P, const double* rpart, const long long* rowid, int nkeep,
+                             double& cmax, long long& carg) {
+    for (int t = threadIdx.x; t < nkeep; t += kTmaConsumerWarps * 32) {
+        double a = 0.0;
+        for (int w = 0; w < kTmaConsumerWarps; ++w) a += rpart[t * kTmaConsumerWarps + w];
+        const long long row = rowid[t];
+        P.r_sq[row] = a;
+        const double as = P.a_sq[row];
+        if (as > 0.0) maxidx_merge(cmax, carg, __ddiv_rn(a, as), P.row0 + row);
+    }
+}
+
 template <bool UPDATE>
 __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ long long stage_row[32];
-    __shared__ double rp[2][kTmaConsumerWarps];
+    __shared__ __align__(16) double stage_g[32][2];
+    __shared__ double rpart[kRowsKept * kTmaConsumerWarps];
+    __shared__ long long rowid[kRowsKept];
     __shared__ double redv[32];
     __shared__ long long redi[32];
     __shared__ bool last;
@@ -809,8 +828,11 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
     const int TW = P.r_chunk;
     const int tpr = (int)((n + TW - 1) / TW);
     const int S = P.r_stages;
+    const bool zst = UPDATE && P.r_zstage;  // z segment staged with each tile
     double* stage = reinterpret_cast<double*>(dsm);
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(dsm + (size_t)S * TW * 8);
+    double* zstage = stage + (size_t)S * TW;
+    unsigned long long* full =
+        reinterpret_cast<unsigned long long*>(dsm + (size_t)S * TW * 8 * (zst ? 2 : 1));
     unsigned long long* empty = full + S;
     if (tid == 0) {
         for (int i = 0; i < S; ++i) {
@@ -822,8 +844,14 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
     __syncthreads();
     double cmax = -INFINITY;
     long long carg = LLONG_MAX;
+    long long sel = 0;
+    double coef = 0.0;
+    if (UPDATE) {
+        coef = st->coef;
+        sel = st->sel;
+    }
     if (warp == kTmaConsumerWarps) {
-        // ---- producer: grab rows dynamically, stream their tiles into the ring ----
+        // ---- producer: grab rows dynamically, stream tiles (+ z segment, + G entry) ----
         if (lane == 0) {
             int s = 0;
             unsigned round = 0;
@@ -839,8 +867,14 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
                         mbar_arrive(&full[s]);  // sentinel: no bytes
                     } else {
                         const unsigned bytes = (unsigned)(min((long long)TW, n - seg * TW) * 8);
-                        mbar_expect_tx(&full[s], bytes);
+                        const bool gload = UPDATE && seg == 0 && P.G;
+                        mbar_expect_tx(&full[s], bytes * (zst ? 2u : 1u) + (gload ? 16u : 0u));
                         tma_load_1d(stage + (size_t)s * TW, src, bytes, &full[s]);
+                        if (zst) tma_load_1d(zstage + (size_t)s * TW, P.z + seg * TW, bytes, &full[s]);
+                        if (gload) {  // 16-byte aligned pair holding G[sel, row]
+                            const long long gi = (sel * m + row) & ~1ll;
+                            tma_load_1d(stage_g[s], P.G + gi, 16u, &full[s]);
+                        }
                     }
                     if (++s == S) {
                         s = 0;
@@ -852,13 +886,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
         }
     } else {
         // ---- 8 consumer warps ----
-        double coef = 0.0;
-        long long sel = 0;
-        if (UPDATE) {
-            coef = st->coef;
-            sel = st->sel;
-        }
-        int s = 0, buf = 0;
+        int s = 0, nkeep = 0;
         unsigned round = 0;
         for (;;) {
             mbar_wait(&full[s], round & 1);
@@ -866,7 +894,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
             if (row < 0) break;
             double f = 0.0;
             if (UPDATE) {
-                const double gl = P.G ? __ldg(P.G + sel * m + row) : __ldg(P.g + row);
+                const double gl = P.G ? stage_g[s][(sel * m + row) & 1] : __ldg(P.g + row);
                 f = __dmul_rn(coef, gl);  // solver.hpp:296
             }
             double acc = 0.0;
@@ -876,12 +904,13 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
                 const int h = (int)(min((long long)TW, n - c0) >> 1);
                 const double2* src = reinterpret_cast<const double2*>(stage + (size_t)s * TW);
                 double2* dst = reinterpret_cast<double2*>(P.R + row * n + c0);
-                const double2* z2 = reinterpret_cast<const double2*>(P.z + c0);
+                const double2* z2 = zst ? reinterpret_cast<const double2*>(zstage + (size_t)s * TW)
+                                        : reinterpret_cast<const double2*>(P.z + c0);
 #pragma unroll 4
                 for (int k = tid; k < h; k += kTmaConsumerWarps * 32) {
                     double2 r = src[k];
                     if (UPDATE) {
-                        const double2 zz = __ldg(z2 + k);
+                        const double2 zz = zst ? z2[k] : __ldg(z2 + k);
                         r.x = __dsub_rn(r.x, __dmul_rn(f, zz.x));  // solver.hpp:300
                         r.y = __dsub_rn(r.y, __dmul_rn(f, zz.y));
                         __stcs(dst + k, r);
@@ -896,24 +925,24 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
                     ++round;
                 }
             }
-            // ‖R_row‖²: fixed-order combine of the 8 warp partials
+            // keep this warp's partial of ‖R_row‖²; combined in fixed order later
             acc = warp_sum(acc);
-            if (lane == 0) rp[buf][warp] = acc;
-            asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
-            if (tid == 0) {
-                double a = 0.0;
-                for (int w = 0; w < kTmaConsumerWarps; ++w) a += rp[buf][w];
-                P.r_sq[row] = a;
-                const double as = P.a_sq[row];
-                if (as > 0.0) maxidx_merge(cmax, carg, __ddiv_rn(a, as), P.row0 + row);
+            if (lane == 0) rpart[nkeep * kTmaConsumerWarps + warp] = acc;
+            if (tid == 0) rowid[nkeep] = row;
+            if (++nkeep == kRowsKept) {  // rare flush (long runs of rows per CTA)
+                asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+                combine_rows(P, rpart, rowid, nkeep, cmax, carg);
+                asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+                nkeep = 0;
             }
-            buf ^= 1;
         }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+        combine_rows(P, rpart, rowid, nkeep, cmax, carg);
     }
     // records: max/argmax only (order-independent); ‖R‖² is summed over the
     // rows in fixed order by the last CTA, so the dynamic row-to-CTA mapping
     // cannot change its rounding.
-    __syncthreads();
+    block_maxidx(cmax, carg, redv, redi);
     if (tid == 0) {
         P.rrec[blockIdx.x] = RowRecord{0.0, cmax, carg, 0.0};
         __threadfence();
@@ -949,7 +978,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
 }
 
 size_t tma_smem_bytes(const Params& P) {
-    return (size_t)P.r_stages * P.r_chunk * 8 + 2 * P.r_stages * 8;
+    return (size_t)P.r_stages * P.r_chunk * 8 * (P.r_zstage ? 2 : 1) + 2 * P.r_stages * 8;
 }
 
 // K3 standalone: (re)select with the configured rule (consume=0: speculative,
@@ -1234,13 +1263,16 @@ void launch_r(const Params& P, cudaStream_t s, bool update) {
             const int dyn = optin - (int)fa.sharedSizeBytes;
             cudaFuncSetAttribute(k_r_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-            // carve out only the shared memory the resident CTAs need, so the
-            // rest of the 256 KB stays L1 for the z vector (read via __ldg)
+            // one shared-memory carve-out for all three iteration kernels, so
+            // consecutive (PDL-overlapped) launches never reconfigure L1/smem
             const int cps = std::max(1, (P.r_grid + 147) / 148);
             int pct = (int)((100.0 * cps * (smem + fa.sharedSizeBytes + 1024)) / optin + 0.999);
             pct = std::min(100, std::max(pct, 1));
+            if (const char* e = std::getenv("AXB_CARVEOUT")) pct = std::atoi(e);
             cudaFuncSetAttribute(k_r_tma<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            cudaFuncSetAttribute(k_yg, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            cudaFuncSetAttribute(k_zx, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             attr_set = (size_t)dyn;
         }
         if (update) launch_pdl(k_r_tma<true>, P.r_grid, kTmaThreads, smem, s, P);

@@ -404,11 +404,12 @@ struct axb_solver {
             // TMA ring: 2 CTAs per SM, rows split evenly, tiles of ≤2048 columns
             // (tunable for sweeps: AXB_R_CPS, AXB_R_STAGES, AXB_R_TILE)
             const int cps = env_int("AXB_R_CPS", 2), stages = env_int("AXB_R_STAGES", 4);
-            const int tile = env_int("AXB_R_TILE", 2048);
+            const int tile = env_int("AXB_R_TILE", 1024);
             P.r_grid = (int)std::min<uint64_t>((uint64_t)148 * cps, m);
             P.r_rows_per_cta = (int)((m + P.r_grid - 1) / P.r_grid);
             P.r_chunk = (int)std::min<uint64_t>(n, (uint64_t)tile);
             P.r_stages = std::max(2, std::min(stages, 16));
+            P.r_zstage = env_int("AXB_R_ZSTAGE", 1);
         } else {
             int rgrid = (int)std::min<uint64_t>((uint64_t)target, std::max<uint64_t>(1, (m + 7) / 8));
             P.r_rows_per_cta = (int)((m + rgrid - 1) / rgrid);

@@ -1,8 +1,8 @@
-# GPU round trip: parity tests, bench, launch list, one ncu --set full capture.
+# GPU round trip: parity tests, default bench, reference arm, launch list, one ncu --set full capture.
 set -x
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest.log 2>&1; echo pytest_exit=$?; tail -3 gpurun_out/pytest.log
-timeout 300 python bench.py --steps 1000 --warmup 10 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_exit=$?
-AXB_R_KERNEL=simple timeout 300 python bench.py --steps 1000 --warmup 10 --no-cpu-baseline --no-e2e --no-tol > gpurun_out/bench_simple.json 2> gpurun_out/bench_simple.err; echo bench_simple_exit=$?
+timeout 300 python -m pytest tests/ -x -q -m gpu > gpurun_out/pytest.log 2>&1; echo pytest_exit=$?; tail -3 gpurun_out/pytest.log
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_exit=$?
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_exit=$?
 B="python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-e2e --no-tol"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_(yg|zx|r|r_tma|select|ctrl)$' -c 400 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_list.log 2>&1; echo list_exit=$?
