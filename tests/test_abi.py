@@ -102,3 +102,35 @@ def test_error_taxonomy_codes():
     with pytest.raises(errors.DivergenceError) as e:
         errors.raise_status(4, "d", iteration=12, residual_norm=3.5)
     assert e.value.iteration == 12 and e.value.residual_norm == 3.5
+
+
+def build_cpp_example(tmp_path):
+    import shutil
+    import subprocess
+
+    from paper_2408_05444_b200 import _lib
+
+    gxx = shutil.which("g++")
+    if not gxx:
+        pytest.skip("g++ not available")
+    exe = str(tmp_path / "dropin")
+    src = os.path.join(ROOT, "tests", "cpp", "dropin_example.cpp")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    cmd = [gxx, "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", exe,
+           f"-L{libdir}", "-laxb_b200", f"-Wl,-rpath,{libdir}"]
+    subprocess.run(cmd, check=True)
+    return exe
+
+
+def test_cpp_dropin_header_compiles_and_fails_loudly_without_device(tmp_path):
+    """include/axb_b200/solver.hpp compiles against the C-ABI; with no device the
+    solver constructor throws (no CPU fallback)."""
+    import subprocess
+
+    import paper_2408_05444_b200 as axb
+
+    exe = build_cpp_example(tmp_path)
+    if axb.device_available():
+        pytest.skip("device present: covered by the GPU test")
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 3 and "CudaError" in out.stdout, out.stdout

@@ -162,3 +162,14 @@ def test_config1_replay_with_refresh(axb, orc, tag, theta):
     sg.replay(ro, mirror_refresh=True)
     assert rel(sg.X(), so.X()) <= RTOL_X
     assert rel(sg.R(), so.R()) <= 1e-8
+
+
+def test_cpp_dropin_runs_on_device(axb, tmp_path):
+    """The C++ shim (include/axb_b200/solver.hpp) drives the device end to end."""
+    import subprocess
+    from test_abi import build_cpp_example
+
+    exe = build_cpp_example(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("iterations=")
