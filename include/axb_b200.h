@@ -110,6 +110,17 @@ typedef struct {
 typedef struct axb_solver axb_solver;
 
 void axb_options_default(axb_options* opt);
+
+/* ---- row sharding (§8(e)): NCCL bootstrap, one communicator per GPU/process ----
+ * Rank 0 creates an id, the caller distributes it (e.g. torch.distributed
+ * broadcast over gloo), every rank creates its communicator and passes it in
+ * axb_options.nccl_comm with world_size, rank, m_global = world·m and
+ * row_offset = rank·m (equal contiguous row shards).  NCCL is loaded at run
+ * time (dlopen "libnccl.so.2"); single-GPU use never touches it. */
+int axb_nccl_unique_id(unsigned char out[128]);
+int axb_nccl_comm_create(int nranks, const unsigned char id[128], int rank, int device,
+                         void** comm);
+int axb_nccl_comm_destroy(void* comm);
 int axb_abi_version(void);
 /* 1 when a device that can run the sm_100a kernels is visible. */
 int axb_device_available(void);

@@ -71,7 +71,7 @@ struct alignas(16) DevState {
     unsigned int _pad1;
     unsigned long long r_next;   // dynamic row counter of the TMA residual kernel
     int32_t replay;              // 1: select from Params::forced_rows (index-stream replay)
-    int32_t _pad2;
+    int32_t packed;              // sharded: this rank's pack_send holds the last row
 };
 
 struct RowRecord {   // per-CTA partial of the residual reduction
@@ -110,6 +110,15 @@ struct Params {
     int* member_flags;           // m (greedy_index_set query)
     const long long* forced_rows;  // replayed index stream, slot = k − k0
     double* gsum;                // ⌈m/32⌉ group member masses (selection scratch)
+    // ---- row sharding over `world` ranks (pack == nullptr: single GPU) ----
+    int world, rank;
+    double* pack;                // n + p + 2 (allreduced): R_i | A_i | sel | coef
+    double* pack_send;           // this rank's contribution (zeros unless owner)
+    double* recs;                // world × 4 (allgathered): Σ‖R_l‖², max ratio, argmax, err
+    double* masses;              // world (allgathered): greedy member mass per shard
+    const double* a_sq_g;        // m_global ‖A_i‖² (allgathered), for BK/RBK/replay
+    long long c0, c1;            // this rank's column slice of B for y and z
+    long long x0r, x1r;          // this rank's rows of X
     DevState* st;
     double alpha, theta, a_fro_sq, tol, ref_sq, c_fro;
     int method, stop_kind, tie_guard, vec2;
@@ -143,6 +152,9 @@ int sumsq_parts(long long n);
 void launch_sumsq(const double* v, long long n, double* part, cudaStream_t s);
 void launch_row_sq_seq(const double* A, long long m, long long p, double* out, cudaStream_t s);
 void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* total, cudaStream_t s);
+// sharded selection (between the record / mass allgathers and the row allreduce)
+void launch_sel1(const Params& P, cudaStream_t s, bool update);
+void launch_sel2(const Params& P, cudaStream_t s);
 
 // ---- DMMA GEMM (axb_gemm.cu) ----
 // D = (Cin ? Cin − A·op(B) : A·op(B)); op(B) = B (K×N) or Bᵀ (B is N×K) when b_trans.

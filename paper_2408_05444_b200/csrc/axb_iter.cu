@@ -146,17 +146,24 @@ __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
     pdl_trigger();
     const DevState* st = P.st;
     if (halted(st)) return;
-    const long long il = st->sel - P.row0;
-    const double* Ri = P.R + il * P.n;
-    const double* Ai = P.A + il * P.p;
+    const double* Ri;
+    const double* Ai;
+    if (P.pack) {  // sharded: the owner's row arrived through the allreduce
+        Ri = P.pack;
+        Ai = P.pack + P.n;
+    } else {
+        const long long il = st->sel - P.row0;
+        Ri = P.R + il * P.n;
+        Ai = P.A + il * P.p;
+    }
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const long long items = P.q + (with_g ? P.m : 0);
     for (long long it = blockIdx.x; it < items; it += gridDim.x) {
         const double* row;
         const double* v;
         long long len;
-        if (it < P.q) {
-            row = P.B + it * P.n; v = Ri; len = P.n;
+        if (it < P.q) {  // this rank's column slice [c0, c1) (all of B on one GPU)
+            row = P.B + it * P.n + P.c0; v = Ri + P.c0; len = P.c1 - P.c0;
         } else {
             row = P.A + (it - P.q) * P.p; v = Ai; len = P.p;
         }
@@ -206,10 +213,11 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
         const int jc = blockIdx.x / P.z_nslab;
         const long long j0 = (long long)jc * P.z_jrows;
         const long long j1 = min(P.q, j0 + P.z_jrows);
-        const long long c = (long long)slab * (2 * kThreads) + 2 * tid;
+        const long long c = P.c0 + (long long)slab * (2 * kThreads) + 2 * tid;
+        const long long cend = P.c1;
         double a0 = 0.0, a1 = 0.0;
         if ((P.n & 1) == 0) {
-            if (c < P.n) {
+            if (c < cend) {
                 const double2* Bc = reinterpret_cast<const double2*>(P.B + c);
                 const long long ld2 = P.n >> 1;
 #pragma unroll 8
@@ -223,25 +231,25 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
         } else {
             for (long long j = j0; j < j1; ++j) {
                 const double yj = __ldg(P.y + j);
-                if (c < P.n) a0 += yj * __ldg(P.B + j * P.n + c);
-                if (c + 1 < P.n) a1 += yj * __ldg(P.B + j * P.n + c + 1);
+                if (c < cend) a0 += yj * __ldg(P.B + j * P.n + c);
+                if (c + 1 < cend) a1 += yj * __ldg(P.B + j * P.n + c + 1);
             }
         }
         if (P.z_nj == 1) {
-            if (c < P.n) P.z[c] = a0;
-            if (c + 1 < P.n) P.z[c + 1] = a1;
+            if (c < cend) P.z[c] = a0;
+            if (c + 1 < cend) P.z[c + 1] = a1;
             return;
         }
         double* zp = P.zpart + (long long)jc * P.n;
-        if (c < P.n) zp[c] = a0;
-        if (c + 1 < P.n) zp[c + 1] = a1;
+        if (c < cend) zp[c] = a0;
+        if (c + 1 < cend) zp[c + 1] = a1;
         __threadfence();
         __syncthreads();
         if (tid == 0) last = atomicAdd(P.zcnt + slab, 1u) == (unsigned)(P.z_nj - 1);
         __syncthreads();
         if (!last) return;
         __threadfence();
-        for (long long cc = c; cc < c + 2 && cc < P.n; ++cc) {
+        for (long long cc = c; cc < c + 2 && cc < cend; ++cc) {
             double s = 0.0;
             for (int k = 0; k < P.z_nj; ++k) s += __ldcg(P.zpart + (long long)k * P.n + cc);
             P.z[cc] = s;
@@ -251,14 +259,14 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
     }
     // ---- X update (solver.hpp:272-290): one warp per row t of X ----
     const int xb = blockIdx.x - nzc;
-    const long long il = st->sel - P.row0;
-    const double* Ai = P.A + il * P.p;
-    const double coef = st->coef;
+    const double* Ai = P.pack ? P.pack + P.n : P.A + (st->sel - P.row0) * P.p;
+    const double coef = P.pack ? P.pack[P.n + P.p + 1] : st->coef;
     const bool track = P.Xref != nullptr;
     const int lane = tid & 31, warp = tid >> 5;
     const long long q = P.q;
     double acc = 0.0;
-    for (long long t = (long long)xb * kWarps + warp; t < P.p; t += (long long)P.x_ctas * kWarps) {
+    for (long long t = P.x0r + (long long)xb * kWarps + warp; t < P.x1r;
+         t += (long long)P.x_ctas * kWarps) {
         const double f = __dmul_rn(coef, __ldg(Ai + t));
         double* xr = P.X + t * q;
         const double* rr = track ? P.Xref + t * q : nullptr;
@@ -322,6 +330,151 @@ struct SelShared {
     long long cand;
     int err;
 };
+
+// ---- greedy membership and the two-level member-mass scan ----------------
+// member mass of local row i (r_sq) when it belongs to the greedy index set
+// 𝒥_k (solver.hpp:226-237), else −1.  ζ follows solver.hpp:215 with separately
+// rounded operations; the argmax row is a member by construction.
+struct Member {
+    const double* a_sq;
+    const double* r_sq;
+    long long row0, argmax;
+    double zeta, r_fro;
+    __device__ double operator()(long long i) const {
+        const double as = a_sq[i];
+        if (as <= 0.0) return -1.0;
+        const double rs = __ldcg(r_sq + i);
+        return (row0 + i == argmax || rs >= __dmul_rn(__dmul_rn(zeta, as), r_fro)) ? rs : -1.0;
+    }
+};
+
+__device__ Member make_member(const Params& P, const DevState* st, double theta) {
+    Member mm;
+    mm.a_sq = P.a_sq;
+    mm.r_sq = P.r_sq;
+    mm.row0 = P.row0;
+    mm.argmax = st->argmax;
+    mm.r_fro = st->r_fro_sq;
+    mm.zeta = __dadd_rn(__dmul_rn(theta, __ddiv_rn(st->max_ratio, mm.r_fro)),
+                        __ddiv_rn(__dsub_rn(1.0, theta), P.a_fro_sq));
+    return mm;
+}
+
+// gs[g] = Σ member masses of rows [32g, 32g+32): coalesced loads, warp trees
+__device__ void grbk_group_sums(const Member& mem, long long m, double* gs) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long ng = (m + 31) / 32;
+    if (warp < kWarps) {
+        constexpr int kG = 4;  // groups in flight per warp
+        for (long long gb = warp; gb < ng; gb += (long long)kWarps * kG) {
+            double w[kG];
+#pragma unroll
+            for (int u = 0; u < kG; ++u) {
+                const long long i = (gb + (long long)u * kWarps) * 32 + lane;
+                w[u] = (i < m) ? mem(i) : -1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kG; ++u) {
+                const long long g = gb + (long long)u * kWarps;
+                const double v = warp_sum(w[u] > 0.0 ? w[u] : 0.0);
+                if (lane == 0 && g < ng) gs[g] = v;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// ordered inclusive prefix over gs: contiguous runs per thread, Hillis–Steele
+// across the runs (fixed order → deterministic).  Returns the total; [g0, g1)
+// and excl describe the calling thread's run.
+__device__ double grbk_prefix(const double* gs, long long ng, SelShared& sh, long long& g0,
+                              long long& g1, double& excl) {
+    const int tid = threadIdx.x;
+    const bool scan_lane = tid < kThreads;  // blocks may carry an extra producer warp
+    const long long gseg = (ng + kThreads - 1) / kThreads;
+    g0 = scan_lane ? min(ng, (long long)tid * gseg) : ng;
+    g1 = min(ng, g0 + gseg);
+    double local = 0.0;
+    for (long long g = g0; g < g1; ++g) local = __dadd_rn(local, gs[g]);
+    if (scan_lane) sh.scan[tid] = local;
+    __syncthreads();
+    for (int off = 1; off < kThreads; off <<= 1) {
+        const double v = (scan_lane && tid >= off) ? sh.scan[tid - off] : 0.0;
+        __syncthreads();
+        if (scan_lane) sh.scan[tid] = __dadd_rn(sh.scan[tid], v);
+        __syncthreads();
+    }
+    excl = (scan_lane && tid) ? sh.scan[tid - 1] : 0.0;
+    const double total = sh.scan[kThreads - 1];
+    __syncthreads();
+    return total;
+}
+
+// First local row whose cumulative member mass (thread prefixes `excl`, which
+// may include a cross-shard base) exceeds target.  Returns −1 when the draw
+// lands within `slack` of a boundary (slack ≥ 0) or the two rounding paths
+// disagree — the caller then falls back to an exact sequential walk.
+__device__ long long grbk_search(const Member& mem, long long m, const double* gs, long long g0,
+                                 long long g1, double excl, double target, double slack,
+                                 SelShared& sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        sh.cand = LLONG_MAX;
+        sh.err = 0;
+    }
+    __syncthreads();
+    long long my_g = LLONG_MAX;
+    double my_before = 0.0;
+    {
+        double cum = excl;
+        for (long long g = g0; g < g1; ++g) {
+            const double nc = __dadd_rn(cum, gs[g]);
+            if (nc > target) {
+                my_g = g;
+                my_before = cum;
+                break;
+            }
+            cum = nc;
+        }
+        if (my_g != LLONG_MAX)
+            atomicMin(reinterpret_cast<unsigned long long*>(&sh.cand), (unsigned long long)my_g);
+    }
+    __syncthreads();
+    const long long G = sh.cand;
+    if (my_g == G && G != LLONG_MAX) sh.redv[0] = my_before;  // unique owner of G
+    __syncthreads();
+    if (G != LLONG_MAX && warp == 0) {
+        // within group G: lane-inclusive scan of the member masses
+        const long long i = G * 32 + lane;
+        const double w = (i < m) ? mem(i) : -1.0;
+        double v = w > 0.0 ? w : 0.0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off) v = __dadd_rn(v, t);
+        }
+        const double before = sh.redv[0];  // cumulative mass before group G
+        const double cum = __dadd_rn(before, v);
+        double prev = __shfl_up_sync(0xffffffffu, cum, 1);
+        if (lane == 0) prev = before;
+        const unsigned hit = __ballot_sync(0xffffffffu, w >= 0.0 && cum > target);
+        if (hit == 0u) {
+            if (lane == 0) sh.err = -1;  // the two rounding paths disagree
+        } else {
+            const int first = __ffs(hit) - 1;
+            const double hi = __shfl_sync(0xffffffffu, cum, first);
+            const double lo = __shfl_sync(0xffffffffu, prev, first);
+            if (lane == 0) {
+                sh.cand = G * 32 + first;
+                if (slack >= 0.0 && (hi - target <= slack || target - lo <= slack)) sh.err = -1;
+            }
+        }
+    }
+    __syncthreads();
+    const long long pick = (G == LLONG_MAX || sh.err == -1) ? -1 : sh.cand;
+    __syncthreads();
+    return pick;
+}
 
 __device__ int select_rows(const Params& P, DevState* st, int method, double theta,
                            long long* out_row, SelShared& sh, double* scratch,
@@ -389,122 +542,22 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
         return sh.err;
     }
     // GRBK / RGRBK (solver.hpp:212-254): ζ, membership, member-mass draw.
-    // Two-level scan: member masses of 32-row groups (coalesced, warp trees),
-    // an ordered prefix over the group sums, then only the chosen group is
-    // reloaded and scanned lane by lane.
-    const double r_fro = st->r_fro_sq;
-    if (!(r_fro > 0.0)) return 2;  // "greedy threshold: zero residual"
-    const long long argmax = st->argmax;
-    const double zeta = __dadd_rn(__dmul_rn(theta, __ddiv_rn(st->max_ratio, r_fro)),
-                                  __ddiv_rn(__dsub_rn(1.0, theta), P.a_fro_sq));
-    auto member_g = [&](long long i) -> double {  // member mass, or −1 for non-members
-        const double as = P.a_sq[i];
-        if (as <= 0.0) return -1.0;
-        const double rs = __ldcg(P.r_sq + i);
-        return (i == argmax || rs >= __dmul_rn(__dmul_rn(zeta, as), r_fro)) ? rs : -1.0;
-    };
-    const int lane = tid & 31, warp = tid >> 5;
-    const long long ng = (m + 31) / 32;
-    double* gs = (scratch != nullptr && ng <= scratch_cap) ? scratch : P.gsum;
-    if (warp < kWarps) {
-        constexpr int kG = 4;  // groups in flight per warp
-        for (long long gb = warp; gb < ng; gb += (long long)kWarps * kG) {
-            double w[kG];
-#pragma unroll
-            for (int u = 0; u < kG; ++u) {
-                const long long i = (gb + (long long)u * kWarps) * 32 + lane;
-                w[u] = (i < m) ? member_g(i) : -1.0;
-            }
-#pragma unroll
-            for (int u = 0; u < kG; ++u) {
-                const long long g = gb + (long long)u * kWarps;
-                const double v = warp_sum(w[u] > 0.0 ? w[u] : 0.0);
-                if (lane == 0 && g < ng) gs[g] = v;
-            }
-        }
-    }
-    __syncthreads();
-    // ordered inclusive prefix over the group sums: contiguous runs per thread,
-    // Hillis–Steele across the runs (fixed order → deterministic)
-    const bool scan_lane = tid < kThreads;  // blocks may carry an extra producer warp
-    const long long gseg = (ng + kThreads - 1) / kThreads;
-    const long long g0 = scan_lane ? min(ng, (long long)tid * gseg) : ng;
-    const long long g1 = min(ng, g0 + gseg);
-    double local = 0.0;
-    for (long long g = g0; g < g1; ++g) local = __dadd_rn(local, gs[g]);
-    if (scan_lane) sh.scan[tid] = local;
-    __syncthreads();
-    for (int off = 1; off < kThreads; off <<= 1) {
-        const double v = (scan_lane && tid >= off) ? sh.scan[tid - off] : 0.0;
-        __syncthreads();
-        if (scan_lane) sh.scan[tid] = __dadd_rn(sh.scan[tid], v);
-        __syncthreads();
-    }
-    const double total = sh.scan[kThreads - 1];
-    const double excl = (scan_lane && tid) ? sh.scan[tid - 1] : 0.0;
+    if (!(st->r_fro_sq > 0.0)) return 2;  // "greedy threshold: zero residual"
+    const Member mem = make_member(P, st, theta);
+    double* gs = (scratch != nullptr && (m + 31) / 32 <= scratch_cap) ? scratch : P.gsum;
+    grbk_group_sums(mem, m, gs);
+    long long g0, g1;
+    double excl;
+    const double total = grbk_prefix(gs, (m + 31) / 32, sh, g0, g1, excl);
     if (!(total > 0.0)) return 2;  // mass on zero rows only (solver.hpp:249-252)
     if (tid == 0) {
         sh.u = rng_unit(st->rng);
         sh.target = __dmul_rn(sh.u, total);
-        sh.cand = LLONG_MAX;
-        sh.err = 0;
     }
     __syncthreads();
-    const double target = sh.target;
-    long long my_g = LLONG_MAX;
-    double my_before = 0.0;
-    {  // first group whose cumulative mass exceeds the target
-        double cum = excl;
-        for (long long g = g0; g < g1; ++g) {
-            const double nc = __dadd_rn(cum, gs[g]);
-            if (nc > target) {
-                my_g = g;
-                my_before = cum;
-                break;
-            }
-            cum = nc;
-        }
-        if (my_g != LLONG_MAX)
-            atomicMin(reinterpret_cast<unsigned long long*>(&sh.cand), (unsigned long long)my_g);
-    }
-    __syncthreads();
-    const long long G = sh.cand;
-    if (my_g == G && G != LLONG_MAX) sh.redv[0] = my_before;  // unique owner of G
-    __syncthreads();
-    if (G != LLONG_MAX && warp == 0) {
-        // within group G: lane-inclusive scan of the member masses
-        const long long i = G * 32 + lane;
-        const double w = (i < m) ? member_g(i) : -1.0;
-        double v = w > 0.0 ? w : 0.0;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const double t = __shfl_up_sync(0xffffffffu, v, off);
-            if (lane >= off) v = __dadd_rn(v, t);
-        }
-        const double before = sh.redv[0];  // cumulative mass before group G
-        const double cum = __dadd_rn(before, v);
-        double prev = __shfl_up_sync(0xffffffffu, cum, 1);
-        if (lane == 0) prev = before;
-        const unsigned hit = __ballot_sync(0xffffffffu, w >= 0.0 && cum > target);
-        if (hit == 0u) {
-            if (lane == 0) sh.err = -1;  // inconsistent rounding: exact replay below
-        } else {
-            const int first = __ffs(hit) - 1;
-            const double hi = __shfl_sync(0xffffffffu, cum, first);
-            const double lo = __shfl_sync(0xffffffffu, prev, first);
-            if (lane == 0) {
-                sh.cand = G * 32 + first;
-                // the ordered prefix rounds differently from the reference's
-                // sequential cumsum; a draw within that rounding of a boundary
-                // re-runs the reference's sequential walk (rare)
-                const double slack = 8.0 * (double)m * DBL_EPSILON * total;
-                if (P.tie_guard && (hi - target <= slack || target - lo <= slack)) sh.err = -1;
-            }
-        }
-    }
-    __syncthreads();
-    long long pick = sh.cand;
-    if (G == LLONG_MAX || sh.err == -1) {
+    const double slack = P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
+    long long pick = grbk_search(mem, m, gs, g0, g1, excl, sh.target, slack, sh);
+    if (pick < 0) {
         __syncthreads();
         if (tid == 0) {
             // Sequential replay of solver.hpp:243-253 + rng.hpp:84-99 with the same
@@ -513,14 +566,14 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
             const double u = sh.u;
             double total_seq = 0.0;
             for (long long r = 0; r < m; ++r) {
-                const double w = member_g(r);
+                const double w = mem(r);
                 if (w >= 0.0) total_seq = __dadd_rn(total_seq, w);
             }
             const double tseq = __dmul_rn(u, total_seq);
             double cum = 0.0;
             long long found = -1, first_member = -1, last_change = -1;
             for (long long r = 0; r < m && found < 0; ++r) {
-                const double w = member_g(r);
+                const double w = mem(r);
                 if (w < 0.0) continue;
                 if (first_member < 0) first_member = r;
                 const double nc = __dadd_rn(cum, w);
@@ -530,13 +583,12 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
             }
             if (found < 0) found = last_change >= 0 ? last_change : first_member;
             sh.cand = found;
-            sh.err = 0;
             atomicAdd(&st->tie_guard_hits, 1);
         }
         __syncthreads();
         pick = sh.cand;
     }
-    *out_row = pick;
+    *out_row = P.row0 + pick;
     return 0;
 }
 
@@ -580,6 +632,19 @@ __device__ void finalize(const Params& P, DevState* st, double s, double mx, lon
     const int tid = threadIdx.x;
     const int mode = UPDATE ? st->fin_mode : FIN_NORMS;
     __syncthreads();
+    if (P.pack) {
+        // sharded: publish this shard's record; the global reduction, the stop
+        // logic and the selection run in k_sel1/k_sel2 after the allgather
+        if (tid == 0) {
+            st->cnt_r = 0u;
+            double* rec = P.recs + 4 * P.rank;
+            rec[0] = s;
+            rec[1] = mx;
+            rec[2] = (double)ax;
+            rec[3] = P.Xref ? st->err_sq : 0.0;
+        }
+        return;
+    }
     if (tid == 0) {
         st->cnt_r = 0u;
         st->r_fro_sq = s;
@@ -674,8 +739,8 @@ __global__ void __launch_bounds__(kThreads) k_r(Params P) {
     double coef = 0.0;
     long long sel = 0;
     if (UPDATE) {
-        coef = st->coef;
-        sel = st->sel;
+        coef = P.pack ? P.pack[P.n + P.p + 1] : st->coef;
+        sel = P.pack ? (long long)P.pack[P.n + P.p] : st->sel;
     }
     for (long long t = tid; t < r1 - r0; t += kThreads) rowacc[t] = 0.0;
     for (long long c0 = 0; c0 < n; c0 += P.r_chunk) {
@@ -847,8 +912,8 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
     long long sel = 0;
     double coef = 0.0;
     if (UPDATE) {
-        coef = st->coef;
-        sel = st->sel;
+        coef = P.pack ? P.pack[P.n + P.p + 1] : st->coef;
+        sel = P.pack ? (long long)P.pack[P.n + P.p] : st->sel;
     }
     if (warp == kTmaConsumerWarps) {
         // ---- producer: grab rows dynamically, stream tiles (+ z segment, + G entry) ----
@@ -981,6 +1046,216 @@ size_t tma_smem_bytes(const Params& P) {
     return (size_t)P.r_stages * P.r_chunk * 8 * (P.r_zstage ? 2 : 1) + 2 * P.r_stages * 8;
 }
 
+// ------------------------------------------------------------------------
+// Sharded selection, part 1 (after the record allgather): global ‖R‖², max
+// ratio / argmax and ‖X−X_ref‖² in rank order (identical on every rank), the
+// stop / divergence logic, and for GRBK this shard's member mass (group sums
+// over the local rows, kept in P.gsum for part 2).
+__global__ void __launch_bounds__(kThreads) k_sel1(Params P, int update) {
+    __shared__ SelShared sh;
+    pdl_wait();
+    DevState* st = P.st;
+    if (update && halted(st)) return;
+    const int tid = threadIdx.x;
+    const int mode = update ? st->fin_mode : FIN_NORMS;
+    if (tid == 0) {
+        double s = 0.0, err = 0.0, mx = -INFINITY;
+        long long ax = LLONG_MAX;
+        for (int r = 0; r < P.world; ++r) {
+            const double* rec = P.recs + 4 * r;
+            s += rec[0];
+            maxidx_merge(mx, ax, rec[1], (long long)rec[2]);
+            err += rec[3];
+        }
+        st->err_sq = err;
+        st->r_fro_sq = s;
+        st->max_ratio = mx;
+        st->argmax = ax;
+        st->sel_valid = 0;
+        const double cf = P.c_fro > 0.0 ? P.c_fro : 1.0;
+        const double rel = sqrt(s > 0.0 ? s : 0.0) / cf;
+        if (mode != FIN_NORMS && !isfinite(s)) {  // solver.hpp:306-307
+            st->status = ST_ERROR;
+            st->err_code = 4;
+            st->err_k = st->k;
+            st->err_val = sqrt(fabs(s));
+        } else if (mode == FIN_ITERATION) {
+            const unsigned long long k = st->k;
+            const double metric = P.stop_kind == 0 ? err / P.ref_sq : rel;
+            const unsigned long long slot = k - st->k0;
+            if (slot < P.trace_cap) {
+                P.trace_row[slot] = (long long)P.pack[P.n + P.p];
+                P.trace_metric[slot] = metric;
+                P.trace_rel[slot] = rel;
+            }
+            st->k = k + 1;
+            st->metric = metric;
+            if (st->run_mode && metric <= P.tol) st->status = ST_PAUSE;
+            else if (st->run_mode && !(s > 0.0)) st->status = ST_ZERO;
+        } else {
+            st->metric = P.stop_kind == 0 ? err / P.ref_sq : rel;
+        }
+    }
+    __syncthreads();
+    if ((P.method == 2 || P.method == 3) && !st->replay && st->r_fro_sq > 0.0 &&
+        st->status != ST_ERROR) {
+        const Member mem = make_member(P, st, P.theta);
+        grbk_group_sums(mem, P.m, P.gsum);
+        long long g0, g1;
+        double excl;
+        const double tot = grbk_prefix(P.gsum, (P.m + 31) / 32, sh, g0, g1, excl);
+        if (tid == 0) P.masses[P.rank] = tot;
+    }
+}
+
+// Sharded selection, part 2 (after the mass allgather): every rank draws the
+// same uniform from its identical xoshiro state, finds the owning shard and
+// the row; the owner packs R_i | A_i | i | coef into pack_send (everyone else
+// contributes zeros), and the allreduce that follows hands the row to all.
+__global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
+    __shared__ SelShared sh;
+    __shared__ long long s_sel;
+    __shared__ int s_owner;
+    pdl_wait();
+    DevState* st = P.st;
+    const int tid = threadIdx.x;
+    const long long n = P.n, p = P.p;
+    const long long mg = P.m_global;
+    if (st->status != ST_RUN || st->k >= st->k_limit) return;
+    if (tid == 0) {
+        for (int k = 0; k < 4; ++k) st->rng_snap[k] = st->rng[k];
+        st->cyclic_snap = st->cyclic_pos;
+        st->skipped_snap = st->skipped_zero_rows;
+        s_sel = -1;
+        s_owner = -1;
+        sh.err = 0;
+        const int method = P.method;
+        if (st->replay) {
+            const long long row = P.forced_rows[st->k - st->k0];
+            if (row < 0 || row >= mg || !(P.a_sq_g[row] > 0.0)) sh.err = 2;
+            else s_sel = row;
+            if (method == 1 || method == 2 || method == 3) (void)rng_next(st->rng);
+            if (method == 0 && !sh.err) st->cyclic_pos = (unsigned long long)((row + 1) % mg);
+        } else if (method == 4) {  // MWRBK
+            s_sel = st->argmax;
+        } else if (method == 0) {  // BK over the global rows
+            sh.err = 2;
+            for (long long tries = 0; tries < mg; ++tries) {
+                const long long i = (long long)st->cyclic_pos;
+                st->cyclic_pos = (st->cyclic_pos + 1) % (unsigned long long)mg;
+                if (P.a_sq_g[i] > 0.0) {
+                    s_sel = i;
+                    sh.err = 0;
+                    break;
+                }
+                ++st->skipped_zero_rows;
+            }
+        } else if (method == 1) {  // RBK on the global CDF
+            const double* cum = P.rbk_cum;
+            const double total = cum[mg - 1];
+            if (!(total > 0.0)) {
+                sh.err = 2;
+            } else {
+                const double target = __dmul_rn(rng_unit(st->rng), total);
+                long long lo = 0, hi = mg - 1;
+                while (lo < hi) {
+                    const long long mid = (lo + hi) / 2;
+                    if (cum[mid] <= target) lo = mid + 1;
+                    else hi = mid;
+                }
+                while (lo > 0 && cum[lo] == cum[lo - 1]) --lo;
+                s_sel = lo;
+            }
+        } else {  // GRBK / RGRBK: shard masses in rank order, then the owner searches
+            if (!(st->r_fro_sq > 0.0)) {
+                sh.err = 2;
+            } else {
+                double total = 0.0;
+                for (int r = 0; r < P.world; ++r) total = __dadd_rn(total, P.masses[r]);
+                if (!(total > 0.0)) {
+                    sh.err = 2;
+                } else {
+                    sh.u = rng_unit(st->rng);
+                    sh.target = __dmul_rn(sh.u, total);
+                    double before = 0.0;
+                    int owner = -1, last_pos = -1;
+                    for (int r = 0; r < P.world; ++r) {
+                        if (P.masses[r] > 0.0) last_pos = r;
+                        const double nc = __dadd_rn(before, P.masses[r]);
+                        if (owner < 0 && nc > sh.target) owner = r;
+                        if (owner < 0) before = nc;
+                    }
+                    if (owner < 0) {  // target rounded past the last cum: last positive shard
+                        owner = last_pos;
+                        before = 0.0;
+                        for (int r = 0; r < owner; ++r) before = __dadd_rn(before, P.masses[r]);
+                        sh.target = __dadd_rn(before, 0.5 * P.masses[owner]);
+                    }
+                    s_owner = owner;
+                    sh.redv[1] = before;  // mass of the shards before the owner
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (sh.err) {
+        if (tid == 0) {
+            st->status = ST_ERROR;
+            st->err_code = sh.err;
+            st->err_k = st->k;
+        }
+        return;
+    }
+    const long long mloc = P.m;
+    if ((P.method == 2 || P.method == 3) && !st->replay) {
+        if (s_owner == P.rank) {
+            const Member mem = make_member(P, st, P.theta);
+            long long g0, g1;
+            double excl;
+            (void)grbk_prefix(P.gsum, (mloc + 31) / 32, sh, g0, g1, excl);
+            const double base = sh.redv[1];
+            long long local = grbk_search(mem, mloc, P.gsum, g0, g1, __dadd_rn(base, excl),
+                                          sh.target, -1.0, sh);
+            if (local < 0) {  // rounding disagreement: last member of the shard with mass
+                if (tid == 0) {
+                    local = 0;
+                    for (long long r = 0; r < mloc; ++r)
+                        if (mem(r) > 0.0) local = r;
+                    sh.cand = local;
+                }
+                __syncthreads();
+                local = sh.cand;
+            }
+            if (tid == 0) s_sel = P.row0 + local;
+        }
+    } else if (tid == 0) {
+        s_owner = (int)(s_sel / mloc);  // equal shards
+    }
+    __syncthreads();
+    // pack: the owner writes its row; the previous owner clears its stale one
+    const bool mine = s_owner == P.rank;
+    const bool was = st->packed != 0;  // this rank packed last time
+    if (mine) {
+        const long long il = s_sel - P.row0;
+        const double* Rr = P.R + il * n;
+        const double* Ar = P.A + il * p;
+        for (long long k = tid; k < n; k += blockDim.x) P.pack_send[k] = Rr[k];
+        for (long long k = tid; k < p; k += blockDim.x) P.pack_send[n + k] = Ar[k];
+        if (tid == 0) {
+            P.pack_send[n + p] = (double)s_sel;
+            P.pack_send[n + p + 1] = __ddiv_rn(P.alpha, P.a_sq[il]);
+        }
+    } else if (was) {
+        for (long long k = tid; k < n + p + 2; k += blockDim.x) P.pack_send[k] = 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        st->sel = s_sel;  // −1 on non-owners for GRBK; the pack carries the row
+        st->sel_valid = 1;
+        st->packed = mine ? 1 : 0;
+    }
+}
+
 // K3 standalone: (re)select with the configured rule (consume=0: speculative,
 // snapshot kept) or run a public select_*(θ) that consumes the stream (consume=1).
 __global__ void __launch_bounds__(kThreads) k_select(Params P, int method, double theta,
@@ -1053,9 +1328,9 @@ __global__ void __launch_bounds__(kThreads) k_err_fresh(Params P) {
     __shared__ double red[kWarps];
     __shared__ bool last;
     DevState* st = P.st;
-    const long long total = P.p * P.q;
+    const long long total = P.x1r * P.q;  // this rank's rows of X: [x0r, x1r)
     double acc = 0.0, bad = 0.0;
-    for (long long e = (long long)blockIdx.x * kThreads + threadIdx.x; e < total;
+    for (long long e = P.x0r * P.q + (long long)blockIdx.x * kThreads + threadIdx.x; e < total;
          e += (long long)gridDim.x * kThreads) {
         const double x = P.X[e];
         if (!isfinite(x)) bad += 1.0;
@@ -1351,6 +1626,12 @@ void launch_row_sq_seq(const double* A, long long m, long long p, double* out, c
 void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* total, cudaStream_t s) {
     k_cumsum_seq<<<1, 1, 0, s>>>(a_sq, m, cum, total);
 }
+
+void launch_sel1(const Params& P, cudaStream_t s, bool update) {
+    k_sel1<<<1, kThreads, 0, s>>>(P, update ? 1 : 0);
+}
+
+void launch_sel2(const Params& P, cudaStream_t s) { k_sel2<<<1, kThreads, 0, s>>>(P); }
 
 void launch_fill(double* p, long long n, double v, cudaStream_t s) {
     int grid = (int)std::min<long long>(1184, (n + 255) / 256);

@@ -19,13 +19,46 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include "../../include/axb_b200.h"
 #include "axb_device.cuh"
+#include "axb_nccl.cuh"
+
+namespace axb_nccl {
+const Api* api(const char** why) {
+    static Api a;
+    static int state = 0;  // 0 untried, 1 ok, −1 failed
+    static const char* reason = "";
+    if (state == 0) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            state = -1;
+            reason = "libnccl.so.2 not found";
+        } else {
+            a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+            a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+            a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+            a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+            a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+            a.GetErrorString =
+                reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+            const bool ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce &&
+                            a.AllGather && a.GetErrorString;
+            state = ok ? 1 : -1;
+            if (!ok) reason = "libnccl.so.2 lacks a required symbol";
+        }
+    }
+    if (why) *why = reason;
+    return state == 1 ? &a : nullptr;
+}
+}  // namespace axb_nccl
 
 using namespace axb_dev;
 
 namespace {
+thread_local std::string g_create_err;  // message of the last handle-less failure
 
 struct AxbError {
     int code;
@@ -160,6 +193,13 @@ struct axb_solver {
     DevBuf<unsigned int> zcnt;
     DevBuf<RowRecord> rrec;
     DevBuf<long long> tr_row, forced;
+    // row sharding (§8(e))
+    bool sharded = false;
+    int world = 1, rank = 0;
+    uint64_t m_g = 0, row0 = 0, p_loc = 0, n_loc = 0;
+    ncclComm_t comm = nullptr;
+    const axb_nccl::Api* nc = nullptr;
+    DevBuf<double> pack, pack_send, recs, masses, a_sq_g, scal_ag;
     DevBuf<int> flags;
     DevBuf<DevState> st;
     DevState* hs = nullptr;  // pinned host mirror
@@ -250,6 +290,37 @@ struct axb_solver {
         return out;
     }
 
+    // ---------------------------------------------------------------- collectives
+    void nccl_ck(ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) fail(AXB_CUDA_ERROR, "%s: %s", what, nc->GetErrorString(r));
+    }
+    void allgather_inplace(double* buf, size_t count) {  // buf holds world × count
+        nccl_ck(nc->AllGather(buf + (size_t)rank * count, buf, count, ncclFloat64, comm, stream),
+                "ncclAllGather");
+    }
+    void allreduce(const double* send, double* recv, size_t count) {
+        nccl_ck(nc->AllReduce(send, recv, count, ncclFloat64, ncclSum, comm, stream),
+                "ncclAllReduce");
+    }
+    // Σ over ranks in rank order of a host scalar (identical on every rank)
+    double global_sum(double local) {
+        if (!sharded) return local;
+        ck(cudaMemcpyAsync(scal_ag.p + rank, &local, sizeof(double), cudaMemcpyHostToDevice, stream),
+           "global sum");
+        allgather_inplace(scal_ag.p, 1);
+        std::vector<double> v(world);
+        ck(cudaMemcpyAsync(v.data(), scal_ag.p, sizeof(double) * world, cudaMemcpyDeviceToHost,
+                           stream), "global sum");
+        sync("global sum");
+        double acc = 0.0;
+        for (double x : v) acc += x;
+        return acc;
+    }
+    // all ranks' rows of X into every rank's full X (p_loc rows per rank)
+    void gather_X() {
+        if (sharded) allgather_inplace(X.p, (size_t)p_loc * q);
+    }
+
     // ---------------------------------------------------------------- init
     void create(const double* A_in, const double* B_in, const double* C_in, const double* X0_in) {
         // Method::validate (solver.hpp:30-38)
@@ -265,8 +336,30 @@ struct axb_solver {
             fail(AXB_CONFIG_ERROR, "unknown alpha rule");
         if (m == 0 || p == 0) fail(AXB_SHAPE_ERROR, "row_sq_norms: empty matrix");
         if (q == 0 || n == 0) fail(AXB_SHAPE_ERROR, "spectral_norm: empty matrix");
-        if (opt.nccl_comm || opt.world_size > 1)
-            fail(AXB_CONFIG_ERROR, "row sharding needs the sharded build (axb_shard)");
+        if (opt.nccl_comm) {
+            sharded = true;
+            world = std::max(1, opt.world_size);
+            rank = opt.rank;
+            m_g = opt.m_global ? opt.m_global : m * (uint64_t)world;
+            row0 = opt.row_offset;
+            const char* why = "";
+            nc = axb_nccl::api(&why);
+            if (!nc) fail(AXB_CUDA_ERROR, "row sharding needs NCCL: %s", why);
+            comm = static_cast<ncclComm_t>(opt.nccl_comm);
+            if (rank < 0 || rank >= world) fail(AXB_CONFIG_ERROR, "rank %d outside [0, %d)", rank, world);
+            if (m_g != m * (uint64_t)world || row0 != m * (uint64_t)rank)
+                fail(AXB_CONFIG_ERROR,
+                     "row sharding needs equal contiguous shards: m_global = world·m and "
+                     "row_offset = rank·m");
+        } else if (opt.world_size > 1) {
+            fail(AXB_CONFIG_ERROR, "world_size > 1 needs an NCCL communicator (opt.nccl_comm)");
+        } else {
+            m_g = m;
+            row0 = 0;
+        }
+        p_loc = (p + world - 1) / world;
+        n_loc = (n + world - 1) / world;
+        if (n_loc & 1) ++n_loc;
         if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN && !cfg.reference)
             fail(AXB_CONFIG_ERROR, "solution_rrn stopping needs a reference solution");
 
@@ -294,7 +387,9 @@ struct axb_solver {
         B.alloc(q * n, "B");
         C.alloc(m * n, "C");
         R.alloc(m * n, "R");
-        X.alloc(p * q, "X");
+        X.alloc(p_loc * world * q, "X");
+        if (p_loc * world > p)
+            ck(cudaMemsetAsync(X.p, 0, sizeof(double) * p_loc * world * q, stream), "X pad");
         ck(cudaMemcpyAsync(A.p, A_in, sizeof(double) * m * p, kind, stream), "copy A");
         ck(cudaMemcpyAsync(B.p, B_in, sizeof(double) * q * n, kind, stream), "copy B");
         ck(cudaMemcpyAsync(C.p, C_in, sizeof(double) * m * n, kind, stream), "copy C");
@@ -308,14 +403,31 @@ struct axb_solver {
                "copy reference");
         }
         a_sq.alloc(m, "a_sq");
-        rbk_cum.alloc(m, "rbk_cum");
+        rbk_cum.alloc(m_g, "rbk_cum");
         r_sq.alloc(m, "r_sq");
         scal.alloc(4, "scalars");
+        if (sharded) {
+            a_sq_g.alloc(m_g, "a_sq global");
+            scal_ag.alloc(world, "scalar allgather");
+            pack.alloc(n + p + 2, "pack");
+            pack_send.alloc(n + p + 2, "pack send");
+            ck(cudaMemsetAsync(pack_send.p, 0, sizeof(double) * (n + p + 2), stream), "pack");
+            recs.alloc(4 * (size_t)world, "records");
+            masses.alloc(world, "masses");
+            ck(cudaMemsetAsync(masses.p, 0, sizeof(double) * world, stream), "masses");
+        }
         sq_part.alloc(sumsq_parts((long long)std::max({m * n, q * n, p * q, m * p})), "parts");
 
         // a_sq_ = row_sq_norms(A); a_fro_sq_; rbk_cumsum_ (solver.hpp:156-166), sequential
         launch_row_sq_seq(A.p, (long long)m, (long long)p, a_sq.p, stream);
-        launch_cumsum_seq(a_sq.p, (long long)m, rbk_cum.p, scal.p, stream);
+        const double* a_all = a_sq.p;
+        if (sharded) {  // every rank holds all ‖A_i‖² (BK/RBK selection, ‖A‖²_F, CDF)
+            ck(cudaMemcpyAsync(a_sq_g.p + row0, a_sq.p, sizeof(double) * m,
+                               cudaMemcpyDeviceToDevice, stream), "a_sq slot");
+            allgather_inplace(a_sq_g.p, m);
+            a_all = a_sq_g.p;
+        }
+        launch_cumsum_seq(a_all, (long long)m_g, rbk_cum.p, scal.p, stream);
         a_sq_h.resize(m);
         ck(cudaMemcpyAsync(a_sq_h.data(), a_sq.p, sizeof(double) * m, cudaMemcpyDeviceToHost,
                            stream), "a_sq");
@@ -358,7 +470,7 @@ struct axb_solver {
         // gram_ = gram_mmt(A) (solver.hpp:171): cached when it fits in HBM
         size_t free_b = 0, total_b = 0;
         ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
-        const double gbytes = 8.0 * (double)m * (double)m;
+        const double gbytes = 8.0 * (double)m_g * (double)m;
         gram_cached = opt.cache_gram == 1 ||
                       (opt.cache_gram < 0 && gbytes < 0.45 * (double)free_b &&
                        gbytes <= 48e9);
@@ -367,14 +479,25 @@ struct axb_solver {
         gemm_sq.alloc(gparts, "gemm parts");
         gemm_diff.alloc(gparts, "gemm parts");
         if (gram_cached) {
-            G.alloc(m * m, "G");
+            // G[:, local rows] = A_all · A_localᵀ (m_global × m); one GPU: G = A·Aᵀ
+            G.alloc(m_g * m, "G");
+            DevBuf<double> A_all;
+            const double* Aa = A.p;
+            if (sharded) {
+                A_all.alloc(m_g * p, "A gathered");
+                ck(cudaMemcpyAsync(A_all.p + row0 * p, A.p, sizeof(double) * m * p,
+                                   cudaMemcpyDeviceToDevice, stream), "A slot");
+                allgather_inplace(A_all.p, m * p);
+                Aa = A_all.p;
+            }
             GemmArgs ga{};
-            ga.M = m; ga.N = m; ga.K = p;
-            ga.A = A.p; ga.lda = p;
+            ga.M = m_g; ga.N = m; ga.K = p;
+            ga.A = Aa; ga.lda = p;
             ga.B = A.p; ga.ldb = p; ga.b_trans = 1;
             ga.D = G.p; ga.ldd = m;
             ga.store = 1;
             launch_gemm(ga, stream);
+            sync("G");  // A_all released at scope end
         } else {
             g.alloc(m, "g");
         }
@@ -386,7 +509,7 @@ struct axb_solver {
             ck(cudaMemcpyAsync(R.p, C.p, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, stream),
                "R = C");
         }
-        c_fro = std::sqrt(reduce_sumsq(C.p, m * n));  // :179
+        c_fro = std::sqrt(global_sum(reduce_sumsq(C.p, m * n)));  // :179
         if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) {   // :180-189
             ref_sq = reduce_sumsq(Xref.p, p * q);
             if (ref_sq == 0.0) fail(AXB_DOMAIN_ERROR, "solution_rrn: zero reference");
@@ -394,10 +517,16 @@ struct axb_solver {
 
         // iteration buffers and launch geometry
         y.alloc(q, "y");
-        z.alloc(n, "z");
+        z.alloc(std::max<uint64_t>(n, n_loc * world), "z");
         P.m = (long long)m; P.p = (long long)p; P.q = (long long)q; P.n = (long long)n;
-        P.row0 = 0;
-        P.m_global = (long long)m;
+        P.row0 = (long long)row0;
+        P.m_global = (long long)m_g;
+        P.world = world;
+        P.rank = rank;
+        P.c0 = sharded ? std::min<long long>((long long)n, (long long)(rank * n_loc)) : 0;
+        P.c1 = sharded ? std::min<long long>((long long)n, P.c0 + (long long)n_loc) : (long long)n;
+        P.x0r = sharded ? std::min<long long>((long long)p, (long long)(rank * p_loc)) : 0;
+        P.x1r = sharded ? std::min<long long>((long long)p, P.x0r + (long long)p_loc) : (long long)p;
         const int target = 148 * 4;
         P.r_tma = (n % 2 == 0) && opt_r_tma();
         if (P.r_tma) {
@@ -419,12 +548,12 @@ struct axb_solver {
         }
         const uint64_t items = q + (gram_cached ? 0 : m);
         P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(148 * 16, items));
-        P.z_nslab = (int)((n + 511) / 512);
+        P.z_nslab = (int)std::max<long long>(1, (P.c1 - P.c0 + 511) / 512);
         int nj = (int)std::max<uint64_t>(1, std::min<uint64_t>((target + P.z_nslab - 1) / P.z_nslab,
                                                                 (q + 7) / 8));
         P.z_jrows = (int)((q + nj - 1) / nj);
         P.z_nj = (int)((q + P.z_jrows - 1) / P.z_jrows);
-        P.x_ctas = (int)std::max<uint64_t>(1, std::min<uint64_t>(296, (p + 7) / 8));
+        P.x_ctas = (int)std::max<long long>(1, std::min<long long>(296, (P.x1r - P.x0r + 7) / 8));
         zpart.alloc((size_t)P.z_nj * n, "zpart");
         zcnt.alloc(P.z_nslab, "zcnt");
         ck(cudaMemsetAsync(zcnt.p, 0, sizeof(unsigned) * P.z_nslab, stream), "zcnt");
@@ -446,6 +575,11 @@ struct axb_solver {
         P.trace_rel = tr_rel.p; P.trace_cap = trace_cap; P.member_flags = flags.p; P.st = st.p;
         P.forced_rows = forced.p;
         P.gsum = gsum.p;
+        P.pack = sharded ? pack.p : nullptr;
+        P.pack_send = pack_send.p;
+        P.recs = recs.p;
+        P.masses = masses.p;
+        P.a_sq_g = sharded ? a_sq_g.p : a_sq.p;
         P.alpha = alpha;
         P.theta = cfg.method == AXB_RGRBK ? cfg.theta : 0.5;
         P.a_fro_sq = a_fro_sq;
@@ -454,7 +588,7 @@ struct axb_solver {
         P.c_fro = c_fro;
         P.method = cfg.method;
         P.stop_kind = cfg.stop_kind;
-        P.tie_guard = opt.tie_guard ? 1 : 0;
+        P.tie_guard = (opt.tie_guard && !sharded) ? 1 : 0;  // exact replay needs all rows
         P.vec2 = (n % 2) == 0;
 
         // DevState: RngStream(cfg.seed) (rng.hpp:20-25), k = 0
@@ -549,8 +683,17 @@ struct axb_solver {
 
     // r_sq_, r_fro_sq_, reductions of the current R (solver.hpp:174-177, :468-476)
     void adopt_norms() {
-        launch_r(P, stream, false);
-        if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) launch_err_fresh(P, stream);
+        if (sharded) {
+            // local ‖X−X_ref‖² first: this shard's record carries it
+            if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) launch_err_fresh(P, stream);
+            launch_r(P, stream, false);
+            allgather_inplace(recs.p, 4);
+            launch_sel1(P, stream, false);
+            allgather_inplace(masses.p, 1);
+        } else {
+            launch_r(P, stream, false);
+            if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) launch_err_fresh(P, stream);
+        }
         sel_valid = false;
     }
 
@@ -561,7 +704,12 @@ struct axb_solver {
     }
 
     void ensure_selection() {
-        if (!sel_valid) {
+        if (!sel_valid && sharded) {
+            launch_sel2(P, stream);
+            allreduce(pack_send.p, pack.p, n + p + 2);
+            kernel_launches += 1;
+            sel_valid = true;
+        } else if (!sel_valid) {
             launch_select(P, stream, cfg.method, P.theta, 0);
             ++kernel_launches;
             sel_valid = true;  // confirmed (or error) at the next state pull
@@ -569,21 +717,32 @@ struct axb_solver {
     }
 
     // ---------------------------------------------------------------- iteration
-    void launch_iteration() {
+    // one iteration; sharded: y partial → allreduce, z slice → allgather, local R
+    // update → record allgather → global stop logic + shard masses → mass
+    // allgather → draw + owner pack → row allreduce
+    void enqueue_iteration() {
         launch_yg(P, stream, !gram_cached);
+        if (sharded) allreduce(y.p, y.p, q);
         launch_zx(P, stream);
+        if (sharded) allgather_inplace(z.p, n_loc);
         launch_r(P, stream, true);
-        kernel_launches += 3;
+        if (sharded) {
+            allgather_inplace(recs.p, 4);
+            launch_sel1(P, stream, true);
+            allgather_inplace(masses.p, 1);
+            launch_sel2(P, stream);
+            allreduce(pack_send.p, pack.p, n + p + 2);
+        }
+    }
+    void launch_iteration() {
+        enqueue_iteration();
+        kernel_launches += sharded ? 5 : 3;
     }
 
     void build_graph() {
         cudaGraph_t g0 = nullptr;
         ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
-        for (int i = 0; i < graph_iters; ++i) {
-            launch_yg(P, stream, !gram_cached);
-            launch_zx(P, stream);
-            launch_r(P, stream, true);
-        }
+        for (int i = 0; i < graph_iters; ++i) enqueue_iteration();
         ck(cudaStreamEndCapture(stream, &g0), "capture end");
         ck(cudaGraphInstantiate(&graph, g0, 0), "graph instantiate");
         cudaGraphDestroy(g0);
@@ -602,11 +761,20 @@ struct axb_solver {
             }
             for (uint64_t i = 0; i < nb; ++i) {
                 launch_yg(P, stream, !gram_cached);
+                if (sharded) allreduce(y.p, y.p, q);
                 launch_zx(P, stream);
+                if (sharded) allgather_inplace(z.p, n_loc);
                 ck(cudaEventRecord(prof_ev[2 * i], stream), "ev");
                 launch_r(P, stream, true);
                 ck(cudaEventRecord(prof_ev[2 * i + 1], stream), "ev");
-                kernel_launches += 3;
+                if (sharded) {
+                    allgather_inplace(recs.p, 4);
+                    launch_sel1(P, stream, true);
+                    allgather_inplace(masses.p, 1);
+                    launch_sel2(P, stream);
+                    allreduce(pack_send.p, pack.p, n + p + 2);
+                }
+                kernel_launches += sharded ? 5 : 3;
             }
         } else if (nb < (uint64_t)graph_iters) {
             for (uint64_t i = 0; i < nb; ++i) launch_iteration();
@@ -614,7 +782,7 @@ struct axb_solver {
             if (!graph) build_graph();
             const uint64_t launches = (nb + graph_iters - 1) / graph_iters;
             for (uint64_t i = 0; i < launches; ++i) ck(cudaGraphLaunch(graph, stream), "graph launch");
-            kernel_launches += 3 * nb;
+            kernel_launches += (sharded ? 5 : 3) * nb;
         }
         pull_state();
         if (profiling) {
@@ -706,7 +874,19 @@ struct axb_solver {
         loop_ms = ms;
     }
 
+    void not_sharded(const char* what) {
+        if (sharded)
+            fail(AXB_CONFIG_ERROR, "%s is not available on a row-sharded solver (use step/steps/"
+                                   "replay/run)", what);
+    }
+    void set_err_sq(double v) {  // publish a host-reduced ‖X−X_ref‖² into DevState
+        ck(cudaMemcpyAsync(reinterpret_cast<char*>(st.p) + offsetof(DevState, err_sq), &v,
+                           sizeof(double), cudaMemcpyHostToDevice, stream), "err_sq");
+        sync("err_sq");
+    }
+
     void update_row(uint64_t i) {  // solver.hpp:264-318
+        not_sharded("update_row");
         if (i >= m) fail(AXB_SHAPE_ERROR, "update_row: row %llu out of range", (unsigned long long)i);
         if (!(a_sq_h[i] > 0.0)) fail(AXB_DOMAIN_ERROR, "update_row: zero row selected");
         rollback();
@@ -731,33 +911,40 @@ struct axb_solver {
         return std::sqrt(std::max(s, 0.0)) / (c_fro > 0.0 ? c_fro : 1.0);
     }
     double exact_residual_rel() {  // solver.hpp:417-419
+        gather_X();
         exact_residual_into(nullptr, gemm_sq.p, nullptr, false);
         launch_reduce_parts(gemm_sq.p, gemm_num_ctas((long long)m, (long long)n), scal.p, stream);
         double s = 0.0;
         ck(cudaMemcpyAsync(&s, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "exact");
         sync("exact residual");
+        s = global_sum(s);
         return std::sqrt(s) / (c_fro > 0.0 ? c_fro : 1.0);
     }
     double exact_metric() {  // solver.hpp:412-416
         if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) {
             launch_err_fresh(P, stream);
             pull_state();
-            return hs->err_sq / ref_sq;
+            if (!sharded) return hs->err_sq / ref_sq;
+            const double e = global_sum(hs->err_sq);
+            set_err_sq(e);
+            return e / ref_sq;
         }
         return exact_residual_rel();
     }
     double residual_drift() {  // solver.hpp:423
+        gather_X();
         exact_residual_into(nullptr, nullptr, R.p, false);
         launch_reduce_parts(gemm_diff.p, gemm_num_ctas((long long)m, (long long)n), scal.p, stream);
         double s = 0.0;
         ck(cudaMemcpyAsync(&s, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "drift");
         sync("drift");
-        return std::sqrt(s);
+        return std::sqrt(global_sum(s));
     }
     void checkpoint() {  // solver.hpp:427-436
         launch_err_fresh(P, stream);
         pull_state();
-        if (!hs->x_finite) {
+        const bool finite = global_sum(hs->x_finite ? 0.0 : 1.0) == 0.0;
+        if (!finite) {
             AxbError e{AXB_DIVERGENCE_ERROR, ""};
             e.k = k;
             e.val = std::sqrt(std::max(hs->r_fro_sq, 0.0));
@@ -768,11 +955,14 @@ struct axb_solver {
             throw e;
         }
         rollback();
+        gather_X();
         // exact residual written in place over R; the epilogue reads R_old first
         exact_residual_into(R.p, nullptr, R.p, true);
         launch_reduce_parts(gemm_diff.p, gemm_num_ctas((long long)m, (long long)n), scal.p, stream);
         double d2 = 0.0;
         ck(cudaMemcpyAsync(&d2, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "drift");
+        sync("checkpoint drift");
+        d2 = global_sum(d2);
         adopt_norms();
         sync("checkpoint");
         const double drift = std::sqrt(d2);
@@ -782,6 +972,7 @@ struct axb_solver {
     }
     void resync() {  // solver.hpp:478
         rollback();
+        gather_X();
         exact_residual_into(R.p, nullptr, nullptr, true);
         adopt_norms();
     }
@@ -852,6 +1043,7 @@ struct axb_solver {
         rep->skipped_zero_rows = hs->skipped_zero_rows;
         rep->trace_len = ntrace;
         if (x_out) {
+            gather_X();
             ck(cudaMemcpyAsync(x_out, X.p, sizeof(double) * p * q, cudaMemcpyDeviceToHost, stream),
                "X out");
             sync("X out");
@@ -860,6 +1052,7 @@ struct axb_solver {
 
     // ---------------------------------------------------------------- public selects
     uint64_t select_consume(int method, double theta) {
+        not_sharded("select_*");
         rollback();
         reset_status();
         launch_select(P, stream, method, theta, 1);
@@ -877,6 +1070,7 @@ struct axb_solver {
         return (uint64_t)hs->q_row;
     }
     void query(double theta, bool want_set) {
+        not_sharded("greedy threshold / index-set queries");
         reset_status();
         launch_query(P, stream, theta, want_set ? 1 : 0);
         pull_state();
@@ -890,7 +1084,6 @@ struct axb_solver {
 // =========================================================================
 // C-ABI
 namespace {
-thread_local std::string g_create_err;
 
 template <class F>
 int guarded(axb_solver* s, F&& f) {
@@ -922,6 +1115,46 @@ void axb_options_default(axb_options* o) {
 }
 
 int axb_abi_version(void) { return AXB_B200_ABI_VERSION; }
+
+int axb_nccl_unique_id(unsigned char out[128]) {
+    const char* why = "";
+    const axb_nccl::Api* a = axb_nccl::api(&why);
+    if (!a) {
+        g_create_err = why;
+        return AXB_CUDA_ERROR;
+    }
+    ncclUniqueId id;
+    if (a->GetUniqueId(&id) != ncclSuccess) return AXB_CUDA_ERROR;
+    std::memcpy(out, id.internal, 128);
+    return AXB_OK;
+}
+
+int axb_nccl_comm_create(int nranks, const unsigned char id[128], int rank, int device,
+                         void** comm) {
+    const char* why = "";
+    const axb_nccl::Api* a = axb_nccl::api(&why);
+    if (!a) {
+        g_create_err = why;
+        return AXB_CUDA_ERROR;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return AXB_CUDA_ERROR;
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    ncclComm_t c = nullptr;
+    const ncclResult_t r = a->CommInitRank(&c, nranks, uid, rank);
+    if (r != ncclSuccess) {
+        g_create_err = a->GetErrorString(r);
+        return AXB_CUDA_ERROR;
+    }
+    *comm = c;
+    return AXB_OK;
+}
+
+int axb_nccl_comm_destroy(void* comm) {
+    const axb_nccl::Api* a = axb_nccl::api(nullptr);
+    if (!a || !comm) return AXB_OK;
+    return a->CommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? AXB_OK : AXB_CUDA_ERROR;
+}
 
 int axb_device_available(void) {
     int n = 0;
@@ -1051,7 +1284,13 @@ static int copy_out(axb_solver* s, double* dst, const double* src, size_t count)
         ck(cudaMemcpy(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost), "copy out");
     });
 }
-int axb_solver_get_X(axb_solver* s, double* out) { return copy_out(s, out, s->X.p, s->p * s->q); }
+int axb_solver_get_X(axb_solver* s, double* out) {
+    const int st = guarded(s, [&] {
+        s->gather_X();
+        s->sync("gather X");
+    });
+    return st ? st : copy_out(s, out, s->X.p, s->p * s->q);
+}
 int axb_solver_get_R(axb_solver* s, double* out) { return copy_out(s, out, s->R.p, s->m * s->n); }
 int axb_solver_get_r_sq(axb_solver* s, double* out) { return copy_out(s, out, s->r_sq.p, s->m); }
 int axb_solver_get_a_sq(axb_solver* s, double* out) { return copy_out(s, out, s->a_sq.p, s->m); }

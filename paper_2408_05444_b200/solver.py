@@ -171,6 +171,13 @@ class Options:
     tie_guard: bool = True        # sequential re-check of near-boundary greedy draws
     spectral_max_iter: int = 0    # 0 = reference default 5000
     alpha_override: float = 0.0   # >0: use verbatim (e.g. the oracle's α)
+    # row sharding: this solver owns rows [row_offset, row_offset+m)
+    # of an m_global-row system; nccl_comm from nccl_comm_create() (see shard.py)
+    nccl_comm: int = 0
+    world_size: int = 1
+    rank: int = 0
+    m_global: int = 0
+    row_offset: int = 0
 
 
 def _device_ptr(a):
@@ -259,6 +266,11 @@ class Solver:
         o.tie_guard = 1 if opts.tie_guard else 0
         o.spectral_max_iter = opts.spectral_max_iter
         o.alpha_override = opts.alpha_override
+        o.nccl_comm = opts.nccl_comm or None
+        o.world_size = opts.world_size
+        o.rank = opts.rank
+        o.m_global = opts.m_global
+        o.row_offset = opts.row_offset
         h = C.c_void_p()
         st = lib.axb_solver_create(ptr(A), m, p, ptr(B), q, n, ptr(C_), ptr(X0), C.byref(c),
                                    C.byref(o), C.byref(h))

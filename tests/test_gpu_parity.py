@@ -173,3 +173,49 @@ def test_cpp_dropin_runs_on_device(axb, tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("iterations=")
+
+
+@pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.MWRBK, None), (O.RBK, None),
+                                       (O.BK, None), (O.RGRBK, 0.3)])
+def test_sharded_mode_one_rank(axb, orc, tag, theta):
+    """The row-sharded path (NCCL collectives, split selection, owner pack) on a
+    1-rank communicator: same rows and X as the oracle."""
+    from paper_2408_05444_b200 import shard
+
+    A, B, X, Cm = O.generate(orc, 7, 500, 100, 80, 400)
+    comm = shard.nccl_comm_create(1, shard.nccl_unique_id(), 0, 0)
+    try:
+        cfg_o = O.make_config(method=tag, theta=theta, seed=42, stop_kind=O.SOLUTION_RRN, tol=0.0,
+                              reference=X, refresh_interval=0)
+        so = O.Solver(orc, A, B, Cm, None, cfg_o)
+        cfg = axb.SolveConfig(method=axb_method(axb, tag, theta),
+                              stop=axb.StopRule.solution_rrn(0.0, X), seed=42, refresh_interval=0)
+        sg = shard.sharded_solver(A, B, Cm, None, cfg, comm, 1, 0)
+        ro = so.steps(1000)
+        rg = sg.steps(1000)
+        mism = np.nonzero(ro != rg)[0]
+        assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+        assert rel(sg.X(), so.X()) <= RTOL_X
+        # exact metric / checkpoint go through the sharded host paths too
+        assert sg.exact_metric() == pytest.approx(so.exact_metric(), rel=1e-8)
+        sg.checkpoint()
+        so.checkpoint()
+        np.testing.assert_array_equal(sg.steps(200), so.steps(200))
+        del sg
+    finally:
+        shard.nccl_comm_destroy(comm)
+
+
+def test_sharded_run_to_tolerance_one_rank(axb, orc):
+    from paper_2408_05444_b200 import shard
+
+    A, B, X, Cm = O.generate(orc, 7, 500, 100, 80, 400)
+    comm = shard.nccl_comm_create(1, shard.nccl_unique_id(), 0, 0)
+    try:
+        cfg = axb.SolveConfig(method=axb.Method.grbk(), stop=axb.StopRule.solution_rrn(1e-12, X),
+                              seed=42, refresh_interval=1000)
+        rep = shard.sharded_solver(A, B, Cm, None, cfg, comm, 1, 0).run()
+        assert rep.terminated_by == axb.Terminated.Tolerance
+        assert abs(rep.iterations - 13483) <= 2
+    finally:
+        shard.nccl_comm_destroy(comm)
