@@ -9,9 +9,13 @@ defaults.  One "step" = one Kaczmarz iteration (select → y → z/X → fused R
 Inputs are synthetic (seeded torch RNG on the device); R (537 MB) exceeds the 126 MB
 L2, so no explicit flush is needed between iterations.
 
-N > 1 (torchrun): one process per GPU, each solving its own independent system of
-the same shape (independent right-hand sides) — weak scaling, no
-data-path collective; value = Σ iterations / max-over-ranks device time.
+N > 1 (torchrun): one process per GPU and ONE system, row-sharded:
+each rank owns m/N rows of A, C, R and a column slice of B; per iteration the
+library issues NCCL collectives inside its CUDA graphs (y allreduce, z allgather,
+record/mass allgathers, owner-row allreduce).  Strong scaling: value = K global
+iterations / max-over-ranks device time.  A is generated in 8 fixed row blocks,
+so the global system is bit-identical at N = 1, 2, 4, 8.  --shard forces the
+sharded code path on one GPU (1-rank communicator).
 
 --impl reference: the reference's per-iteration algorithm on the host cores (the
 oracle C port, bitwise-pinned to the reference; kind "port"), one solver per core
@@ -47,6 +51,21 @@ CONFIGS = {
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+class stdout_to_stderr:
+    """Route C-level stdout (fd 1) to stderr, e.g. NCCL's version banner, so the
+    bench's stdout carries exactly one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
 
 
 def peaks():
@@ -108,16 +127,25 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- workload
-def make_inputs_device(cfg, seed, device):
+def make_inputs_device(cfg, seed, device, world=1, rank=0, blocks=8):
+    """This rank's rows of A and C (A drawn in `blocks` fixed row blocks so the
+    global system does not depend on the world size) plus full B, X*, X0."""
     import torch
 
-    g = torch.Generator(device=f"cuda:{device}").manual_seed(seed)
-    kw = dict(dtype=torch.float64, device=f"cuda:{device}", generator=g)
-    A = torch.randn(cfg["m"], cfg["p"], **kw) * cfg["scale_a"]
-    B = torch.randn(cfg["q"], cfg["n"], **kw) * cfg["scale_b"]
-    Xs = torch.randn(cfg["p"], cfg["q"], **kw)
+    dev = f"cuda:{device}"
+    kw = dict(dtype=torch.float64, device=dev)
+    mb = cfg["m"] // blocks
+    per = blocks // world
+    parts = []
+    for b in range(rank * per, (rank + 1) * per):
+        g = torch.Generator(device=dev).manual_seed(seed * 1000 + b)
+        parts.append(torch.randn(mb, cfg["p"], generator=g, **kw))
+    A = torch.cat(parts) * cfg["scale_a"]
+    g = torch.Generator(device=dev).manual_seed(seed * 1000 + 999)
+    B = torch.randn(cfg["q"], cfg["n"], generator=g, **kw) * cfg["scale_b"]
+    Xs = torch.randn(cfg["p"], cfg["q"], generator=g, **kw)
+    X0 = torch.randn(cfg["p"], cfg["q"], generator=g, **kw) if cfg["x0"] == "randn" else None
     C = (A @ Xs) @ B
-    X0 = torch.randn(cfg["p"], cfg["q"], **kw) if cfg["x0"] == "randn" else None
     torch.cuda.synchronize(device)
     return A, B, C, X0, Xs
 
@@ -231,7 +259,7 @@ def reference_arm(args, cfg):
         "impl": "reference",
         "metric": "kaczmarz_iterations_per_sec", "value": value, "unit": "iter/s",
         "n_gpus": args.gpus, "steps": total, "warmup": wper * T, "ms_per_step": 1000.0 * dt / total,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (numpy seeded N(0,1))",
         "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
                    "n": cfg["n"], "method": "grbk", "parallelism": f"{T} independent solves"},
@@ -258,6 +286,9 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--ref-threads", type=int, default=16)
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
+    ap.add_argument("--shard", action="store_true",
+                    help="use the row-sharded path even on one GPU (1-rank NCCL communicator)")
+    ap.add_argument("--watchdog-s", type=float, default=1500.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -270,6 +301,10 @@ def main():
         if rank == 0:
             reference_arm(args, cfg)
         return
+
+    import faulthandler
+
+    faulthandler.dump_traceback_later(args.watchdog_s, exit=True)  # never hang the box
 
     import torch
     import torch.distributed as dist
@@ -292,13 +327,31 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    seed = 1000 + rank
+    seed = 1000
     max_iter = 10 ** 9
-    log(f"[rank {rank}] generating {cfg['desc']}")
-    A, B, C, X0, Xs = make_inputs_device(cfg, seed, local)
-    opts = axb.Options(device=local, spectral_max_iter=200000)
+    sharded = world > 1 or args.shard
+    comm = 0
+    if sharded:
+        from paper_2408_05444_b200 import shard
+
+        with stdout_to_stderr():
+            if world == 1:
+                comm = shard.nccl_comm_create(1, shard.nccl_unique_id(), 0, local)
+            else:
+                comm, _, _ = shard.init_comm(local)
+    log(f"[rank {rank}] generating {cfg['desc']} (rows {rank}/{world})")
+    A, B, C, X0, Xs = make_inputs_device(cfg, seed, local, world, rank)
+    sopts = dict(spectral_max_iter=200000)
+
+    def make_solver(A_, B_, C_, X0_, Xs_):
+        if sharded:
+            return shard.sharded_solver(A_, B_, C_, X0_, solver_config(axb, Xs_, max_iter), comm,
+                                        world, rank, device=local, **sopts)
+        return axb.Solver(A_, B_, C_, X0_, solver_config(axb, Xs_, max_iter),
+                          axb.Options(device=local, **sopts))
+
     t0 = time.perf_counter()
-    s = axb.Solver(A, B, C, X0, solver_config(axb, Xs, max_iter), opts)
+    s = make_solver(A, B, C, X0, Xs)
     setup_s = time.perf_counter() - t0
     del A, B, C, X0
     torch.cuda.empty_cache()
@@ -316,7 +369,7 @@ def main():
     tm = s.last_timing()
     ms = allmax(tm["loop_ms"])
     launches = tm["kernel_launches"]
-    value = world * args.steps / (ms / 1000.0)
+    value = args.steps / (ms / 1000.0)  # K global iterations of one system
     log(f"[rank {rank}] {args.steps} iterations in {tm['loop_ms']:.2f} ms -> "
         f"{args.steps / (tm['loop_ms'] / 1000):.1f} it/s")
 
@@ -352,7 +405,7 @@ def main():
     # K iterations, D2H of X), wall clock, max over ranks
     e2e = None
     if not args.no_e2e:
-        Ad, Bd, Cd, X0d, Xsd = make_inputs_device(cfg, seed + 7919, local)
+        Ad, Bd, Cd, X0d, Xsd = make_inputs_device(cfg, seed + 7919, local, world, rank)
         host = {}
         for name, t in (("A", Ad), ("B", Bd), ("C", Cd), ("X0", X0d), ("Xs", Xsd)):
             if t is None:
@@ -366,14 +419,13 @@ def main():
         h2d = sum(v.nbytes for v in host.values() if v is not None)
         barrier()
         t0 = time.perf_counter()
-        s2 = axb.Solver(host["A"], host["B"], host["C"], host["X0"],
-                        solver_config(axb, host["Xs"], max_iter), opts)
+        s2 = make_solver(host["A"], host["B"], host["C"], host["X0"], host["Xs"])
         s2.steps(args.steps, mirror_refresh=True)
         Xout = s2.X()
         torch.cuda.synchronize(local)
         e2e_s = allmax(time.perf_counter() - t0)
         d2h = Xout.nbytes + 8 * args.steps
-        e2e = {"value": world * args.steps / e2e_s, "unit": "iter/s",
+        e2e = {"value": args.steps / e2e_s, "unit": "iter/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
                "seconds": round(e2e_s, 4),
                "what": "Solver(host A,B,C,X0,X*) -> steps(K) -> X() through the C-ABI; "
@@ -383,9 +435,9 @@ def main():
 
     # time-to-tolerance on config 1 (the reference's CPU-runnable case)
     ttt = None
-    if rank == 0 and not args.no_tol:
+    if rank == 0 and world == 1 and not args.no_tol:
         c1 = CONFIGS[1]
-        A1, B1, C1, _, X1 = make_inputs_device(c1, 7, local)
+        A1, B1, C1, _, X1 = make_inputs_device(c1, 7, local, 1, 0, blocks=4)
         s1 = axb.Solver(A1, B1, C1, None, solver_config(axb, X1, 10 ** 6), axb.Options(device=local))
         s1.cfg.max_iter = 10 ** 6
         t0 = time.perf_counter()
@@ -406,12 +458,12 @@ def main():
             "metric": "kaczmarz_iterations_per_sec", "value": round(value, 2), "unit": "iter/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded torch N(0,1) on device)",
             "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
                        "n": cfg["n"], "method": "grbk", "refresh_interval": 1000,
-                       "parallelism": f"{world} independent systems (one per GPU)" if world > 1
-                       else "single GPU",
+                       "parallelism": (f"row-sharded over {world} GPUs (NCCL)" if sharded
+                                       else "single GPU"),
                        "l2": "R is 8*m*n bytes > 126 MB L2: inputs larger than L2, no flush"},
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -422,6 +474,8 @@ def main():
             "setup_s": round(setup_s, 3),
         }
         print(json.dumps(line), flush=True)
+    if sharded:
+        shard.nccl_comm_destroy(comm)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
