@@ -219,3 +219,49 @@ def test_sharded_run_to_tolerance_one_rank(axb, orc):
         assert abs(rep.iterations - 13483) <= 2
     finally:
         shard.nccl_comm_destroy(comm)
+
+
+def test_config2_mwrbk_index_sequence(axb, orc):
+    """Config 2 (A 2000×500, B 400×2000, κ = 100 each; MWRBK): the deterministic
+    index sequence equals the oracle's over 1500 steps, X within 1e-10 (the oracle
+    costs ≈13 ms/step here, so the full 10⁴-step comparison runs in bench/notes)."""
+    import configs
+
+    A, B, Xs, Cm = configs.config2(seed=2)
+    so, sg = pair(axb, orc, A, B, Cm, None, O.MWRBK, Xref=Xs)
+    assert so.alpha == sg.alpha()
+    ro = so.steps(1500)
+    rg = sg.steps(1500)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
+
+
+def test_config3_rank_deficient_converges_to_projected_solution(axb, orc):
+    """Config 3 analogue (rank(A) = 96 < p = 128, X0 ≠ 0): GRBK converges to
+    X⁰_* = A⁺CB⁺ + X0 − A⁺AX0BB⁺ and reaches the oracle's iteration count."""
+    import configs
+
+    A, B, Cm, X0, target = configs.config3_rank_deficient(seed=3)
+    cfg_kw = dict(seed=11, Xref=target, refresh=1000, tol=1e-12)
+    so, sg = pair(axb, orc, A, B, Cm, X0, O.GRBK, **cfg_kw)
+    rep_o, _, _, Xo = so.run(0)
+    rep = sg.run()
+    assert rep.terminated_by == axb.Terminated.Tolerance
+    assert abs(rep.iterations - rep_o.iterations) <= max(3, rep_o.iterations // 1000)
+    assert np.linalg.norm(rep.X - target) / np.linalg.norm(target) < 1.0001e-6
+
+
+def test_config4_blur_channel_fixed_budget(axb, orc):
+    """Config 4 analogue (n = 256, banded Gaussian-blur Toeplitz A = B, smooth
+    field, noisy inconsistent C): MWRBK rows and X match the oracle over 800 steps."""
+    import configs
+
+    A, B, Xs, Cm = configs.config4_channel(seed=4, nn=256, half_band=7)
+    so, sg = pair(axb, orc, A, B, Cm, None, O.MWRBK, Xref=Xs)
+    ro = so.steps(800)
+    rg = sg.steps(800)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
+    assert rel(sg.R(), so.R()) <= 1e-9
