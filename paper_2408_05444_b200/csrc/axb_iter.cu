@@ -916,38 +916,60 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
         sel = P.pack ? (long long)P.pack[P.n + P.p] : st->sel;
     }
     if (warp == kTmaConsumerWarps) {
-        // ---- producer: grab rows dynamically, stream tiles (+ z segment, + G entry) ----
-        if (lane == 0) {
-            int s = 0;
-            unsigned round = 0;
-            for (;;) {
-                const long long row = (long long)atomicAdd(&st->r_next, 1ull);
-                const bool done = row >= m;
-                const long long ntiles = done ? 1 : tpr;
-                const double* src = P.R + row * n;
-                for (long long seg = 0; seg < ntiles; ++seg, src += TW) {
-                    if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-                    stage_row[s] = done ? -1 : row;
-                    if (done) {
-                        mbar_arrive(&full[s]);  // sentinel: no bytes
-                    } else {
-                        const unsigned bytes = (unsigned)(min((long long)TW, n - seg * TW) * 8);
-                        const bool gload = UPDATE && seg == 0 && P.G;
-                        mbar_expect_tx(&full[s], bytes * (zst ? 2u : 1u) + (gload ? 16u : 0u));
+        // ---- producer warp: grab 32 rows at a time, read their Gram coefficients
+        // coalesced, stream only rows with g ≠ 0 (an exactly-zero coefficient
+        // leaves R_l and ‖R_l‖² unchanged — the reference's sparse G iterates
+        // stored entries only, solver.hpp:294-295); unchanged rows still enter
+        // the max/argmax with their standing ratio ----
+        int s = 0;
+        unsigned round = 0;
+        for (;;) {
+            long long base = 0;
+            if (lane == 0) base = (long long)atomicAdd(&st->r_next, 32ull);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base >= m) break;
+            const long long row = base + lane;
+            const bool valid = row < m;
+            double gl = 0.0;
+            bool work = valid;
+            if (UPDATE && valid) {
+                gl = P.G ? __ldg(P.G + sel * m + row) : __ldg(P.g + row);
+                work = gl != 0.0;
+                if (!work) {
+                    const double as = P.a_sq[row];
+                    if (as > 0.0)
+                        maxidx_merge(cmax, carg, __ddiv_rn(__ldcg(P.r_sq + row), as), P.row0 + row);
+                }
+            }
+            unsigned mask = __ballot_sync(0xffffffffu, work);
+            while (mask) {
+                const int l = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const double g_l = __shfl_sync(0xffffffffu, gl, l);
+                if (lane == 0) {
+                    const double* src = P.R + (base + l) * n;
+                    for (int seg = 0; seg < tpr; ++seg, src += TW) {
+                        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+                        stage_row[s] = base + l;
+                        stage_g[s][0] = g_l;
+                        const unsigned bytes = (unsigned)(min((long long)TW, n - (long long)seg * TW) * 8);
+                        mbar_expect_tx(&full[s], bytes * (zst ? 2u : 1u));
                         tma_load_1d(stage + (size_t)s * TW, src, bytes, &full[s]);
-                        if (zst) tma_load_1d(zstage + (size_t)s * TW, P.z + seg * TW, bytes, &full[s]);
-                        if (gload) {  // 16-byte aligned pair holding G[sel, row]
-                            const long long gi = (sel * m + row) & ~1ll;
-                            tma_load_1d(stage_g[s], P.G + gi, 16u, &full[s]);
+                        if (zst)
+                            tma_load_1d(zstage + (size_t)s * TW, P.z + (long long)seg * TW, bytes,
+                                        &full[s]);
+                        if (++s == S) {
+                            s = 0;
+                            ++round;
                         }
                     }
-                    if (++s == S) {
-                        s = 0;
-                        ++round;
-                    }
                 }
-                if (done) break;
             }
+        }
+        if (lane == 0) {  // sentinel: no bytes
+            if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+            stage_row[s] = -1;
+            mbar_arrive(&full[s]);
         }
     } else {
         // ---- 8 consumer warps ----
@@ -958,10 +980,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
             const long long row = stage_row[s];
             if (row < 0) break;
             double f = 0.0;
-            if (UPDATE) {
-                const double gl = P.G ? stage_g[s][(sel * m + row) & 1] : __ldg(P.g + row);
-                f = __dmul_rn(coef, gl);  // solver.hpp:296
-            }
+            if (UPDATE) f = __dmul_rn(coef, stage_g[s][0]);  // solver.hpp:296
             double acc = 0.0;
             long long c0 = 0;
             for (int seg = 0; seg < tpr; ++seg, c0 += TW) {
