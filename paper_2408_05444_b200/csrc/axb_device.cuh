@@ -144,6 +144,10 @@ void launch_coldot(const double* M, long long rows, long long cols, const double
 void launch_power_step(const double* v_in, const double* w, double* v_out, long long dim,
                        double* out2, cudaStream_t s);
 void launch_fill(double* p, long long n, double v, cudaStream_t s);
+void launch_power_step2(double* v, const double* w, long long dim, double* ps, double tol,
+                        double max_iter, cudaStream_t s);
+void launch_transpose(const double* in, long long rows, long long cols, double* out,
+                      cudaStream_t s);
 void launch_ctrl(DevState* st, unsigned long long k0, unsigned long long k_limit, int fin_mode,
                  int run_mode, int reset_status, cudaStream_t s);
 void launch_set_sel(DevState* st, long long sel, double coef, cudaStream_t s);

@@ -1450,6 +1450,62 @@ __global__ void __launch_bounds__(1024) k_power_step(const double* v, const doub
         for (long long i = threadIdx.x; i < dim; i += blockDim.x) v_out[i] = w[i] / wn;
 }
 
+// Power-iteration step on a small Gram M (w = M·v already formed), with the
+// reference's stop test on the device (decomp.hpp:227-238):
+//   rayleigh = v·w, wn = ‖w‖, v ← w / wn; stop when it > 0 and
+//   |rayleigh − λ| ≤ ½·tol·|rayleigh|  →  ‖B‖₂ = √rayleigh.
+// ps: [0] λ, [1] result, [2] iteration, [3] state (0 running, 1 done, 2 cap hit)
+__global__ void __launch_bounds__(1024) k_power_step2(double* v, const double* w, long long dim,
+                                                      double* ps, double tol, double max_iter) {
+    __shared__ double red[32];
+    __shared__ int stop;
+    if (ps[3] != 0.0) return;
+    double a = 0.0, b = 0.0;
+    for (long long i = threadIdx.x; i < dim; i += blockDim.x) {
+        a += v[i] * w[i];
+        b += w[i] * w[i];
+    }
+    a = block_sum(a, red);
+    b = block_sum(b, red);
+    const double wn = sqrt(b);
+    if (threadIdx.x == 0) {
+        stop = 0;
+        if (wn == 0.0) {
+            ps[1] = 0.0;
+            ps[3] = 1.0;
+            stop = 1;
+        } else {
+            const double it = ps[2];
+            if (it > 0.0 && fabs(a - ps[0]) <= 0.5 * tol * fabs(a)) {
+                ps[1] = sqrt(a);
+                ps[3] = 1.0;
+            } else {
+                ps[0] = a;
+                if (it + 1.0 >= max_iter) ps[3] = 2.0;
+            }
+            ps[2] = it + 1.0;
+        }
+    }
+    __syncthreads();
+    if (stop) return;
+    for (long long i = threadIdx.x; i < dim; i += blockDim.x) v[i] = w[i] / wn;
+}
+
+// out (cols × rows) = inᵀ, 32×32 smem tiles
+__global__ void k_transpose(const double* in, long long rows, long long cols, double* out) {
+    __shared__ double t[32][33];
+    const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const long long r = r0 + j, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) t[j][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const long long c = c0 + j, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = t[threadIdx.x][j];
+    }
+}
+
 __global__ void k_fill(double* p, long long n, double v) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
@@ -1651,6 +1707,17 @@ void launch_sel1(const Params& P, cudaStream_t s, bool update) {
 }
 
 void launch_sel2(const Params& P, cudaStream_t s) { k_sel2<<<1, kThreads, 0, s>>>(P); }
+
+void launch_power_step2(double* v, const double* w, long long dim, double* ps, double tol,
+                        double max_iter, cudaStream_t s) {
+    k_power_step2<<<1, 1024, 0, s>>>(v, w, dim, ps, tol, max_iter);
+}
+
+void launch_transpose(const double* in, long long rows, long long cols, double* out,
+                      cudaStream_t s) {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out);
+}
 
 void launch_fill(double* p, long long n, double v, cudaStream_t s) {
     int grid = (int)std::min<long long>(1184, (n + 255) / 256);

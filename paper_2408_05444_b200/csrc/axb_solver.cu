@@ -390,18 +390,43 @@ struct axb_solver {
         X.alloc(p_loc * world * q, "X");
         if (p_loc * world > p)
             ck(cudaMemsetAsync(X.p, 0, sizeof(double) * p_loc * world * q, stream), "X pad");
-        ck(cudaMemcpyAsync(A.p, A_in, sizeof(double) * m * p, kind, stream), "copy A");
-        ck(cudaMemcpyAsync(B.p, B_in, sizeof(double) * q * n, kind, stream), "copy B");
-        ck(cudaMemcpyAsync(C.p, C_in, sizeof(double) * m * n, kind, stream), "copy C");
+        // inputs arrive on a copy stream in the order they are needed; the
+        // compute stream waits per input, so ‖B‖₂ (and G) overlap the C copy
+        cudaStream_t cs = nullptr;
+        ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
+        cudaEvent_t evA, evB, evRest;
+        ck(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&evRest, cudaEventDisableTiming), "event");
+        struct Guard {
+            cudaStream_t s;
+            cudaEvent_t a, b, c;
+            ~Guard() {
+                cudaStreamSynchronize(s);
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+                cudaEventDestroy(c);
+                cudaStreamDestroy(s);
+            }
+        } guard{cs, evA, evB, evRest};
+        ck(cudaEventRecord(ev0, stream), "event");  // X pad before the X0 copy
+        ck(cudaStreamWaitEvent(cs, ev0, 0), "wait");
+        ck(cudaMemcpyAsync(A.p, A_in, sizeof(double) * m * p, kind, cs), "copy A");
+        ck(cudaEventRecord(evA, cs), "event");
+        ck(cudaMemcpyAsync(B.p, B_in, sizeof(double) * q * n, kind, cs), "copy B");
+        ck(cudaEventRecord(evB, cs), "event");
+        ck(cudaMemcpyAsync(C.p, C_in, sizeof(double) * m * n, kind, cs), "copy C");
         if (X0_in)
-            ck(cudaMemcpyAsync(X.p, X0_in, sizeof(double) * p * q, kind, stream), "copy X0");
+            ck(cudaMemcpyAsync(X.p, X0_in, sizeof(double) * p * q, kind, cs), "copy X0");
         else
-            ck(cudaMemsetAsync(X.p, 0, sizeof(double) * p * q, stream), "zero X0");
+            ck(cudaMemsetAsync(X.p, 0, sizeof(double) * p * q, cs), "zero X0");
         if (cfg.reference) {
             Xref.alloc(p * q, "Xref");
-            ck(cudaMemcpyAsync(Xref.p, cfg.reference, sizeof(double) * p * q, kind, stream),
+            ck(cudaMemcpyAsync(Xref.p, cfg.reference, sizeof(double) * p * q, kind, cs),
                "copy reference");
         }
+        ck(cudaEventRecord(evRest, cs), "event");
+        ck(cudaStreamWaitEvent(stream, evA, 0), "wait A");
         a_sq.alloc(m, "a_sq");
         rbk_cum.alloc(m_g, "rbk_cum");
         r_sq.alloc(m, "r_sq");
@@ -437,6 +462,7 @@ struct axb_solver {
         if (a_fro_sq == 0.0) fail(AXB_DOMAIN_ERROR, "solve: A is the zero matrix");
 
         // b_spec_ = spectral_norm(B); resolve_alpha() (solver.hpp:168-169, :439-456)
+        ck(cudaStreamWaitEvent(stream, evB, 0), "wait B");
         if (opt.alpha_override > 0.0) {
             alpha = opt.alpha_override;
             b_spec = 0.0;
@@ -503,6 +529,7 @@ struct axb_solver {
         }
 
         // r_ = C − (A·X0)·B (solver.hpp:173)
+        ck(cudaStreamWaitEvent(stream, evRest, 0), "wait C, X0, X_ref");
         if (X0_in) {
             exact_residual_into(R.p, nullptr, nullptr, true);
         } else {
@@ -612,8 +639,53 @@ struct axb_solver {
         pull_state();
     }
 
+    // ‖B‖₂ on the device: the reference's power iteration (decomp.hpp:207-239: same
+    // start vector, same stop test) applied to the small Gram M = B·Bᵀ (q ≤ n) or
+    // BᵀB, formed once by the DMMA GEMM and then L2-resident; the stop test runs
+    // on the device and the host looks every 32 iterations.
     double spectral_norm_device(double tol, size_t max_iter) {
         if (reduce_sumsq(B.p, q * n) == 0.0) fail(AXB_DOMAIN_ERROR, "spectral_norm: zero matrix");
+        const bool use_mtm = n <= q;
+        const size_t dim = use_mtm ? n : q;
+        if (8.0 * (double)dim * (double)dim > 16e9) return spectral_norm_device_2pass(tol, max_iter);
+        DevBuf<double> M, Bt, v, w, ps;
+        M.alloc(dim * dim, "power Gram");
+        GemmArgs ga{};
+        ga.M = dim; ga.N = dim; ga.store = 1; ga.b_trans = 1;
+        if (use_mtm) {  // M = BᵀB = (Bᵀ)(Bᵀ)ᵀ
+            Bt.alloc(q * n, "B transposed");
+            launch_transpose(B.p, (long long)q, (long long)n, Bt.p, stream);
+            ga.K = q; ga.A = Bt.p; ga.lda = q; ga.B = Bt.p; ga.ldb = q;
+        } else {        // M = B·Bᵀ
+            ga.K = n; ga.A = B.p; ga.lda = n; ga.B = B.p; ga.ldb = n;
+        }
+        ga.D = M.p; ga.ldd = dim;
+        launch_gemm(ga, stream);
+        std::vector<double> v0 = power_start(dim);
+        v.alloc(dim, "power v");
+        w.alloc(dim, "power w");
+        ps.alloc(4, "power state");
+        ck(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * dim, cudaMemcpyHostToDevice, stream),
+           "v0");
+        ck(cudaMemsetAsync(ps.p, 0, sizeof(double) * 4, stream), "power state");
+        double h[4] = {0, 0, 0, 0};
+        for (size_t done = 0; done < max_iter; done += 32) {
+            for (int i = 0; i < 32; ++i) {
+                launch_rowdot(M.p, (long long)dim, (long long)dim, v.p, w.p, stream);
+                launch_power_step2(v.p, w.p, (long long)dim, ps.p, tol, (double)max_iter, stream);
+            }
+            ck(cudaMemcpyAsync(h, ps.p, sizeof h, cudaMemcpyDeviceToHost, stream), "power");
+            sync("power");
+            if (h[3] != 0.0) break;
+        }
+        if (h[3] == 1.0) return h[1];
+        AxbError e{AXB_CONVERGENCE_ERROR, "spectral_norm: power iteration did not converge"};
+        e.val = std::sqrt(std::abs(h[0]));
+        throw e;
+    }
+
+    // two GEMV passes over B per iteration (for a Gram too large to form)
+    double spectral_norm_device_2pass(double tol, size_t max_iter) {
         const bool use_mtm = n <= q;
         const size_t dim = use_mtm ? n : q, other = use_mtm ? q : n;
         std::vector<double> v0 = power_start(dim);
