@@ -124,6 +124,7 @@ struct Params {
     int method, stop_kind, tie_guard, vec2;
     // launch geometry
     int r_grid, r_rows_per_cta, r_chunk, r_tma, r_stages, r_zstage;
+    int persist, persist_grid;   // small systems: one cooperative kernel per batch
     int yg_grid;
     int z_nslab, z_nj, z_jrows, x_ctas;
 };
@@ -159,6 +160,8 @@ void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* tot
 // sharded selection (between the record / mass allgathers and the row allreduce)
 void launch_sel1(const Params& P, cudaStream_t s, bool update);
 void launch_sel2(const Params& P, cudaStream_t s);
+// persistent cooperative batch kernel for small systems; returns a cudaError_t
+int launch_persist(const Params& P, cudaStream_t s);
 
 // ---- DMMA GEMM (axb_gemm.cu) ----
 // D = (Cin ? Cin − A·op(B) : A·op(B)); op(B) = B (K×N) or Bᵀ (B is N×K) when b_trans.

@@ -25,6 +25,8 @@
 #include <climits>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "axb_device.cuh"
 
 namespace axb_dev {
@@ -1275,6 +1277,257 @@ __global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
     }
 }
 
+// ------------------------------------------------------------------------
+// Small systems (everything L2-resident, per-iteration work ≪ launch latency):
+// ONE persistent cooperative kernel runs a whole batch.  Per iteration:
+//   y (+g) phase ─grid.sync─ z + X phase ─grid.sync─ R update + records ─grid.sync─
+//   every CTA reduces the records (fixed order) and selects the next row in its
+//   own shared-memory copy of DevState (same xoshiro stream, same inputs →
+//   identical results), so no fourth barrier is needed; CTA 0 writes the trace
+//   and, at the end, the state.
+constexpr int kPersistThreads = 256;
+
+__global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double pscratch[];  // selection scratch: ⌈m/32⌉ group sums
+    __shared__ DevState lst;
+    __shared__ SelShared sh;
+    __shared__ double red[32];
+    __shared__ long long redi[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long m = P.m, n = P.n, p = P.p, q = P.q;
+    const long long gw = (long long)blockIdx.x * kWarps + warp;  // global warp
+    const long long nw = (long long)gridDim.x * kWarps;
+    if (tid == 0) lst = *P.st;
+    __syncthreads();
+    for (;;) {
+        if (lst.status != ST_RUN || lst.k >= lst.k_limit) break;
+        if (!lst.sel_valid) {  // K3 (every CTA, identically)
+            long long row = 0;
+            if (tid == 0) sh.err = 0;
+            __syncthreads();
+            const int err = select_rows(P, &lst, P.method, P.theta, &row, sh, pscratch,
+                                        (m + 31) / 32);
+            __syncthreads();
+            if (tid == 0) {
+                if (err) {
+                    lst.status = ST_ERROR;
+                    lst.err_code = err;
+                    lst.err_k = lst.k;
+                } else {
+                    lst.sel = row;
+                    lst.coef = __ddiv_rn(P.alpha, P.a_sq[row]);
+                    lst.sel_valid = 1;
+                }
+            }
+            __syncthreads();
+            if (lst.status != ST_RUN) break;
+        }
+        const long long sel = lst.sel;
+        const double coef = lst.coef;
+        const double* Ri = P.R + sel * n;
+        const double* Ai = P.A + sel * p;
+        // ---- y = B·R_iᵀ (+ g = A·A_iᵀ) ----
+        const long long items = q + (P.G ? 0 : m);
+        for (long long it = gw; it < items; it += nw) {
+            if (it < q) {
+                const double a = warp_dot(P.B + it * n, Ri, n, lane, (n & 1) == 0);
+                if (lane == 0) P.y[it] = a;
+            } else {
+                const double a = warp_dot(P.A + (it - q) * p, Ai, p, lane, (p & 1) == 0);
+                if (lane == 0) P.g[it - q] = a;
+            }
+        }
+        grid.sync();
+        // ---- z = yᵀ·B, stage 1: (column slab × row chunk) partials; X update ----
+        {
+            const int items = P.z_nslab * P.z_nj;
+            for (int itm = blockIdx.x; itm < items; itm += gridDim.x) {
+                const int slab = itm % P.z_nslab, jc = itm / P.z_nslab;
+                const long long j0 = (long long)jc * P.z_jrows, j1 = min(q, j0 + P.z_jrows);
+                const long long c = (long long)slab * (2 * kPersistThreads) + 2 * tid;
+                double a0 = 0.0, a1 = 0.0;
+                if (c < n) {
+#pragma unroll 8
+                    for (long long j = j0; j < j1; ++j) {
+                        const double yj = __ldcg(P.y + j);
+                        a0 += yj * __ldg(P.B + j * n + c);
+                        if (c + 1 < n) a1 += yj * __ldg(P.B + j * n + c + 1);
+                    }
+                    double* zp = P.zpart + (long long)jc * n;
+                    zp[c] = a0;
+                    if (c + 1 < n) zp[c + 1] = a1;
+                }
+            }
+        }
+        double xacc = 0.0;
+        for (long long t = gw; t < p; t += nw) {
+            const double f = __dmul_rn(coef, Ai[t]);
+            double* xr = P.X + t * q;
+            const double* rr = P.Xref ? P.Xref + t * q : nullptr;
+            for (long long k0 = lane; k0 < q; k0 += 32 * 4) {
+                double xv[4], yv[4], rv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const long long k = k0 + 32 * u;
+                    if (k < q) {
+                        xv[u] = xr[k];
+                        yv[u] = __ldcg(P.y + k);
+                        rv[u] = rr ? rr[k] : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const long long k = k0 + 32 * u;
+                    if (k < q) {
+                        const double x1 = __dadd_rn(xv[u], __dmul_rn(f, yv[u]));
+                        xr[k] = x1;
+                        if (rr) {
+                            const double d1 = x1 - rv[u];
+                            xacc += d1 * d1;
+                        }
+                    }
+                }
+            }
+        }
+        xacc = block_sum(xacc, red);
+        if (tid == 0) P.xpart[blockIdx.x] = xacc;
+        grid.sync();
+        // ---- z stage 2: fixed-order combine of the row-chunk partials ----
+        for (long long c = (long long)blockIdx.x * kPersistThreads + tid; c < n;
+             c += (long long)gridDim.x * kPersistThreads) {
+            double a = 0.0;
+            for (int k = 0; k < P.z_nj; ++k) a += __ldcg(P.zpart + (long long)k * n + c);
+            P.z[c] = a;
+        }
+        grid.sync();
+        // ---- R update + row norms (warp per row, static mapping) ----
+        double wsum = 0.0, wmax = -INFINITY;
+        long long warg = LLONG_MAX;
+        for (long long l = gw; l < m; l += nw) {
+            const double gl = P.G ? __ldcg(P.G + sel * m + l) : __ldcg(P.g + l);
+            double rs;
+            if (gl == 0.0) {  // R_l unchanged (sparse-G semantics, solver.hpp:294-295)
+                rs = __ldcg(P.r_sq + l);
+            } else {
+                const double f = __dmul_rn(coef, gl);
+                double* row = P.R + l * n;
+                double acc = 0.0;
+                for (long long k0 = lane; k0 < n; k0 += 32 * 4) {
+                    double rv[4], zv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const long long k = k0 + 32 * u;
+                        if (k < n) {
+                            rv[u] = row[k];
+                            zv[u] = __ldcg(P.z + k);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const long long k = k0 + 32 * u;
+                        if (k < n) {
+                            const double r = __dsub_rn(rv[u], __dmul_rn(f, zv[u]));
+                            row[k] = r;
+                            acc += r * r;
+                        }
+                    }
+                }
+                rs = warp_sum(acc);
+                if (lane == 0) P.r_sq[l] = rs;
+            }
+            wsum += rs;
+            const double as = P.a_sq[l];
+            if (as > 0.0) maxidx_merge(wmax, warg, __ddiv_rn(rs, as), l);
+        }
+        // per-CTA record: warp partials combined in warp order (fixed mapping)
+        __syncthreads();
+        if (lane == 0) {
+            red[warp] = wsum;
+            sh.scan[warp] = wmax;
+            redi[warp] = warg;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, mx = -INFINITY;
+            long long ax = LLONG_MAX;
+            for (int w = 0; w < kWarps; ++w) {
+                a += red[w];
+                maxidx_merge(mx, ax, sh.scan[w], redi[w]);
+            }
+            P.rrec[blockIdx.x] = RowRecord{a, mx, ax, 0.0};
+        }
+        grid.sync();
+        // ---- every CTA: reduce the records + the ‖X−X_ref‖² partials (block-
+        // parallel loads, fixed-order trees → identical in every CTA), finalize ----
+        {
+            double ps = 0.0, pe = 0.0, pm = -INFINITY;
+            long long pa = LLONG_MAX;
+            for (int b = tid; b < (int)gridDim.x; b += kPersistThreads) {
+                const double* rp = reinterpret_cast<const double*>(P.rrec + b);
+                ps += __ldcg(rp);
+                maxidx_merge(pm, pa, __ldcg(rp + 1), __ldcg(reinterpret_cast<const long long*>(rp + 2)));
+                pe += __ldcg(P.xpart + b);
+            }
+            ps = block_sum(ps, red);
+            pe = block_sum(pe, red);
+            block_maxidx(pm, pa, sh.redv, sh.redi);
+            if (tid == 0) {
+                sh.scan[0] = ps;
+                sh.scan[1] = pe;
+                sh.scan[2] = pm;
+                sh.cand = pa;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            const double s = sh.scan[0], e = sh.scan[1], mx = sh.scan[2];
+            const long long ax = sh.cand;
+            lst.r_fro_sq = s;
+            lst.max_ratio = mx;
+            lst.argmax = ax;
+            lst.err_sq = e;
+            lst.sel_valid = 0;
+            const double cf = P.c_fro > 0.0 ? P.c_fro : 1.0;
+            const double rel = sqrt(s > 0.0 ? s : 0.0) / cf;
+            if (!isfinite(s)) {  // solver.hpp:306-307
+                lst.status = ST_ERROR;
+                lst.err_code = 4;
+                lst.err_k = lst.k;
+                lst.err_val = sqrt(fabs(s));
+            } else {
+                const unsigned long long k = lst.k;
+                const double metric = P.stop_kind == 0 ? e / P.ref_sq : rel;
+                const unsigned long long slot = k - lst.k0;
+                if (blockIdx.x == 0 && slot < P.trace_cap) {
+                    P.trace_row[slot] = sel;
+                    P.trace_metric[slot] = metric;
+                    P.trace_rel[slot] = rel;
+                }
+                lst.k = k + 1;
+                lst.metric = metric;
+                if (lst.run_mode && metric <= P.tol) lst.status = ST_PAUSE;
+                else if (lst.run_mode && !(s > 0.0)) lst.status = ST_ZERO;
+            }
+        }
+        __syncthreads();
+        // no barrier needed before the next y phase: it only reads R/B (last
+        // written before the grid.sync above) and writes y, which nobody reads
+        // until after the next grid.sync
+    }
+    if (blockIdx.x == 0 && tid == 0) *P.st = lst;
+}
+
+int persist_grid(const Params& P) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = sizeof(double) * (size_t)((P.m + 31) / 32);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_persist, kPersistThreads, smem);
+    return std::max(1, sms * std::min(per, 1));
+}
+
 // K3 standalone: (re)select with the configured rule (consume=0: speculative,
 // snapshot kept) or run a public select_*(θ) that consumes the stream (consume=1).
 __global__ void __launch_bounds__(kThreads) k_select(Params P, int method, double theta,
@@ -1717,6 +1970,15 @@ void launch_transpose(const double* in, long long rows, long long cols, double* 
                       cudaStream_t s) {
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
     k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out);
+}
+
+int launch_persist(const Params& P, cudaStream_t s) {
+    const int grid = std::min(P.persist_grid, persist_grid(P));
+    const size_t smem = sizeof(double) * (size_t)((P.m + 31) / 32);
+    Params Pc = P;
+    void* args[] = {&Pc};
+    return (int)cudaLaunchCooperativeKernel((const void*)k_persist, dim3((unsigned)grid),
+                                            dim3(kPersistThreads), args, smem, s);
 }
 
 void launch_fill(double* p, long long n, double v, cudaStream_t s) {

@@ -616,6 +616,18 @@ struct axb_solver {
         P.method = cfg.method;
         P.stop_kind = cfg.stop_kind;
         P.tie_guard = (opt.tie_guard && !sharded) ? 1 : 0;  // exact replay needs all rows
+        // small systems (per-iteration working set L2-resident): one persistent
+        // cooperative kernel per batch instead of a graph of 3 kernels/iteration
+        {
+            const double ws = 8.0 * ((double)m * n + (double)q * n + 2.0 * p * q + (double)m * p);
+            const int force = env_int("AXB_PERSIST", -1);
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
+            P.persist = !sharded && (force == 1 || (force < 0 && ws <= 64e6));
+            // grid: enough SMs for the L2 bandwidth of R, few enough for cheap grid syncs
+            const int want = (int)std::min<double>(sms, std::max(64.0, (double)m * n / 16384.0));
+            P.persist_grid = env_int("AXB_PERSIST_GRID", want);
+        }
         P.vec2 = (n % 2) == 0;
 
         // DevState: RngStream(cfg.seed) (rng.hpp:20-25), k = 0
@@ -824,8 +836,17 @@ struct axb_solver {
     uint64_t batch(uint64_t nb, int run_mode) {
         launch_ctrl(st.p, k, k + nb, FIN_ITERATION, run_mode, 0, stream);
         ++kernel_launches;
-        ensure_selection();
-        if (profiling) {
+        if (P.persist && !profiling) {
+            // the kernel selects at the top of each iteration itself
+            const int e = launch_persist(P, stream);
+            if (e != 0) ck(static_cast<cudaError_t>(e), "persistent kernel launch");
+            ++kernel_launches;
+        } else {
+            ensure_selection();
+        }
+        if (P.persist && !profiling) {
+            // nothing more to enqueue
+        } else if (profiling) {
             if (prof_ev.size() < 2 * nb) {
                 size_t have = prof_ev.size();
                 prof_ev.resize(2 * nb);
