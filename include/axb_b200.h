@@ -138,6 +138,29 @@ int axb_solver_last_error_info(const axb_solver* s, uint64_t* iteration, double*
 /* message for failures of axb_solver_create (handle-less), thread-local */
 const char* axb_last_create_error(void);
 
+/* Storage-agnostic matrix descriptor: the reference's axb::Matrix variant
+ * (matrix.hpp:178, DenseMatrix or CSR SparseMatrix :94-175).  kind 0 = dense
+ * row-major `dense`; kind 1 = CSR (row_ptr[rows+1], col_idx[nnz] ascending per
+ * row, values[nnz]), validated like SparseMatrix::validate.  Host pointers. */
+typedef struct {
+    int32_t kind;
+    int32_t _pad;
+    uint64_t rows, cols, nnz;
+    const double* dense;
+    const uint64_t* row_ptr;
+    const uint64_t* col_idx;
+    const double* values;
+} axb_matrix;
+
+/* solve(const Matrix& A, const Matrix& B, …) dispatch — solver.hpp:518-526.
+ * CSR operands are expanded on the device path: every reference loop over stored
+ * entries (RowView, gram_mmt, matmul's zero skip) adds exact zeros in the dense
+ * form, so results are unchanged, and K2 skips the rows whose Gram coefficient
+ * is exactly zero (the sparse-G iteration of solver.hpp:294-295). */
+int axb_solver_create_ex(const axb_matrix* A, const axb_matrix* B, const double* C,
+                         const double* X0, const axb_config* cfg, const axb_options* opt,
+                         axb_solver** out);
+
 /* Solver::step() — solver.hpp:321-333.  One iteration; returns the row. */
 int axb_solver_step(axb_solver* s, uint64_t* row);
 /* k consecutive step() calls (the acceptance.cpp:128-141 driver loop, batched

@@ -75,6 +75,22 @@ class AxbOptions(C.Structure):
     ]
 
 
+class AxbMatrix(C.Structure):
+    """axb_matrix — the reference's axb::Matrix variant (dense or CSR)."""
+
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("_pad", C.c_int32),
+        ("rows", C.c_uint64),
+        ("cols", C.c_uint64),
+        ("nnz", C.c_uint64),
+        ("dense", C.c_void_p),
+        ("row_ptr", C.c_void_p),
+        ("col_idx", C.c_void_p),
+        ("values", C.c_void_p),
+    ]
+
+
 # (name, restype, argtypes) for every symbol include/axb_b200.h declares
 _H = C.c_void_p
 SIGNATURES = [
@@ -88,6 +104,9 @@ SIGNATURES = [
     ("axb_solver_create", C.c_int,
      [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
       C.c_void_p, C.POINTER(AxbConfig), C.POINTER(AxbOptions), C.POINTER(_H)]),
+    ("axb_solver_create_ex", C.c_int,
+     [C.POINTER(AxbMatrix), C.POINTER(AxbMatrix), C.c_void_p, C.c_void_p, C.POINTER(AxbConfig),
+      C.POINTER(AxbOptions), C.POINTER(_H)]),
     ("axb_solver_destroy", None, [_H]),
     ("axb_solver_last_error", C.c_char_p, [_H]),
     ("axb_last_create_error", C.c_char_p, []),

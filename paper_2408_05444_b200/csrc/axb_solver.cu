@@ -1278,6 +1278,62 @@ int axb_solver_create(const double* A, uint64_t m, uint64_t p, const double* B, 
     return AXB_OK;
 }
 
+namespace {
+// SparseMatrix::validate (matrix.hpp:94-175) + expansion to row-major dense
+int expand(const axb_matrix* M, std::vector<double>& out, const char* name) {
+    if (M->kind == 0) return AXB_OK;
+    if (M->kind != 1) {
+        g_create_err = std::string(name) + ": unknown matrix kind";
+        return AXB_CONFIG_ERROR;
+    }
+    const uint64_t r = M->rows, c = M->cols;
+    if (!M->row_ptr || (M->nnz && (!M->col_idx || !M->values)) || M->row_ptr[0] != 0 ||
+        M->row_ptr[r] != M->nnz) {
+        g_create_err = std::string(name) + ": malformed CSR row pointer";
+        return AXB_SHAPE_ERROR;
+    }
+    out.assign(r * c, 0.0);
+    for (uint64_t i = 0; i < r; ++i) {
+        if (M->row_ptr[i + 1] < M->row_ptr[i]) {
+            g_create_err = std::string(name) + ": CSR row pointer decreases";
+            return AXB_SHAPE_ERROR;
+        }
+        for (uint64_t t = M->row_ptr[i]; t < M->row_ptr[i + 1]; ++t) {
+            const uint64_t j = M->col_idx[t];
+            const double v = M->values[t];
+            if (j >= c || (t > M->row_ptr[i] && j <= M->col_idx[t - 1])) {
+                g_create_err = std::string(name) + ": CSR column indices must ascend within a row";
+                return AXB_SHAPE_ERROR;
+            }
+            if (!std::isfinite(v) || v == 0.0) {
+                g_create_err = std::string(name) + ": CSR values must be finite and nonzero";
+                return AXB_DOMAIN_ERROR;
+            }
+            out[i * c + j] = v;
+        }
+    }
+    return AXB_OK;
+}
+}  // namespace
+
+int axb_solver_create_ex(const axb_matrix* A, const axb_matrix* B, const double* C,
+                         const double* X0, const axb_config* cfg, const axb_options* opt,
+                         axb_solver** out) {
+    *out = nullptr;
+    if (opt && opt->inputs_on_device && (A->kind == 1 || B->kind == 1)) {
+        g_create_err = "CSR operands are host arrays";
+        return AXB_CONFIG_ERROR;
+    }
+    std::vector<double> Ad, Bd;
+    int st = expand(A, Ad, "A");
+    if (st) return st;
+    st = expand(B, Bd, "B");
+    if (st) return st;
+    return axb_solver_create(A->kind == 1 ? Ad.data() : A->dense, A->rows, A->cols,
+                             B->kind == 1 ? Bd.data() : B->dense, B->rows, B->cols, C, X0, cfg,
+                             opt, out);
+}
+
 void axb_solver_destroy(axb_solver* s) { delete s; }
 const char* axb_solver_last_error(const axb_solver* s) { return s->err.c_str(); }
 

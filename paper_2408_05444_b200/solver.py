@@ -204,7 +204,13 @@ def _contig(iface):
     return True
 
 
+def _is_csr(a):
+    return hasattr(a, "indptr") and hasattr(a, "indices") and hasattr(a, "format")
+
+
 def _shape(a):
+    if _is_csr(a):
+        return tuple(a.shape)
     if hasattr(a, "__cuda_array_interface__"):
         return tuple(a.__cuda_array_interface__["shape"])
     return tuple(np.shape(a))
@@ -272,8 +278,33 @@ class Solver:
         o.m_global = opts.m_global
         o.row_offset = opts.row_offset
         h = C.c_void_p()
-        st = lib.axb_solver_create(ptr(A), m, p, ptr(B), q, n, ptr(C_), ptr(X0), C.byref(c),
-                                   C.byref(o), C.byref(h))
+        if _is_csr(A) or _is_csr(B):
+            if on_dev:
+                raise ConfigError("CSR operands are host arrays")
+
+            def desc(M):
+                d = _lib.AxbMatrix()
+                d.rows, d.cols = M.shape
+                if _is_csr(M):
+                    M = M.tocsr()
+                    M.sort_indices()
+                    rp = np.ascontiguousarray(M.indptr, dtype=np.uint64)
+                    ci = np.ascontiguousarray(M.indices, dtype=np.uint64)
+                    vv = np.ascontiguousarray(M.data, dtype=np.float64)
+                    keep.extend([rp, ci, vv])
+                    d.kind, d.nnz = 1, vv.size
+                    d.row_ptr, d.col_idx, d.values = rp.ctypes.data, ci.ctypes.data, vv.ctypes.data
+                else:
+                    d.kind = 0
+                    d.dense = ptr(M)
+                return d
+
+            dA, dB = desc(A), desc(B)
+            st = lib.axb_solver_create_ex(C.byref(dA), C.byref(dB), ptr(C_), ptr(X0), C.byref(c),
+                                          C.byref(o), C.byref(h))
+        else:
+            st = lib.axb_solver_create(ptr(A), m, p, ptr(B), q, n, ptr(C_), ptr(X0), C.byref(c),
+                                       C.byref(o), C.byref(h))
         if st:
             raise_status(st, lib.axb_last_create_error().decode())
         self._h = h

@@ -134,3 +134,19 @@ def test_cpp_dropin_header_compiles_and_fails_loudly_without_device(tmp_path):
         pytest.skip("device present: covered by the GPU test")
     out = subprocess.run([exe], capture_output=True, text=True)
     assert out.returncode == 3 and "CudaError" in out.stdout, out.stdout
+
+
+def test_csr_validation_errors_before_any_device_work():
+    """SparseMatrix::validate (matrix.hpp:94-175) equivalents are host-side."""
+    import scipy.sparse as sp
+
+    import paper_2408_05444_b200 as axb
+
+    bad = sp.csr_matrix(np.eye(3))
+    bad.data[1] = 0.0  # stored zero: the reference rejects it
+    with pytest.raises(axb.DomainError):
+        axb.Solver(bad, np.eye(3), np.eye(3), None, axb.SolveConfig())
+    nanm = sp.csr_matrix(np.eye(3))
+    nanm.data[0] = np.nan
+    with pytest.raises(axb.DomainError):
+        axb.Solver(nanm, np.eye(3), np.eye(3), None, axb.SolveConfig())

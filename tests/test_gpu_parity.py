@@ -265,3 +265,25 @@ def test_config4_blur_channel_fixed_budget(axb, orc):
     assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
     assert rel(sg.X(), so.X()) <= RTOL_X
     assert rel(sg.R(), so.R()) <= 1e-9
+
+
+@pytest.mark.parametrize("tag", [O.MWRBK, O.GRBK])
+def test_csr_operands_match_dense_and_oracle(axb, orc, tag):
+    """solve(const Matrix&…) with CSR A and B (test_solver.cpp:546-561): the CSR
+    run equals the dense run bit for bit and the oracle's rows / X."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(6501)
+    Ad = np.where(rng.random((300, 40)) < 0.4, rng.uniform(-1, 1, (300, 40)), 0.0)
+    Bd = np.where(rng.random((30, 120)) < 0.6, rng.uniform(-1, 1, (30, 120)), 0.0)
+    Xs = rng.standard_normal((40, 30))
+    Cm = Ad @ Xs @ Bd
+    so, sg = pair(axb, orc, Ad, Bd, Cm, None, tag, seed=3, Xref=Xs)
+    cfg = axb.SolveConfig(method=axb_method(axb, tag), stop=axb.StopRule.solution_rrn(0.0, Xs),
+                          seed=3, refresh_interval=0)
+    sc = axb.Solver(sp.csr_matrix(Ad), sp.csr_matrix(Bd), Cm, None, cfg)
+    rd, rc, ro = sg.steps(1500), sc.steps(1500), so.steps(1500)
+    np.testing.assert_array_equal(rc, rd)
+    np.testing.assert_array_equal(sc.X(), sg.X())
+    np.testing.assert_array_equal(rd, ro)
+    assert rel(sc.X(), so.X()) <= RTOL_X
