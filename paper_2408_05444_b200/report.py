@@ -1,0 +1,79 @@
+"""Report and trace formats of the reference, for drop-in CLIs.
+
+Byte-compatible restatements of report.hpp:
+  trace_to_csv          report.hpp:55-61   (RFC-4180, CRLF, %.17g, inf/-inf)
+  solve_report_to_json  report.hpp:102-117 (+ "stop"/"tol" as axbsolve.cpp:208-209)
+  dumps_json            nlohmann::json::dump(2): keys sorted, 2-space indent, "\\n"
+validated by schemas/solve_report.schema.json's required keys and enums.
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+from typing import Iterable, Optional
+
+from .solver import SolveReport, Terminated, TracePoint
+
+TOOL_VERSION = "1.0.0"  # report.hpp:18
+
+
+def _escape(field: str) -> str:  # report.hpp:25-34
+    if not any(ch in field for ch in ',"\r\n'):
+        return field
+    return '"' + field.replace('"', '""') + '"'
+
+
+def _num(v: float) -> str:  # report.hpp:36-41
+    if math.isinf(v):
+        return "inf" if v > 0 else "-inf"
+    return "%.17g" % v
+
+
+def _row(fields: Iterable[str]) -> str:  # report.hpp:43-50
+    return ",".join(_escape(f) for f in fields) + "\r\n"
+
+
+def trace_to_csv(trace: Iterable[TracePoint]) -> str:
+    out = _row(["k", "rrn", "residual_rel", "row"])
+    for t in trace:
+        out += _row([str(t.k), _num(t.rrn), _num(t.residual_rel), str(t.selected_row)])
+    return out
+
+
+def solve_report_to_json(rep: SolveReport, stop: Optional[str] = None,
+                         tol: Optional[float] = None) -> dict:
+    j = {
+        "iterations": int(rep.iterations),
+        "wall_seconds": float(rep.wall_seconds),
+        "final_rrn": float(rep.final_rrn),
+        "final_residual_rel": float(rep.final_residual_rel),
+        "terminated_by": "tolerance" if rep.terminated_by == Terminated.Tolerance else "max_iter",
+        "method": rep.method_label,
+        "alpha": float(rep.alpha),
+        "seed": int(rep.seed),
+        "alpha_outside_bound": bool(rep.alpha_outside_bound),
+        "skipped_zero_rows": int(rep.skipped_zero_rows),
+        "x_rows": int(rep.X.shape[0]) if rep.X is not None else 0,
+        "x_cols": int(rep.X.shape[1]) if rep.X is not None else 0,
+    }
+    if stop is not None:
+        j["stop"] = stop
+    if tol is not None:
+        j["tol"] = float(tol)
+    return j
+
+
+def dumps_json(obj) -> str:
+    return json.dumps(obj, indent=2, sort_keys=True) + "\n"
+
+
+def write_solve_outputs(out_dir: str, rep: SolveReport, stop: str, tol: float,
+                        trace: bool = True) -> None:
+    """report.json (+ trace.csv) as `axbsolve solve` writes them (axbsolve.cpp:205-212)."""
+    os.makedirs(out_dir, exist_ok=True)
+    with open(os.path.join(out_dir, "report.json"), "w", newline="") as f:
+        f.write(dumps_json(solve_report_to_json(rep, stop, tol)))
+    if trace:
+        with open(os.path.join(out_dir, "trace.csv"), "w", newline="") as f:
+            f.write(trace_to_csv(rep.trace))
