@@ -1,12 +1,14 @@
 #!/usr/bin/env python3
 """Benchmark: Kaczmarz iterations/s of the B200 solver (BASELINE.json metric).
 
-Workload (default --config 3, BASELINE.json configs[2], the HBM-bound case):
-ME-GRBK (θ=½, i.e. RGRBK θ=0.5) fp64, A 8192×2048 and B 2048×8192 iid N(0,1),
-X* 2048×2048 N(0,1), C = A·X*·B, X0 N(0,1), stop solution_rrn(1e-12, X*) (never met
-within the timed window), refresh checkpoints every 1000 iterations as the reference
-defaults.  One "step" = one Kaczmarz iteration (select → y → z/X → fused R update).
-Inputs are synthetic (seeded torch RNG on the device); R (537 MB) exceeds the 126 MB
+Workload (default --config 5, BASELINE.json configs[4]: the large row-sharded
+system, the largest that fits one GPU): ME-GRBK fp64, A 65536×8192 N(0,1/8192),
+B 8192×32768 N(0,1/32768), X* 8192×8192 N(0,1), C = A·X*·B, X0 = 0, stop
+solution_rrn(1e-12, X*), refresh checkpoints every 1000 iterations (the reference
+default; none fall inside a default run).  --config 3 (A 8192×2048, B 2048×8192,
+X0 N(0,1)) and --config 1 are the other bench workloads.  One "step" = one
+Kaczmarz iteration (select → y → z/X → fused R update).  Inputs are synthetic
+(seeded torch RNG on the device); R (17 GB; 537 MB at config 3) exceeds the 126 MB
 L2, so no explicit flush is needed between iterations.
 
 N > 1 (torchrun): one process per GPU and ONE system, row-sharded:
@@ -37,13 +39,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    1: dict(m=500, p=100, q=80, n=400, x0="zero", scale_a=1.0, scale_b=1.0,
+    1: dict(m=500, p=100, q=80, n=400, x0="zero", scale_a=1.0, scale_b=1.0, cpu_div=1,
             desc="config1: ME-GRBK fp64 A 500x100, B 80x400 iid N(0,1), X0=0"),
-    3: dict(m=8192, p=2048, q=2048, n=8192, x0="randn", scale_a=1.0, scale_b=1.0,
+    3: dict(m=8192, p=2048, q=2048, n=8192, x0="randn", scale_a=1.0, scale_b=1.0, cpu_div=1,
             desc="config3: ME-GRBK(theta=1/2) fp64 A 8192x2048, B 2048x8192 iid N(0,1), "
                  "X0 N(0,1), X* N(0,1), C=A.X*.B"),
     5: dict(m=65536, p=8192, q=8192, n=32768, x0="zero", scale_a=8192 ** -0.5,
-            scale_b=32768 ** -0.5,
+            scale_b=32768 ** -0.5, cpu_div=8,
             desc="config5: ME-GRBK fp64 A 65536x8192 N(0,1/8192), B 8192x32768 N(0,1/32768), "
                  "X* 8192x8192 N(0,1), X0=0"),
 }
@@ -169,6 +171,21 @@ def iteration_bytes(cfg, gram_cached=True):
 
 
 # --------------------------------------------------------------------- CPU legs
+def cpu_sample_cfg(cfg):
+    """The CPU legs run the reference's per-iteration algorithm on the workload
+    itself, or (config 5: its R alone is 17 GB and the reference constructor
+    needs ~10¹⁴ FLOP) on the instance with every dimension divided by cpu_div.
+    Each per-iteration term of the reference (R update m·n, z = BᵀB·R_iᵀ n²,
+    y q·n, X p·q) then shrinks by exactly cpu_div², which scales the time back."""
+    d = cfg["cpu_div"]
+    c = dict(cfg)
+    for k in ("m", "p", "q", "n"):
+        c[k] = cfg[k] // d
+    c["scale_a"] = c["p"] ** -0.5 if cfg["scale_a"] != 1.0 else 1.0
+    c["scale_b"] = c["n"] ** -0.5 if cfg["scale_b"] != 1.0 else 1.0
+    return c, d * d
+
+
 def cpu_prepared_state(cfg, seed):
     """Host inputs + the reference constructor's caches (numpy BLAS: setup only)."""
     import numpy as np
@@ -201,7 +218,8 @@ def cpu_baseline(cfg, budget_s=15.0):
     import oracle_lib as O
 
     orc = O.oracle()
-    state = cpu_prepared_state(cfg, 7)
+    scfg, factor = cpu_sample_cfg(cfg)
+    state = cpu_prepared_state(scfg, 7)
     s, _keep = cpu_solver(O, orc, state, 42)
     s.steps(1)  # warm
     t0 = time.perf_counter()
@@ -212,10 +230,13 @@ def cpu_baseline(cfg, budget_s=15.0):
         if time.perf_counter() - t0 >= budget_s or done >= 2000:
             break
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "iter/s", "cores": 1, "kind": "port",
-            "sample": f"{done} ME-GRBK iterations of one {cfg['m']}x{cfg['p']}.{cfg['q']}x{cfg['n']} "
-                      f"solve (oracle C port of solver.hpp step(); constructor caches "
-                      f"precomputed with numpy), {dt:.1f}s on 1 core"}
+    shape = f"{scfg['m']}x{scfg['p']}.{scfg['q']}x{scfg['n']}"
+    extra = (f"; extrapolated x{factor} to {cfg['m']}x{cfg['p']}.{cfg['q']}x{cfg['n']} "
+             f"(every per-iteration term scales by {factor})" if factor > 1 else "")
+    return {"value": done / dt / factor, "unit": "iter/s", "cores": 1, "kind": "port",
+            "sample": f"{done} ME-GRBK iterations of one {shape} solve (oracle C port of "
+                      f"solver.hpp step(); constructor caches precomputed with numpy), "
+                      f"{dt:.1f}s on 1 core{extra}"}
 
 
 def reference_arm(args, cfg):
@@ -225,7 +246,8 @@ def reference_arm(args, cfg):
     orc = O.oracle()
     T = max(1, min(os.cpu_count() or 1, args.ref_threads))
     log(f"[reference] preparing {cfg['desc']} on the host; {T} solver threads")
-    state = cpu_prepared_state(cfg, 7)
+    scfg, factor = cpu_sample_cfg(cfg)
+    state = cpu_prepared_state(scfg, 7)
     solvers = [cpu_solver(O, orc, state, 42 + t) for t in range(T)]
     per = max(1, math.ceil(args.steps / T))
     budget = args.ref_budget_s
@@ -238,6 +260,7 @@ def reference_arm(args, cfg):
     solvers[0][0].steps(1)
     one = time.perf_counter() - t0
     per = max(1, min(per, int(budget / max(one, 1e-9) / 1.5)))
+    per = max(per, min(int(10.0 / max(one, 1e-9)), 10 ** 6))  # at least ~10 s of CPU work
     counts = [0] * T
 
     def work(t):
@@ -253,12 +276,16 @@ def reference_arm(args, cfg):
         th.join()
     dt = time.perf_counter() - t0
     total = sum(counts)
-    value = total / dt
+    value = total / dt / factor
     cores = T
+    shape = f"{scfg['m']}x{scfg['p']}.{scfg['q']}x{scfg['n']}"
+    extra = (f"; instance {shape} (every dimension /{cfg['cpu_div']}), time extrapolated "
+             f"x{factor}" if factor > 1 else "")
     line = {
         "impl": "reference",
         "metric": "kaczmarz_iterations_per_sec", "value": value, "unit": "iter/s",
-        "n_gpus": args.gpus, "steps": total, "warmup": wper * T, "ms_per_step": 1000.0 * dt / total,
+        "n_gpus": args.gpus, "steps": total, "warmup": wper * T,
+        "ms_per_step": 1000.0 * dt * factor / total,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (numpy seeded N(0,1))",
         "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
@@ -266,7 +293,7 @@ def reference_arm(args, cfg):
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port",
                          "sample": f"{T} concurrent solves x {per} iterations (reference "
                                    f"benchmark-pool pattern), oracle C port of solver.hpp "
-                                   f"step(), {dt:.1f}s wall"},
+                                   f"step(), {dt:.1f}s wall{extra}"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -276,10 +303,10 @@ def reference_arm(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tol", action="store_true")
@@ -377,6 +404,7 @@ def main():
     s.set_profiling(True)
     s.steps(args.profile_steps, mirror_refresh=False)
     pt = s.last_timing()
+    kt = s.kernel_times()
     s.set_profiling(False)
     k2_ms = pt["k2_ms"] / max(pt["k2_launches"], 1)
     peak, peak_kind = peaks()
@@ -396,6 +424,8 @@ def main():
                 "algorithmic_bytes_per_launch": kb, "k2_ms": round(k2_ms, 5),
                 "peak_kind": peak_kind,
                 "k2_share_of_step": round(k2_ms / per_iter_ms, 4),
+                "in_pipeline_ms": {"k_yg": round(kt["yg_ms"], 5), "k_zx": round(kt["zx_ms"], 5),
+                                   "k_r_tma": round(kt["k2_ms"], 5)},
                 "iteration_bytes": iteration_bytes(cfg),
                 "iteration_achieved_gbs": round(iteration_bytes(cfg) / (per_iter_ms / 1000) / 1e9, 1)}
     del s

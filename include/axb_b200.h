@@ -219,6 +219,9 @@ int axb_solver_dims(const axb_solver* s, uint64_t dims[4]); /* m, p, q, n */
  * it, with its launch count. */
 int axb_solver_last_timing(const axb_solver* s, double* loop_ms, double* k2_ms,
                            uint64_t* k2_launches, uint64_t* kernel_launches);
+/* Average per-launch device times (ms) of K4 (y), K4b+K5 (z, X) and K2 over the
+ * last profiled steps()/run(), CUDA events between consecutive launches. */
+int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]);
 /* Enable per-kernel CUDA-event timing of K2 inside steps()/run() (adds events to
  * the captured graph; off by default). */
 int axb_solver_set_profiling(axb_solver* s, int32_t on);

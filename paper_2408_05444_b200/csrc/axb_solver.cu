@@ -222,7 +222,7 @@ struct axb_solver {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;
-    double loop_ms = 0.0, k2_ms = 0.0;
+    double loop_ms = 0.0, k2_ms = 0.0, yg_ms = 0.0, zx_ms = 0.0;
     uint64_t k2_launches = 0, kernel_launches = 0;
 
     ~axb_solver() {
@@ -847,19 +847,21 @@ struct axb_solver {
         if (P.persist && !profiling) {
             // nothing more to enqueue
         } else if (profiling) {
-            if (prof_ev.size() < 2 * nb) {
+            if (prof_ev.size() < 4 * nb) {
                 size_t have = prof_ev.size();
-                prof_ev.resize(2 * nb);
+                prof_ev.resize(4 * nb);
                 for (size_t i = have; i < prof_ev.size(); ++i) ck(cudaEventCreate(&prof_ev[i]), "ev");
             }
             for (uint64_t i = 0; i < nb; ++i) {
+                ck(cudaEventRecord(prof_ev[4 * i], stream), "ev");
                 launch_yg(P, stream, !gram_cached);
+                ck(cudaEventRecord(prof_ev[4 * i + 1], stream), "ev");
                 if (sharded) allreduce(y.p, y.p, q);
                 launch_zx(P, stream);
                 if (sharded) allgather_inplace(z.p, n_loc);
-                ck(cudaEventRecord(prof_ev[2 * i], stream), "ev");
+                ck(cudaEventRecord(prof_ev[4 * i + 2], stream), "ev");
                 launch_r(P, stream, true);
-                ck(cudaEventRecord(prof_ev[2 * i + 1], stream), "ev");
+                ck(cudaEventRecord(prof_ev[4 * i + 3], stream), "ev");
                 if (sharded) {
                     allgather_inplace(recs.p, 4);
                     launch_sel1(P, stream, true);
@@ -881,9 +883,13 @@ struct axb_solver {
         if (profiling) {
             const uint64_t done = hs->k - k;
             for (uint64_t i = 0; i < done; ++i) {
-                float ms = 0.f;
-                ck(cudaEventElapsedTime(&ms, prof_ev[2 * i], prof_ev[2 * i + 1]), "elapsed");
-                k2_ms += ms;
+                float a = 0.f, b = 0.f, c = 0.f;
+                ck(cudaEventElapsedTime(&a, prof_ev[4 * i], prof_ev[4 * i + 1]), "elapsed");
+                ck(cudaEventElapsedTime(&b, prof_ev[4 * i + 1], prof_ev[4 * i + 2]), "elapsed");
+                ck(cudaEventElapsedTime(&c, prof_ev[4 * i + 2], prof_ev[4 * i + 3]), "elapsed");
+                yg_ms += a;
+                zx_ms += b;
+                k2_ms += c;
                 ++k2_launches;
             }
         }
@@ -1460,9 +1466,18 @@ int axb_solver_last_error_info(const axb_solver* s, uint64_t* iteration, double*
     if (value) *value = s->err_val;
     return AXB_OK;
 }
+int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]) {
+    const double nl = s->k2_launches ? (double)s->k2_launches : 1.0;
+    out_ms[0] = s->yg_ms / nl;
+    out_ms[1] = s->zx_ms / nl;
+    out_ms[2] = s->k2_ms / nl;
+    return AXB_OK;
+}
 int axb_solver_set_profiling(axb_solver* s, int32_t on) {
     s->profiling = on != 0;
     s->k2_ms = 0.0;
+    s->yg_ms = 0.0;
+    s->zx_ms = 0.0;
     s->k2_launches = 0;
     s->kernel_launches = 0;
     return AXB_OK;

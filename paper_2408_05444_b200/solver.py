@@ -469,6 +469,12 @@ class Solver:
     def set_profiling(self, on: bool):
         self._lib.axb_solver_set_profiling(self._h, 1 if on else 0)
 
+    def kernel_times(self):
+        """Average in-pipeline ms per launch of K4 (y), K4b+K5 (z, X), K2 (profiled runs)."""
+        out = (C.c_double * 3)()
+        self._lib.axb_solver_kernel_times(self._h, out)
+        return {"yg_ms": out[0], "zx_ms": out[1], "k2_ms": out[2]}
+
     def last_timing(self):
         a = C.c_double(); b = C.c_double(); c = C.c_uint64(); d = C.c_uint64()
         self._lib.axb_solver_last_timing(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
