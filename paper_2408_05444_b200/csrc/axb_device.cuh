@@ -178,9 +178,12 @@ struct GemmArgs {
     double* sq_part;
     double* diff_part;
     int store;
+    int sym;  // D = A·Aᵀ: compute only tiles on/above the diagonal (mirror with launch_mirror_lower)
 };
 int gemm_num_ctas(long long M, long long N);
 void launch_gemm(const GemmArgs& g, cudaStream_t s);
 void launch_reduce_parts(const double* part, long long n, double* out, cudaStream_t s);
+// D[i][j] = D[j][i] for the strictly-lower 32×32 blocks of a square matrix
+void launch_mirror_lower(double* D, long long nn, long long ld, cudaStream_t s);
 
 }  // namespace axb_dev

@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dgemm(GemmArgs g) {
     const int wm = warp >> 2, wn = warp & 3;  // 2 × 4 warps
     const int gq = lane >> 2, tq = lane & 3;
     const long long m0 = (long long)blockIdx.y * BM, n0 = (long long)blockIdx.x * BN;
+    if (g.sym && n0 + BN <= m0) return;  // strictly below the diagonal: mirrored later
     const long long KT = (g.K + BK - 1) / BK;
 
     double acc[8][4][2];
@@ -250,6 +251,23 @@ __global__ void __launch_bounds__(1024) k_reduce_parts(const double* part, long 
     }
 }
 
+// lower 32×32 blocks ← transposed upper blocks (gram_mmt's mirror, matrix.hpp:489-490)
+__global__ void k_mirror_lower(double* D, long long nn, long long ld) {
+    __shared__ double t[32][33];
+    const long long bi = blockIdx.y, bj = blockIdx.x;  // destination block (bi, bj), bj < bi
+    if (bj >= bi) return;
+    const long long r0 = bj * 32, c0 = bi * 32;  // source block (bj, bi) in the upper part
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const long long r = r0 + j, c = c0 + threadIdx.x;
+        if (r < nn && c < nn) t[j][threadIdx.x] = D[r * ld + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const long long r = c0 + j, c = r0 + threadIdx.x;  // D[c0+j][r0+x] = D[r0+x][c0+j]
+        if (r < nn && c < nn) D[r * ld + c] = t[threadIdx.x][j];
+    }
+}
+
 template <bool BT, bool V>
 void launch_t(const GemmArgs& g, cudaStream_t s) {
     const size_t smem = sizeof(double) * (size_t)STAGES * (A_STAGE + B_STAGE);
@@ -279,6 +297,11 @@ void launch_gemm(const GemmArgs& g, cudaStream_t s) {
         if (v16) launch_t<false, true>(g, s);
         else launch_t<false, false>(g, s);
     }
+}
+
+void launch_mirror_lower(double* D, long long nn, long long ld, cudaStream_t s) {
+    const unsigned nb = (unsigned)((nn + 31) / 32);
+    k_mirror_lower<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(D, nn, ld);
 }
 
 void launch_reduce_parts(const double* part, long long n, double* out, cudaStream_t s) {

@@ -138,12 +138,22 @@ __device__ double warp_dot(const double* __restrict__ row, const double* __restr
 
 // ------------------------------------------------------------------------
 // K4: y = B·R_iᵀ (solver.hpp:270) [+ g = A·A_iᵀ, the Gram column of :294].
-// One 128-thread CTA per output row (grid-stride): 4 warps share a row so the
-// B stream has enough loads in flight even when q is small; fixed-order
-// lane/warp reduction (deterministic).
-constexpr int kYgThreads = 128;
+// A CTA computes 8 row dots (one per warp) against the shared vector, which is
+// staged through shared memory in kYgSeg-column segments, so R_i (A_i) is read
+// from L2 once per 8 rows instead of once per row.  Each lane accumulates its
+// columns in order across segments, then a shuffle tree: deterministic, and the
+// same order as one pass over the row.
+constexpr int kYgThreads = 256;
+constexpr int kYgWarps = kYgThreads / 32;
+constexpr int kYgSeg = 2048;
+// rows per CTA: enough CTAs to cover the chip (≈148×8), as many rows as possible
+// per staged segment of the shared vector
+__host__ __device__ inline int yg_rows_per_cta(long long rows) {
+    return rows >= 8 * 1184 ? 8 : rows >= 4 * 1184 ? 4 : rows >= 2 * 1184 ? 2 : 1;
+}
 __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
-    __shared__ double red[kYgThreads / 32];
+    __shared__ __align__(16) double vs[kYgSeg];
+    __shared__ double part[kYgWarps];
     pdl_wait();
     pdl_trigger();
     const DevState* st = P.st;
@@ -159,42 +169,85 @@ __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
         Ai = P.A + il * P.p;
     }
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const long long items = P.q + (with_g ? P.m : 0);
-    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-        const double* row;
-        const double* v;
-        long long len;
-        if (it < P.q) {  // this rank's column slice [c0, c1) (all of B on one GPU)
-            row = P.B + it * P.n + P.c0; v = Ri + P.c0; len = P.c1 - P.c0;
-        } else {
-            row = P.A + (it - P.q) * P.p; v = Ai; len = P.p;
-        }
-        double a0 = 0.0, a1 = 0.0;
-        if ((len & 1) == 0) {
-            const double2* r2 = reinterpret_cast<const double2*>(row);
-            const double2* v2 = reinterpret_cast<const double2*>(v);
-            const long long h = len >> 1;
+    const int rbq = yg_rows_per_cta(P.q), rbm = yg_rows_per_cta(P.m);
+    const long long nbq = (P.q + rbq - 1) / rbq;
+    const long long nb = nbq + (with_g ? (P.m + rbm - 1) / rbm : 0);
+    for (long long b = blockIdx.x; b < nb; b += gridDim.x) {
+        const bool isB = b < nbq;
+        const int rb = isB ? rbq : rbm;
+        const int wpr = kYgWarps / rb;  // warps per row
+        const int r = w / wpr, pw = w % wpr;
+        const long long it = isB ? b * rb + r : (b - nbq) * rb + r;
+        const long long rows = isB ? P.q : P.m;
+        const double* row = isB ? P.B + it * P.n + P.c0 : P.A + it * P.p;
+        const double* v = isB ? Ri + P.c0 : Ai;
+        const long long len = isB ? P.c1 - P.c0 : P.p;
+        const bool live = it < rows;
+        const bool v2 = (len & 1) == 0 && ((reinterpret_cast<uintptr_t>(row) |
+                                            reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+        if (rb == 1) {
+            // one row per CTA: no reuse to stage for; all 256 threads stride the
+            // row, the vector comes through L1, fixed-order block reduction
+            double a0 = 0.0, a1 = 0.0;
+            if (live) {
+                if (v2) {
+                    const double2* r2 = reinterpret_cast<const double2*>(row);
+                    const double2* s2 = reinterpret_cast<const double2*>(v);
 #pragma unroll 8
-            for (long long k = tid; k < h; k += kYgThreads) {
-                const double2 a = __ldg(r2 + k);  // keep B in L2 for the z pass
-                const double2 b = __ldg(v2 + k);
-                a0 += a.x * b.x;
-                a1 += a.y * b.y;
+                    for (long long k = tid; k < (len >> 1); k += kYgThreads) {
+                        const double2 a = __ldg(r2 + k);
+                        const double2 bb = __ldg(s2 + k);
+                        a0 += a.x * bb.x;
+                        a1 += a.y * bb.y;
+                    }
+                } else {
+#pragma unroll 8
+                    for (long long k = tid; k < len; k += kYgThreads) a0 += __ldg(row + k) * __ldg(v + k);
+                }
             }
-        } else {
+            const double t = block_sum(a0 + a1, part);
+            if (live && tid == 0) {
+                if (isB) P.y[it] = t;
+                else P.g[it] = t;
+            }
+            __syncthreads();
+            continue;
+        }
+        double acc = 0.0;
+        for (long long c0 = 0; c0 < len; c0 += kYgSeg) {
+            const int sw = (int)min((long long)kYgSeg, len - c0);
+            __syncthreads();
+            for (int k = tid; k < sw; k += kYgThreads) vs[k] = __ldg(v + c0 + k);
+            __syncthreads();
+            if (!live) continue;
+            // this warp's contiguous share of the segment (multiples of 64 columns)
+            const int chunk = (((sw + wpr - 1) / wpr) + 63) & ~63;
+            const int k0 = pw * chunk, k1 = min(sw, k0 + chunk);
+            if (v2) {
+                const double2* r2 = reinterpret_cast<const double2*>(row + c0);
+                const double2* s2 = reinterpret_cast<const double2*>(vs);
 #pragma unroll 8
-            for (long long k = tid; k < len; k += kYgThreads) a0 += __ldg(row + k) * __ldg(v + k);
+                for (int k = (k0 >> 1) + lane; k < (k1 >> 1); k += 32) {
+                    const double2 a = __ldg(r2 + k);  // keep B in L2 for the z pass
+                    const double2 bb = s2[k];
+                    acc += a.x * bb.x;
+                    acc += a.y * bb.y;
+                }
+            } else {
+#pragma unroll 8
+                for (int k = k0 + lane; k < k1; k += 32) acc += __ldg(row + c0 + k) * vs[k];
+            }
         }
-        double acc = warp_sum(a0 + a1);
-        if (lane == 0) red[w] = acc;
+        acc = warp_sum(acc);
         __syncthreads();
-        if (tid == 0) {
+        if (lane == 0) part[w] = acc;
+        __syncthreads();
+        if (live && pw == 0 && lane == 0) {  // fixed-order combine of the row's warps
             double t = 0.0;
-            for (int k = 0; k < kYgThreads / 32; ++k) t += red[k];
-            if (it < P.q) P.y[it] = t;
-            else P.g[it - P.q] = t;
+            for (int k = 0; k < wpr; ++k) t += part[r * wpr + k];
+            if (isB) P.y[it] = t;
+            else P.g[it] = t;
         }
-        __syncthreads();
     }
 }
 

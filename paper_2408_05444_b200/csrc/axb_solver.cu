@@ -522,7 +522,9 @@ struct axb_solver {
             ga.B = A.p; ga.ldb = p; ga.b_trans = 1;
             ga.D = G.p; ga.ldd = m;
             ga.store = 1;
+            ga.sym = sharded ? 0 : 1;  // one GPU: G = A·Aᵀ symmetric, upper tiles + mirror
             launch_gemm(ga, stream);
+            if (!sharded) launch_mirror_lower(G.p, (long long)m, (long long)m, stream);
             sync("G");  // A_all released at scope end
         } else {
             g.alloc(m, "g");
@@ -573,10 +575,14 @@ struct axb_solver {
             P.r_chunk = (int)std::min<uint64_t>(n, 4096);
             if (P.r_chunk & 1) P.r_chunk += (n > (uint64_t)P.r_chunk) ? 1 : 0;
         }
-        const uint64_t items = q + (gram_cached ? 0 : m);
-        P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(148 * 16, items));
+        {
+            auto rpc = [](uint64_t r) { return r >= 8 * 1184 ? 8 : r >= 4 * 1184 ? 4 : r >= 2 * 1184 ? 2 : 1; };
+            const uint64_t blocks = (q + rpc(q) - 1) / rpc(q) + (gram_cached ? 0 : (m + rpc(m) - 1) / rpc(m));
+            P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, blocks));
+        }
         P.z_nslab = (int)std::max<long long>(1, (P.c1 - P.c0 + 511) / 512);
-        int nj = (int)std::max<uint64_t>(1, std::min<uint64_t>((target + P.z_nslab - 1) / P.z_nslab,
+        const int ztarget = env_int("AXB_Z_TARGET", 148 * 8);  // z-part CTAs
+        int nj = (int)std::max<uint64_t>(1, std::min<uint64_t>((ztarget + P.z_nslab - 1) / P.z_nslab,
                                                                 (q + 7) / 8));
         P.z_jrows = (int)((q + nj - 1) / nj);
         P.z_nj = (int)((q + P.z_jrows - 1) / P.z_jrows);
@@ -672,7 +678,9 @@ struct axb_solver {
             ga.K = n; ga.A = B.p; ga.lda = n; ga.B = B.p; ga.ldb = n;
         }
         ga.D = M.p; ga.ldd = dim;
+        ga.sym = 1;
         launch_gemm(ga, stream);
+        launch_mirror_lower(M.p, (long long)dim, (long long)dim, stream);
         std::vector<double> v0 = power_start(dim);
         v.alloc(dim, "power v");
         w.alloc(dim, "power w");

@@ -6,6 +6,8 @@ xoshiro256** stream — same index sequence (the oracle's) and iterates within
 1e-10 relative; every variant reaches the same relative error.
 Oracle = oracle/axb_oracle.c, bitwise-pinned to the unmodified reference.
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -287,3 +289,19 @@ def test_csr_operands_match_dense_and_oracle(axb, orc, tag):
     np.testing.assert_array_equal(sc.X(), sg.X())
     np.testing.assert_array_equal(rd, ro)
     assert rel(sc.X(), so.X()) <= RTOL_X
+
+
+def test_device_spectral_norm_matches_reference_power_iteration(axb, orc):
+    """‖B‖₂ on the device (power iteration on the DMMA-formed, mirrored Gram) agrees
+    with the reference's host power iteration (decomp.hpp:207-239) to its tolerance."""
+    A, B, X, Cm = O.generate(orc, 5, 200, 60, 300, 700)   # q < n: Gram B·Bᵀ
+    A2, B2, X2, C2 = O.generate(orc, 6, 200, 60, 700, 300)  # n < q: Gram BᵀB
+    for (a, b, c) in ((A, B, Cm), (A2, B2, C2)):
+        cfg = axb.SolveConfig(method=axb.Method.mwrbk(), stop=axb.StopRule.residual_rel(0.0))
+        host = axb.Solver(a, b, c, None, cfg, axb.Options(spectral_on_device=0)).spectral_norm_b()
+        dev = axb.Solver(a, b, c, None, cfg, axb.Options(spectral_on_device=1)).spectral_norm_b()
+        st = C.c_int()
+        ref = orc.spectral_norm(O._ptr(np.ascontiguousarray(b)), b.shape[0], b.shape[1], 1e-10, 5000,
+                                C.byref(st), None)
+        assert host == ref
+        assert abs(dev - ref) <= 1e-9 * ref

@@ -5,6 +5,7 @@ usage: python tools/summarize_profile.py r1_config3
 import collections, csv, json, os, subprocess, sys
 
 tag = sys.argv[1]
+cfg_id = sys.argv[2] if len(sys.argv) > 2 else "5"
 G = "gpurun_out"
 os.makedirs("profiles", exist_ok=True)
 out = [f"# ncu summary {tag}\n"]
@@ -65,7 +66,7 @@ for name, d in summary.items():
         wr = float(d["dram__bytes_write.sum"]) * mult[d["_units"]["dram__bytes_write.sum"]]
         json.dump({"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr,
                    "source": f"profiles/{tag}_ncu_full.json (ncu --set full, one launch)"},
-                  open(os.path.join("profiles", "k2_traffic_config3.json"), "w"), indent=1)
+                  open(os.path.join("profiles", f"k2_traffic_config{cfg_id}.json"), "w"), indent=1)
 for b in ("bench.json", "bench_ref.json"):
     p = os.path.join(G, b)
     if os.path.exists(p):
