@@ -1,0 +1,159 @@
+"""Benchmark pool over the B200 path — the reference harness, device-side.
+
+Mirrors axb::benchmark (analysis.hpp:255-356): every (problem, method, trial)
+combination runs with the shared per-trial substream seed
+RngStream(seed).substream(trial).seed() (:279, rng.hpp:102-104), X0 = 0; IT and
+wall time are averaged over converged trials, divergent or budget-exhausted
+trials are counted as failures, and each row reports its speed-up against the
+RBK row of the same problem (:315-354).
+
+Where the reference runs one solve per CPU thread, tasks here are spread over
+``jobs`` host threads driving independent solver handles (each with its own CUDA
+stream) on ``devices`` round-robin: the small, latency-bound solves of the
+harness overlap on one GPU instead of queueing.  The C-ABI
+releases the GIL for the duration of each call.
+"""
+from __future__ import annotations
+
+import math
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from .errors import ConfigError, DivergenceError
+from .solver import AlphaRule, Method, MethodTag, Options, SolveConfig, Solver, StopRule, Terminated
+
+_M64 = (1 << 64) - 1
+
+
+def _mix_pure(z: int) -> int:  # rng.hpp:113-117
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def substream_seed(seed: int, trial: int) -> int:
+    """RngStream(seed).substream(trial).seed() — rng.hpp:102-104."""
+    return (seed ^ _mix_pure((0x5851F42D4C957F2D + trial) & _M64)) & _M64
+
+
+@dataclass
+class BenchProblem:
+    id: str
+    A: np.ndarray
+    B: np.ndarray
+    C: np.ndarray
+    X_star: Optional[np.ndarray] = None  # reference solution for solution_rrn stopping
+
+
+@dataclass
+class BenchmarkOptions:  # analysis.hpp BenchmarkOptions
+    trials: int = 20
+    alpha_rule: AlphaRule = AlphaRule.Safe
+    alpha_value: float = 0.0
+    max_iter: int = 200000
+    seed: int = 0
+    stop_kind: StopRule.Kind = StopRule.Kind.SolutionRrn
+    tol: float = 1e-6
+    jobs: int = 4
+    devices: Sequence[int] = (0,)
+    options: dict = field(default_factory=dict)  # extra solver Options fields
+
+
+@dataclass
+class BenchmarkRow:  # analysis.hpp:225-236
+    problem_id: str
+    method: str
+    theta: Optional[float]
+    alpha_rule: str
+    trials: int
+    it_mean: float = 0.0
+    it_std: float = 0.0
+    wall_mean_s: float = 0.0
+    speed_up_vs_rbk: Optional[float] = None
+    failures: int = 0
+
+
+def benchmark(problems: List[BenchProblem], methods: List[Method],
+              opt: BenchmarkOptions) -> List[BenchmarkRow]:
+    if opt.trials < 1:
+        raise ConfigError("benchmark: trials must be >= 1")
+    for m in methods:
+        m.validate()
+    tasks = [(p, mi, t) for p in range(len(problems)) for mi in range(len(methods))
+             for t in range(opt.trials)]
+    outcomes = [None] * len(tasks)
+
+    def run_task(idx):
+        p, mi, t = tasks[idx]
+        pb = problems[p]
+        if opt.stop_kind == StopRule.Kind.SolutionRrn:
+            if pb.X_star is None:
+                raise ConfigError(f"problem {pb.id}: solution_rrn stopping needs X_star")
+            stop = StopRule.solution_rrn(opt.tol, pb.X_star)
+        else:
+            stop = StopRule.residual_rel(opt.tol)
+        cfg = SolveConfig(method=methods[mi], alpha_rule=opt.alpha_rule,
+                          alpha_value=opt.alpha_value, stop=stop, max_iter=opt.max_iter,
+                          seed=substream_seed(opt.seed, t))
+        dev = opt.devices[idx % len(opt.devices)]
+        try:
+            rep = Solver(pb.A, pb.B, pb.C, None, cfg, Options(device=dev, **opt.options)).run()
+            outcomes[idx] = (float(rep.iterations), rep.wall_seconds,
+                             rep.terminated_by == Terminated.MaxIter)
+        except DivergenceError:
+            outcomes[idx] = (0.0, 0.0, True)
+
+    jobs = max(1, min(opt.jobs, len(tasks)))
+    nxt = [0]
+    lock = threading.Lock()
+    errors = []
+
+    def worker():
+        while True:
+            with lock:
+                i = nxt[0]
+                nxt[0] += 1
+            if i >= len(tasks):
+                return
+            try:
+                run_task(i)
+            except Exception as e:  # surface after the pool drains
+                errors.append(e)
+                return
+
+    threads = [threading.Thread(target=worker) for _ in range(jobs)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+
+    rows, rbk_wall = [], [-1.0] * len(problems)
+    for p, pb in enumerate(problems):
+        for mi, m in enumerate(methods):
+            row = BenchmarkRow(pb.id, m.label(), m.theta, opt.alpha_rule.name.lower(), opt.trials)
+            its, walls = [], []
+            for t in range(opt.trials):
+                it, wall, failed = outcomes[(p * len(methods) + mi) * opt.trials + t]
+                if failed:
+                    row.failures += 1
+                    continue
+                its.append(it)
+                walls.append(wall)
+            if its:
+                row.it_mean = sum(its) / len(its)
+                row.wall_mean_s = sum(walls) / len(walls)
+                var = sum((v - row.it_mean) ** 2 for v in its)
+                row.it_std = math.sqrt(var / (len(its) - 1)) if len(its) > 1 else 0.0
+            if m.tag == MethodTag.RBK and its:
+                rbk_wall[p] = row.wall_mean_s
+            rows.append(row)
+    for row in rows:
+        for p, pb in enumerate(problems):
+            if pb.id == row.problem_id and rbk_wall[p] > 0.0 and row.wall_mean_s > 0.0:
+                row.speed_up_vs_rbk = rbk_wall[p] / row.wall_mean_s
+    return rows

@@ -41,6 +41,17 @@ def trace_to_csv(trace: Iterable[TracePoint]) -> str:
     return out
 
 
+def benchmark_to_csv(rows) -> str:  # report.hpp:63-75
+    out = _row(["problem_id", "method", "theta", "alpha_rule", "trials", "it_mean", "it_std",
+                "wall_mean_s", "speed_up_vs_rbk", "failures"])
+    for r in rows:
+        out += _row([r.problem_id, r.method, "" if r.theta is None else _num(r.theta), r.alpha_rule,
+                     str(r.trials), _num(r.it_mean), _num(r.it_std), _num(r.wall_mean_s),
+                     "" if r.speed_up_vs_rbk is None else _num(r.speed_up_vs_rbk),
+                     str(r.failures)])
+    return out
+
+
 def solve_report_to_json(rep: SolveReport, stop: Optional[str] = None,
                          tol: Optional[float] = None) -> dict:
     j = {

@@ -305,3 +305,29 @@ def test_device_spectral_norm_matches_reference_power_iteration(axb, orc):
                                 C.byref(st), None)
         assert host == ref
         assert abs(dev - ref) <= 1e-9 * ref
+
+
+def test_benchmark_pool_matches_sequential_oracle(axb, orc):
+    """analysis.hpp:255-356 on the device: per-trial substream seeds, concurrent
+    handles on one GPU; every trial's iteration count equals the oracle's."""
+    from paper_2408_05444_b200 import pool
+
+    probs = []
+    for k, seed in enumerate((31, 32)):
+        A, B, X, Cm = O.generate(orc, seed, 120, 30, 20, 90)
+        probs.append(pool.BenchProblem(f"p{k}", A, B, Cm, X))
+    methods = [axb.Method.rbk(), axb.Method.grbk(), axb.Method.mwrbk()]
+    opt = pool.BenchmarkOptions(trials=3, seed=5, tol=1e-12, jobs=6)
+    rows = pool.benchmark(probs, methods, opt)
+    assert len(rows) == 6 and all(r.failures == 0 for r in rows)
+    for r in rows:
+        pb = next(p for p in probs if p.id == r.problem_id)
+        tag = {"rbk": O.RBK, "grbk": O.GRBK, "mwrbk": O.MWRBK}[r.method]
+        its = []
+        for t in range(3):
+            cfg = O.make_config(method=tag, stop_kind=O.SOLUTION_RRN, tol=1e-12, reference=pb.X_star,
+                                seed=pool.substream_seed(5, t))
+            rep, _, _, _ = O.Solver(orc, pb.A, pb.B, pb.C, None, cfg).run(0)
+            its.append(rep.iterations)
+        assert abs(r.it_mean - np.mean(its)) <= 2.0, (r, its)
+    assert rows[0].speed_up_vs_rbk == 1.0

@@ -46,3 +46,24 @@ def test_report_json_matches_schema_and_nlohmann_layout(tmp_path):
 def test_csv_escaping():
     assert report._escape('a"b,c') == '"a""b,c"'
     assert report._escape("plain") == "plain"
+
+
+def test_substream_seeds_match_reference_golden():
+    """pool.substream_seed == RngStream(seed).substream(t).seed() (rng.hpp:102-104)."""
+    from paper_2408_05444_b200 import pool
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "rng.npz"))
+    for i, sd in enumerate(g["seeds"]):
+        for t in range(4):
+            assert pool.substream_seed(int(sd), t) == int(g["substream_seeds"][i][t])
+
+
+def test_benchmark_csv_layout():
+    from paper_2408_05444_b200.pool import BenchmarkRow
+
+    rows = [BenchmarkRow("p1", "rbk", None, "safe", 3, 10.0, 1.0, 0.5, 1.0, 0),
+            BenchmarkRow("p1", "rgrbk", 0.5, "safe", 3, 5.0, 0.0, 0.25, 2.0, 1)]
+    csv = report.benchmark_to_csv(rows)
+    assert csv.splitlines()[0] == ("problem_id,method,theta,alpha_rule,trials,it_mean,it_std,"
+                                   "wall_mean_s,speed_up_vs_rbk,failures")
+    assert csv.splitlines()[2] == "p1,rgrbk,0.5,safe,3,5,0,0.25,2,1"
