@@ -46,9 +46,18 @@ def pair(axb, orc, A, B, Cm, X0, tag, theta=None, seed=0, Xref=None, refresh=0, 
     return so, sg
 
 
+@pytest.fixture(params=["persistent", "graph"])
+def path(request, monkeypatch):
+    """Small systems default to the persistent cooperative kernel; "graph" forces
+    the CUDA-graph path (K4/K4b/TMA-K2 launches) on the same inputs."""
+    if request.param == "graph":
+        monkeypatch.setenv("AXB_PERSIST", "0")
+    return request.param
+
+
 @pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.MWRBK, None), (O.RGRBK, 0.25),
                                        (O.RGRBK, 0.75), (O.RBK, None), (O.BK, None)])
-def test_config1_step_sequence(axb, orc, tag, theta):
+def test_config1_step_sequence(axb, orc, tag, theta, path):
     """Config-1 shape (A 500×100, B 80×400): 3000 steps, identical rows, X within 1e-10."""
     A, B, X, Cm = O.generate(orc, 7, 500, 100, 80, 400)
     so, sg = pair(axb, orc, A, B, Cm, None, tag, theta, seed=42, Xref=X)
@@ -62,7 +71,7 @@ def test_config1_step_sequence(axb, orc, tag, theta):
     assert rel(sg.R(), so.R()) <= 1e-9
 
 
-def test_config1_run_to_tolerance(axb, orc):
+def test_config1_run_to_tolerance(axb, orc, path):
     """Config 1 end to end: ‖X−X*‖/‖X*‖ < 1e-6 ⇔ squared RRN ≤ 1e-12, refresh every 1000."""
     A, B, X, Cm = O.generate(orc, 7, 500, 100, 80, 400)
     so, sg = pair(axb, orc, A, B, Cm, None, O.GRBK, seed=42, Xref=X, refresh=1000, tol=1e-12)
@@ -125,7 +134,7 @@ def test_residual_init_with_x0(axb, orc):
     assert rel(sg.X(), so.X()) <= RTOL_X
 
 
-def test_tall_system_mwrbk_sequence(axb, orc):
+def test_tall_system_mwrbk_sequence(axb, orc, path):
     """m = 8192 rows (selection staged through the TMA ring / global path): the
     deterministic rule reproduces the reference's index sequence."""
     A, B, X, Cm = O.generate(orc, 21, 8192, 32, 16, 64)
@@ -139,7 +148,7 @@ def test_tall_system_mwrbk_sequence(axb, orc):
 
 @pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.RGRBK, 0.8), (O.RBK, None),
                                        (O.BK, None)])
-def test_tall_system_replay(axb, orc, tag, theta):
+def test_tall_system_replay(axb, orc, tag, theta, path):
     """Randomized variants replaying the reference's index stream: iterates within
     1e-10 relative after 1500 steps on a system whose residual falls by ~1e12
     (there the reference's running ‖R‖² drifts by ~1e-4 relative, so self-selected
@@ -223,7 +232,7 @@ def test_sharded_run_to_tolerance_one_rank(axb, orc):
         shard.nccl_comm_destroy(comm)
 
 
-def test_config2_mwrbk_index_sequence(axb, orc):
+def test_config2_mwrbk_index_sequence(axb, orc, path):
     """Config 2 (A 2000×500, B 400×2000, κ = 100 each; MWRBK): the deterministic
     index sequence equals the oracle's over 1500 steps, X within 1e-10 (the oracle
     costs ≈13 ms/step here, so the full 10⁴-step comparison runs in bench/notes)."""
@@ -331,3 +340,16 @@ def test_benchmark_pool_matches_sequential_oracle(axb, orc):
             its.append(rep.iterations)
         assert abs(r.it_mean - np.mean(its)) <= 2.0, (r, its)
     assert rows[0].speed_up_vs_rbk == 1.0
+
+
+@pytest.mark.parametrize("tag", [O.GRBK, O.MWRBK])
+def test_odd_width_register_streaming_path(axb, orc, tag, path):
+    """Odd n (no 16-byte rows): the register-streaming K2 on the graph path."""
+    A, B, X, Cm = O.generate(orc, 13, 700, 64, 48, 301)
+    so, sg = pair(axb, orc, A, B, Cm, None, tag, seed=4, Xref=X)
+    ro = so.steps(2000)
+    rg = sg.steps(2000)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
+    assert rel(sg.R(), so.R()) <= 1e-9
