@@ -219,6 +219,10 @@ int axb_solver_dims(const axb_solver* s, uint64_t dims[4]); /* m, p, q, n */
  * it, with its launch count. */
 int axb_solver_last_timing(const axb_solver* s, double* loop_ms, double* k2_ms,
                            uint64_t* k2_launches, uint64_t* kernel_launches);
+/* Diagnostics: out[5] = greedy selections made, out[6] = exact sequential
+ * fallbacks taken by the tie guard; out[0..4], out[7] = selection phase
+ * timestamps (ns) when built with -DAXB_TRACE_SELECT. */
+int axb_solver_debug_state(axb_solver* s, uint64_t out[8]);
 /* Average per-launch device times (ms) of K4 (y), K4b+K5 (z, X) and K2 over the
  * last profiled steps()/run(), CUDA events between consecutive launches. */
 int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]);

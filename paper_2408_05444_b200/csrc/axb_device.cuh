@@ -72,6 +72,7 @@ struct alignas(16) DevState {
     unsigned long long r_next;   // dynamic row counter of the TMA residual kernel
     int32_t replay;              // 1: select from Params::forced_rows (index-stream replay)
     int32_t packed;              // sharded: this rank's pack_send holds the last row
+    unsigned long long dbg[8];   // phase timestamps of the last greedy selection (ns)
 };
 
 struct RowRecord {   // per-CTA partial of the residual reduction

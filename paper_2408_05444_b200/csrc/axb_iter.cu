@@ -45,6 +45,19 @@ __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// phase timestamps of the greedy selection into DevState::dbg (build with
+// -DAXB_TRACE_SELECT; read with axb_solver_debug_state, tools/sel_timing.py)
+#ifdef AXB_TRACE_SELECT
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define AXB_STAMP(slot) (st->dbg[slot] = gtime())
+#else
+#define AXB_STAMP(slot) ((void)0)
+#endif
+
 __device__ __forceinline__ bool halted(const DevState* st) {
     return st->status != ST_RUN || st->k >= st->k_limit;
 }
@@ -415,25 +428,32 @@ __device__ Member make_member(const Params& P, const DevState* st, double theta)
     return mm;
 }
 
-// gs[g] = Σ member masses of rows [32g, 32g+32): coalesced loads, warp trees
+// gs[g] = Σ member masses of rows [32g, 32g+32): coalesced, branch-free loads
+// (8 groups × 2 arrays in flight per warp, every warp of the block), warp trees
 __device__ void grbk_group_sums(const Member& mem, long long m, double* gs) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (int)(blockDim.x >> 5);
     const long long ng = (m + 31) / 32;
-    if (warp < kWarps) {
-        constexpr int kG = 4;  // groups in flight per warp
-        for (long long gb = warp; gb < ng; gb += (long long)kWarps * kG) {
-            double w[kG];
+    constexpr int kG = 8;
+    for (long long gb = warp; gb < ng; gb += (long long)nw * kG) {
+        double as[kG], rs[kG];
 #pragma unroll
-            for (int u = 0; u < kG; ++u) {
-                const long long i = (gb + (long long)u * kWarps) * 32 + lane;
-                w[u] = (i < m) ? mem(i) : -1.0;
-            }
+        for (int u = 0; u < kG; ++u) {
+            const long long g = gb + (long long)u * nw;
+            const long long i = g * 32 + lane;
+            const bool ok = g < ng && i < m;
+            as[u] = ok ? __ldg(mem.a_sq + i) : 0.0;
+            rs[u] = ok ? __ldcg(mem.r_sq + i) : 0.0;
+        }
 #pragma unroll
-            for (int u = 0; u < kG; ++u) {
-                const long long g = gb + (long long)u * kWarps;
-                const double v = warp_sum(w[u] > 0.0 ? w[u] : 0.0);
-                if (lane == 0 && g < ng) gs[g] = v;
-            }
+        for (int u = 0; u < kG; ++u) {
+            const long long g = gb + (long long)u * nw;
+            const long long i = g * 32 + lane;
+            const bool member =
+                as[u] > 0.0 && (mem.row0 + i == mem.argmax ||
+                                rs[u] >= __dmul_rn(__dmul_rn(mem.zeta, as[u]), mem.r_fro));
+            const double v = warp_sum(member ? rs[u] : 0.0);
+            if (lane == 0 && g < ng) gs[g] = v;
         }
     }
     __syncthreads();
@@ -598,12 +618,15 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
     }
     // GRBK / RGRBK (solver.hpp:212-254): ζ, membership, member-mass draw.
     if (!(st->r_fro_sq > 0.0)) return 2;  // "greedy threshold: zero residual"
+    if (tid == 0) AXB_STAMP(0);
     const Member mem = make_member(P, st, theta);
     double* gs = (scratch != nullptr && (m + 31) / 32 <= scratch_cap) ? scratch : P.gsum;
     grbk_group_sums(mem, m, gs);
+    if (tid == 0) AXB_STAMP(1);
     long long g0, g1;
     double excl;
     const double total = grbk_prefix(gs, (m + 31) / 32, sh, g0, g1, excl);
+    if (tid == 0) AXB_STAMP(2);
     if (!(total > 0.0)) return 2;  // mass on zero rows only (solver.hpp:249-252)
     if (tid == 0) {
         sh.u = rng_unit(st->rng);
@@ -612,6 +635,11 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
     __syncthreads();
     const double slack = P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
     long long pick = grbk_search(mem, m, gs, g0, g1, excl, sh.target, slack, sh);
+    if (tid == 0) {
+        AXB_STAMP(3);
+        st->dbg[5] += 1;  // selections
+        if (pick < 0) st->dbg[6] += 1;  // exact sequential fallbacks
+    }
     if (pick < 0) {
         __syncthreads();
         if (tid == 0) {
@@ -643,6 +671,7 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
         __syncthreads();
         pick = sh.cand;
     }
+    if (tid == 0) AXB_STAMP(4);
     *out_row = P.row0 + pick;
     return 0;
 }
@@ -930,7 +959,7 @@ __device__ void combine_rows(const Params& P, const double* rpart, const long lo
 }
 
 template <bool UPDATE>
-__global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
+__global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ long long stage_row[32];
     __shared__ __align__(16) double stage_g[32][2];
@@ -1093,17 +1122,28 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
     double sum = 0.0, mx = -INFINITY;
     long long ax = LLONG_MAX;
     {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        // fixed-order ‖R‖² over r_sq: 16-byte loads, 8 independent accumulators
+        // per thread (deep memory-level parallelism for the serial tail)
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const long long T = blockDim.x;
-        long long l = tid;
-        for (; l + 3 * T < m; l += 4 * T) {
-            a0 += __ldcg(P.r_sq + l);
-            a1 += __ldcg(P.r_sq + l + T);
-            a2 += __ldcg(P.r_sq + l + 2 * T);
-            a3 += __ldcg(P.r_sq + l + 3 * T);
+        const long long h = m >> 1;
+        const double2* r2 = reinterpret_cast<const double2*>(P.r_sq);
+        long long k = tid;
+        for (; k + 3 * T < h; k += 4 * T) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double2 v = __ldcg(r2 + k + u * T);
+                acc[2 * u] += v.x;
+                acc[2 * u + 1] += v.y;
+            }
         }
-        for (; l < m; l += T) a0 += __ldcg(P.r_sq + l);
-        sum = (a0 + a1) + (a2 + a3);
+        for (; k < h; k += T) {
+            const double2 v = __ldcg(r2 + k);
+            acc[0] += v.x;
+            acc[1] += v.y;
+        }
+        if ((m & 1) && tid == 0) acc[0] += __ldcg(P.r_sq + m - 1);
+        sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     }
     for (int k = tid; k < (int)gridDim.x; k += blockDim.x) {
         const double* rpp = reinterpret_cast<const double*>(P.rrec + k);
@@ -1111,7 +1151,10 @@ __global__ void __launch_bounds__(kTmaThreads) k_r_tma(Params P) {
     }
     sum = block_sum(sum, redv);
     block_maxidx(mx, ax, redv, redi);
-    if (tid == 0) st->r_next = 0ull;
+    if (tid == 0) {
+        st->r_next = 0ull;
+        AXB_STAMP(7);
+    }
     // the TMA ring is idle now: reuse it as selection scratch
     finalize<UPDATE>(P, st, sum, mx, ax, stage, (long long)S * TW);
 }

@@ -781,7 +781,7 @@ struct axb_solver {
             launch_r(P, stream, false);
             allgather_inplace(recs.p, 4);
             launch_sel1(P, stream, false);
-            allgather_inplace(masses.p, 1);
+            if (needs_masses()) allgather_inplace(masses.p, 1);
         } else {
             launch_r(P, stream, false);
             if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) launch_err_fresh(P, stream);
@@ -812,6 +812,10 @@ struct axb_solver {
     // one iteration; sharded: y partial → allreduce, z slice → allgather, local R
     // update → record allgather → global stop logic + shard masses → mass
     // allgather → draw + owner pack → row allreduce
+    // greedy rules need the per-shard member masses; the others select from the
+    // allgathered records (MWRBK) or the replicated ‖A_i‖² (BK, RBK) alone
+    bool needs_masses() const { return cfg.method == AXB_GRBK || cfg.method == AXB_RGRBK; }
+
     void enqueue_iteration() {
         launch_yg(P, stream, !gram_cached);
         if (sharded) allreduce(y.p, y.p, q);
@@ -821,7 +825,7 @@ struct axb_solver {
         if (sharded) {
             allgather_inplace(recs.p, 4);
             launch_sel1(P, stream, true);
-            allgather_inplace(masses.p, 1);
+            if (needs_masses()) allgather_inplace(masses.p, 1);
             launch_sel2(P, stream);
             allreduce(pack_send.p, pack.p, n + p + 2);
         }
@@ -873,7 +877,7 @@ struct axb_solver {
                 if (sharded) {
                     allgather_inplace(recs.p, 4);
                     launch_sel1(P, stream, true);
-                    allgather_inplace(masses.p, 1);
+                    if (needs_masses()) allgather_inplace(masses.p, 1);
                     launch_sel2(P, stream);
                     allreduce(pack_send.p, pack.p, n + p + 2);
                 }
@@ -1473,6 +1477,12 @@ int axb_solver_last_error_info(const axb_solver* s, uint64_t* iteration, double*
     if (iteration) *iteration = s->err_k;
     if (value) *value = s->err_val;
     return AXB_OK;
+}
+int axb_solver_debug_state(axb_solver* s, uint64_t out[8]) {
+    return guarded(s, [&] {
+        s->pull_state();
+        for (int i = 0; i < 8; ++i) out[i] = s->hs->dbg[i];
+    });
 }
 int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]) {
     const double nl = s->k2_launches ? (double)s->k2_launches : 1.0;
