@@ -853,3 +853,364 @@ int orc_solver_steps(orc_solver* s, uint64_t k, uint64_t* rows) {
     }
     return 0;
 }
+
+/* ======================================================================== */
+/* Reference solutions: decomp.hpp + analysis.hpp             */
+/* ======================================================================== */
+
+static int set_err(char* err, int code, const char* msg) {
+    if (err) snprintf(err, 256, "%s", msg);
+    return code;
+}
+
+static double* transposed(const double* a, size_t rows, size_t cols) { /* matrix.hpp:448-453 */
+    double* t = (double*)malloc(sizeof(double) * (rows * cols ? rows * cols : 1));
+    for (size_t i = 0; i < rows; ++i)
+        for (size_t j = 0; j < cols; ++j) t[j * rows + i] = a[i * cols + j];
+    return t;
+}
+
+static double* mm(const double* a, size_t ar, size_t ac, const double* b, size_t bc) {
+    double* c = (double*)malloc(sizeof(double) * (ar * bc ? ar * bc : 1));
+    orc_matmul(a, ar, ac, b, bc, c);
+    return c;
+}
+
+static double default_rank_tol(size_t rows, size_t cols, double sigma_max) { /* decomp.hpp:30-33 */
+    return 8.0 * (double)(rows > cols ? rows : cols) * sigma_max * ldexp(1.0, -52);
+}
+
+/* detail::complete_orthonormal_columns (decomp.hpp:39-65); u is m×r */
+static int complete_orthonormal_columns(double* u, size_t m, size_t r, size_t from) {
+    size_t next_basis = 0;
+    double* cand = (double*)malloc(sizeof(double) * (m ? m : 1));
+    for (size_t j = from; j < r; ++j) {
+        for (; next_basis <= m; ++next_basis) {
+            if (next_basis == m) {
+                free(cand);
+                return -1;
+            }
+            memset(cand, 0, sizeof(double) * m);
+            cand[next_basis] = 1.0;
+            for (int pass = 0; pass < 2; ++pass) { /* twice-is-enough Gram-Schmidt */
+                for (size_t c = 0; c < j; ++c) {
+                    double dot = 0.0;
+                    for (size_t i = 0; i < m; ++i) dot += cand[i] * u[i * r + c];
+                    for (size_t i = 0; i < m; ++i) cand[i] -= dot * u[i * r + c];
+                }
+            }
+            double nrm = 0.0;
+            for (size_t i = 0; i < m; ++i) nrm += cand[i] * cand[i];
+            nrm = sqrt(nrm);
+            if (nrm > 0.5) {
+                for (size_t i = 0; i < m; ++i) u[i * r + j] = cand[i] / nrm;
+                ++next_basis;
+                break;
+            }
+        }
+    }
+    free(cand);
+    return 0;
+}
+
+/* detail::jacobi_factor (decomp.hpp:71-109): one-sided cyclic Jacobi on w (m×n,
+ * m >= n), right rotations accumulated into v (n×n); -1 when the cap is hit */
+static int jacobi_factor(double* w, size_t m, size_t n, double* v, size_t max_sweeps) {
+    const double tol = 1e-15;
+    const double null_sq = orc_frobenius_sq(w, m * n) * 1e-30;
+    for (size_t sweep = 0; sweep < max_sweeps; ++sweep) {
+        int rotated = 0;
+        for (size_t p = 0; p + 1 < n; ++p) {
+            for (size_t q = p + 1; q < n; ++q) {
+                double app = 0.0, aqq = 0.0, apq = 0.0;
+                for (size_t i = 0; i < m; ++i) {
+                    double wp = w[i * n + p], wq = w[i * n + q];
+                    app += wp * wp;
+                    aqq += wq * wq;
+                    apq += wp * wq;
+                }
+                if (app <= null_sq || aqq <= null_sq) continue;
+                if (fabs(apq) <= tol * sqrt(app * aqq)) continue;
+                rotated = 1;
+                double zeta = (aqq - app) / (2.0 * apq);
+                double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                double c = 1.0 / sqrt(1.0 + t * t);
+                double s = c * t;
+                for (size_t i = 0; i < m; ++i) {
+                    double wp = w[i * n + p], wq = w[i * n + q];
+                    w[i * n + p] = c * wp - s * wq;
+                    w[i * n + q] = s * wp + c * wq;
+                }
+                for (size_t i = 0; i < n; ++i) {
+                    double vp = v[i * n + p], vq = v[i * n + q];
+                    v[i * n + p] = c * vp - s * vq;
+                    v[i * n + q] = s * vp + c * vq;
+                }
+            }
+        }
+        if (!rotated) return 0;
+    }
+    return -1;
+}
+
+int orc_svd(const double* M, size_t rows, size_t cols, size_t max_sweeps, double* U_out,
+            double* sigma_out, double* V_out, size_t* rank_out, char* err) {
+    if (rows == 0 || cols == 0) return set_err(err, ORC_SHAPE_ERROR, "svd: empty matrix");
+    const int wide = rows < cols;
+    double* w = wide ? transposed(M, rows, cols) : dup(M, rows * cols);
+    const size_t m = wide ? cols : rows, n = wide ? rows : cols;
+    double* v = (double*)calloc(n * n, sizeof(double));
+    for (size_t i = 0; i < n; ++i) v[i * n + i] = 1.0;
+    if (jacobi_factor(w, m, n, v, max_sweeps) != 0) {
+        free(w);
+        free(v);
+        return set_err(err, ORC_DECOMPOSITION_ERROR, "svd: Jacobi sweeps exceeded cap");
+    }
+    double* sigma = (double*)malloc(sizeof(double) * n);
+    for (size_t j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (size_t i = 0; i < m; ++i) s += w[i * n + j] * w[i * n + j];
+        sigma[j] = sqrt(s);
+    }
+    size_t* order = (size_t*)malloc(sizeof(size_t) * n);
+    for (size_t j = 0; j < n; ++j) { /* std::stable_sort by sigma, descending */
+        size_t k = j;
+        while (k > 0 && sigma[order[k - 1]] < sigma[j]) {
+            order[k] = order[k - 1];
+            --k;
+        }
+        order[k] = j;
+    }
+    double* sv = (double*)malloc(sizeof(double) * n);
+    double* fU = (double*)calloc(m * n, sizeof(double));
+    double* fV = (double*)malloc(sizeof(double) * n * n);
+    for (size_t j = 0; j < n; ++j) {
+        size_t src = order[j];
+        sv[j] = sigma[src];
+        for (size_t i = 0; i < n; ++i) fV[i * n + j] = v[i * n + src];
+    }
+    const double cutoff = default_rank_tol(rows, cols, sv[0]);
+    size_t solid = 0;
+    for (size_t j = 0; j < n; ++j) {
+        size_t src = order[j];
+        if (sv[j] > cutoff) {
+            for (size_t i = 0; i < m; ++i) fU[i * n + j] = w[i * n + src] / sv[j];
+            solid = j + 1;
+        }
+    }
+    int rc = complete_orthonormal_columns(fU, m, n, solid);
+    if (rc == 0) {
+        /* tall: U = fU (rows×n), V = fV (cols×n); wide: swapped */
+        const double* u = wide ? fV : fU;
+        const double* vv = wide ? fU : fV;
+        if (U_out) memcpy(U_out, u, sizeof(double) * rows * n);
+        if (V_out) memcpy(V_out, vv, sizeof(double) * cols * n);
+        if (sigma_out) memcpy(sigma_out, sv, sizeof(double) * n);
+        if (rank_out) *rank_out = solid;
+    }
+    free(w); free(v); free(sigma); free(order); free(sv); free(fU); free(fV);
+    if (rc != 0) return set_err(err, ORC_DECOMPOSITION_ERROR, "svd: failed to complete orthonormal basis");
+    return ORC_OK;
+}
+
+int orc_pseudoinverse(const double* M, size_t rows, size_t cols, double rank_tol, double* P,
+                      char* err) {
+    if (rows == 0 || cols == 0) return set_err(err, ORC_SHAPE_ERROR, "svd: empty matrix");
+    const size_t r = rows < cols ? rows : cols;
+    double* U = (double*)malloc(sizeof(double) * rows * r);
+    double* V = (double*)malloc(sizeof(double) * cols * r);
+    double* sv = (double*)malloc(sizeof(double) * r);
+    int rc = orc_svd(M, rows, cols, 64, U, sv, V, NULL, err);
+    if (rc == ORC_OK) {
+        if (rank_tol < 0.0) rank_tol = default_rank_tol(rows, cols, sv[0]);
+        memset(P, 0, sizeof(double) * cols * rows);
+        for (size_t k = 0; k < r; ++k) {
+            double s = sv[k];
+            if (s <= rank_tol) continue;
+            double inv = 1.0 / s;
+            for (size_t i = 0; i < cols; ++i) {
+                double vik = V[i * r + k] * inv;
+                if (vik == 0.0) continue;
+                for (size_t j = 0; j < rows; ++j) P[i * rows + j] += vik * U[j * r + k];
+            }
+        }
+    }
+    free(U); free(V); free(sv);
+    return rc;
+}
+
+int orc_lu_solve(double* a, size_t n, double* b, size_t k, char* err) {
+    for (size_t col = 0; col < n; ++col) {
+        size_t piv = col;
+        for (size_t i = col + 1; i < n; ++i)
+            if (fabs(a[i * n + col]) > fabs(a[piv * n + col])) piv = i;
+        if (a[piv * n + col] == 0.0)
+            return set_err(err, ORC_DECOMPOSITION_ERROR, "lu_solve: singular matrix");
+        if (piv != col) {
+            for (size_t j = 0; j < n; ++j) {
+                double t = a[col * n + j]; a[col * n + j] = a[piv * n + j]; a[piv * n + j] = t;
+            }
+            for (size_t j = 0; j < k; ++j) {
+                double t = b[col * k + j]; b[col * k + j] = b[piv * k + j]; b[piv * k + j] = t;
+            }
+        }
+        double d = a[col * n + col];
+        for (size_t i = col + 1; i < n; ++i) {
+            double f = a[i * n + col] / d;
+            if (f == 0.0) continue;
+            for (size_t j = col; j < n; ++j) a[i * n + j] -= f * a[col * n + j];
+            for (size_t j = 0; j < k; ++j) b[i * k + j] -= f * b[col * k + j];
+        }
+    }
+    for (size_t col = n; col-- > 0;) {
+        double d = a[col * n + col];
+        for (size_t j = 0; j < k; ++j) {
+            double s = b[col * k + j];
+            for (size_t t = col + 1; t < n; ++t) s -= a[col * n + t] * b[t * k + j];
+            b[col * k + j] = s / d;
+        }
+    }
+    return ORC_OK;
+}
+
+/* detail::right_solve_sym (analysis.hpp:39-41): x·m⁻¹ = (m⁻¹ᵀ... via lu_solve(m, xᵀ))ᵀ;
+ * x is r×c, m c×c (consumed); result r×c in a new buffer */
+static double* right_solve_sym(const double* x, size_t r, size_t c, double* msq, int* rc,
+                               char* err) {
+    double* xt = transposed(x, r, c);
+    *rc = orc_lu_solve(msq, c, xt, r, err);
+    double* out = transposed(xt, c, r);
+    free(xt);
+    return out;
+}
+
+int orc_reference_solution(const double* A, size_t m, size_t p, const double* B, size_t q,
+                           size_t n, const double* C, double rank_tol, double* X, int* kind,
+                           double* residual_check, char* err) {
+    if (!m || !p || !q || !n) return set_err(err, ORC_SHAPE_ERROR, "svd: empty matrix");
+    const size_t ra = m < p ? m : p, rb = q < n ? q : n;
+    double* sa = (double*)malloc(sizeof(double) * ra);
+    double* sb = (double*)malloc(sizeof(double) * rb);
+    size_t rank_a = 0, rank_b = 0;
+    int rc = orc_svd(A, m, p, 64, NULL, sa, NULL, &rank_a, err);
+    if (rc == ORC_OK) rc = orc_svd(B, q, n, 64, NULL, sb, NULL, &rank_b, err);
+    if (rc != ORC_OK) {
+        free(sa); free(sb);
+        return rc;
+    }
+    if (rank_tol >= 0.0) { /* rank_of (analysis.hpp:54-61) */
+        rank_a = rank_b = 0;
+        for (size_t k = 0; k < ra; ++k) rank_a += sa[k] > rank_tol;
+        for (size_t k = 0; k < rb; ++k) rank_b += sb[k] > rank_tol;
+    }
+    free(sa); free(sb);
+    const int a_full_col = rank_a == p, a_full_row = rank_a == m;
+    const int b_full_col = rank_b == n, b_full_row = rank_b == q;
+    double* At = transposed(A, m, p);
+    double* Bt = transposed(B, q, n);
+    double* xs = NULL;
+    if (a_full_col && b_full_row) {
+        /* (AᵀA)⁻¹ Aᵀ C Bᵀ (BBᵀ)⁻¹ (analysis.hpp:70-75) */
+        double* ata = mm(At, p, m, A, p);
+        double* atc = mm(At, p, m, C, n);
+        double* y = mm(atc, p, n, Bt, q);
+        free(atc);
+        rc = orc_lu_solve(ata, p, y, q, err);
+        free(ata);
+        if (rc == ORC_OK) {
+            double* bbt = mm(B, q, n, Bt, q);
+            xs = right_solve_sym(y, p, q, bbt, &rc, err);
+            free(bbt);
+        }
+        free(y);
+        if (kind) *kind = ORC_REF_UNIQUE_FULL_RANK;
+    } else if (a_full_row && b_full_col) {
+        /* Aᵀ (AAᵀ)⁻¹ C (BᵀB)⁻¹ Bᵀ (analysis.hpp:76-81) */
+        double* aat = mm(A, m, p, At, m);
+        double* w = dup(C, m * n);
+        rc = orc_lu_solve(aat, m, w, n, err);
+        free(aat);
+        if (rc == ORC_OK) {
+            double* btb = mm(Bt, n, q, B, n);
+            double* z = right_solve_sym(w, m, n, btb, &rc, err);
+            free(btb);
+            if (rc == ORC_OK) {
+                double* atz = mm(At, p, m, z, n);
+                xs = mm(atz, p, n, Bt, q);
+                free(atz);
+            }
+            free(z);
+        }
+        free(w);
+        if (kind) *kind = ORC_REF_LEAST_NORM_FULL_ROW_COL;
+    } else {
+        double* Ap = (double*)malloc(sizeof(double) * p * m);
+        double* Bp = (double*)malloc(sizeof(double) * n * q);
+        rc = orc_pseudoinverse(A, m, p, rank_tol, Ap, err);
+        if (rc == ORC_OK) rc = orc_pseudoinverse(B, q, n, rank_tol, Bp, err);
+        if (rc == ORC_OK) {
+            double* apc = mm(Ap, p, m, C, n);
+            xs = mm(apc, p, n, Bp, q);
+            free(apc);
+        }
+        free(Ap); free(Bp);
+        if (kind) *kind = ORC_REF_LEAST_NORM_GENERAL;
+    }
+    free(At); free(Bt);
+    if (rc != ORC_OK) {
+        free(xs);
+        return rc;
+    }
+    /* residual_check = frobenius_dist(A·X*·B, C) (analysis.hpp:86-90) */
+    double* ax = mm(A, m, p, xs, q);
+    double* axb = mm(ax, m, q, B, n);
+    free(ax);
+    double d = 0.0;
+    for (size_t i = 0; i < m * n; ++i) {
+        double t = axb[i] - C[i];
+        d += t * t;
+    }
+    free(axb);
+    d = sqrt(d);
+    memcpy(X, xs, sizeof(double) * p * q);
+    free(xs);
+    if (residual_check) *residual_check = d;
+    if (d > 1e-8 * (1.0 + sqrt(orc_frobenius_sq(C, m * n)))) {
+        if (err) snprintf(err, 256, "reference_solution: system is not consistent (residual %f)", d);
+        return ORC_DOMAIN_ERROR;
+    }
+    return ORC_OK;
+}
+
+int orc_bk_limit(const double* A, size_t m, size_t p, const double* B, size_t q, size_t n,
+                 const double* C, const double* X0, double* out, char* err) {
+    if (!m || !p || !q || !n) return set_err(err, ORC_SHAPE_ERROR, "svd: empty matrix");
+    double* Ap = (double*)malloc(sizeof(double) * p * m);
+    double* Bp = (double*)malloc(sizeof(double) * n * q);
+    int rc = orc_pseudoinverse(A, m, p, -1.0, Ap, err);
+    if (rc == ORC_OK) rc = orc_pseudoinverse(B, q, n, -1.0, Bp, err);
+    if (rc == ORC_OK) {
+        double* apc = mm(Ap, p, m, C, n);
+        double* xs = mm(apc, p, n, Bp, q);
+        double* ax = mm(A, m, p, X0, q);
+        double* axb = mm(ax, m, q, B, n);
+        double* t = mm(Ap, p, m, axb, n);
+        double* proj = mm(t, p, n, Bp, q);
+        for (size_t i = 0; i < p * q; ++i) out[i] = xs[i] + (X0[i] - proj[i]);
+        free(apc); free(xs); free(ax); free(axb); free(t); free(proj);
+    }
+    free(Ap); free(Bp);
+    return rc;
+}
+
+int orc_rrn(const double* xk, const double* ref, size_t len, double* out, char* err) {
+    const double ref_sq = orc_frobenius_sq(ref, len);
+    if (ref_sq == 0.0) return set_err(err, ORC_DOMAIN_ERROR, "rrn: zero reference");
+    double d = 0.0;
+    for (size_t i = 0; i < len; ++i) {
+        double t = xk[i] - ref[i];
+        d += t * t;
+    }
+    *out = d / ref_sq;
+    return ORC_OK;
+}

@@ -31,7 +31,8 @@ enum {
     ORC_CONFIG_ERROR = 3,      /* axb::ConfigError */
     ORC_DIVERGENCE_ERROR = 4,  /* axb::DivergenceError{iteration,residual_norm} */
     ORC_INVARIANT_ERROR = 5,   /* axb::InvariantError */
-    ORC_CONVERGENCE_ERROR = 6  /* axb::ConvergenceError{last_estimate} */
+    ORC_CONVERGENCE_ERROR = 6, /* axb::ConvergenceError{last_estimate} */
+    ORC_DECOMPOSITION_ERROR = 9 /* axb::DecompositionError (errors.hpp:48-50) */
 };
 
 /* MethodTag (solver.hpp:16), AlphaRule (:68), StopRule::Kind (:80). */
@@ -153,6 +154,34 @@ void orc_solver_get_R(const orc_solver* s, double* out);
 void orc_solver_get_r_sq(const orc_solver* s, double* out);
 void orc_solver_get_a_sq(const orc_solver* s, double* out);
 void orc_solver_rng_state(const orc_solver* s, uint64_t out[4]);
+
+/* ------------------------------------------------------------------------
+ * Reference solutions: decomp.hpp svd / pseudoinverse / lu_solve
+ * and analysis.hpp reference_solution / bk_limit / rrn, dense operands.
+ * Errors: ORC_SHAPE_ERROR, ORC_DOMAIN_ERROR, ORC_DECOMPOSITION_ERROR; the
+ * message is copied to err (≥ 256 bytes) when err is non-NULL.
+ * ------------------------------------------------------------------------ */
+enum { ORC_REF_UNIQUE_FULL_RANK = 0, ORC_REF_LEAST_NORM_FULL_ROW_COL = 1,
+       ORC_REF_LEAST_NORM_GENERAL = 2 }; /* ReferenceCase (analysis.hpp:18) */
+
+/* svd(M, max_sweeps) (decomp.hpp:113-157): r = min(rows, cols); U rows×r,
+ * sigma r (nonincreasing), V cols×r, all row-major; any output may be NULL. */
+int orc_svd(const double* M, size_t rows, size_t cols, size_t max_sweeps, double* U,
+            double* sigma, double* V, size_t* numeric_rank, char* err);
+/* pseudoinverse(M, rank_tol) (decomp.hpp:161-177): P is cols×rows. */
+int orc_pseudoinverse(const double* M, size_t rows, size_t cols, double rank_tol, double* P,
+                      char* err);
+/* lu_solve(a, b) (decomp.hpp:249-279): a n×n, b n×k, both overwritten; b = a⁻¹b. */
+int orc_lu_solve(double* a, size_t n, double* b, size_t k, char* err);
+/* reference_solution(A, B, C, rank_tol) (analysis.hpp:48-91): X p×q. */
+int orc_reference_solution(const double* A, size_t m, size_t p, const double* B, size_t q,
+                           size_t n, const double* C, double rank_tol, double* X, int* kind,
+                           double* residual_check, char* err);
+/* bk_limit(A, B, C, X0) (analysis.hpp:95-104): out p×q. */
+int orc_bk_limit(const double* A, size_t m, size_t p, const double* B, size_t q, size_t n,
+                 const double* C, const double* X0, double* out, char* err);
+/* rrn(xk, reference) (analysis.hpp:107-111). */
+int orc_rrn(const double* xk, const double* ref, size_t len, double* out, char* err);
 
 #ifdef __cplusplus
 }

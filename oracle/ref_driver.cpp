@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include "axb/analysis.hpp"
+#include "axb/decomp.hpp"
 #include "axb/rng.hpp"
 #include "axb/solver.hpp"
 
@@ -108,6 +110,9 @@ int guarded(Handle* h, F&& f) {
     } catch (const ConvergenceError& e) {
         h->err = e.what();
         return 6;
+    } catch (const DecompositionError& e) {
+        h->err = e.what();
+        return 9;
     } catch (const std::exception& e) {
         h->err = e.what();
         return 99;
@@ -283,5 +288,56 @@ void ref_solver_get_a_sq(void* hp, double* out) {
     std::memcpy(out, v.data(), sizeof(double) * v.size());
 }
 const char* ref_solver_last_error(void* hp) { return static_cast<Handle*>(hp)->err.c_str(); }
+
+// ---- analysis.hpp / decomp.hpp: svd, pseudoinverse,
+// reference_solution, bk_limit, rrn on dense operands; errors in ref_analysis_error().
+static thread_local Handle g_an;
+
+const char* ref_analysis_error() { return g_an.err.c_str(); }
+
+int ref_svd(const double* M, size_t rows, size_t cols, size_t max_sweeps, double* U,
+            double* sigma, double* V, size_t* rank) {
+    return guarded(&g_an, [&] {
+        SvdFactors f = svd(mk(M, rows, cols), max_sweeps);
+        if (U) std::memcpy(U, f.U.data().data(), sizeof(double) * f.U.size());
+        if (V) std::memcpy(V, f.V.data().data(), sizeof(double) * f.V.size());
+        if (sigma)
+            std::memcpy(sigma, f.singular_values.data(),
+                        sizeof(double) * f.singular_values.size());
+        if (rank) *rank = f.numeric_rank;
+    });
+}
+
+int ref_pseudoinverse(const double* M, size_t rows, size_t cols, double rank_tol, double* P) {
+    return guarded(&g_an, [&] {
+        DenseMatrix p = pseudoinverse(mk(M, rows, cols), rank_tol);
+        std::memcpy(P, p.data().data(), sizeof(double) * p.size());
+    });
+}
+
+int ref_reference_solution(const double* A, size_t m, size_t p, const double* B, size_t q,
+                           size_t n, const double* C, double rank_tol, double* X, int* kind,
+                           double* residual_check) {
+    return guarded(&g_an, [&] {
+        Matrix a = mk(A, m, p), b = mk(B, q, n);
+        ReferenceSolution r = reference_solution(a, b, mk(C, m, n), rank_tol);
+        std::memcpy(X, r.X_star.data().data(), sizeof(double) * r.X_star.size());
+        if (kind) *kind = static_cast<int>(r.kind);
+        if (residual_check) *residual_check = r.residual_check;
+    });
+}
+
+int ref_bk_limit(const double* A, size_t m, size_t p, const double* B, size_t q, size_t n,
+                 const double* C, const double* X0, double* out) {
+    return guarded(&g_an, [&] {
+        Matrix a = mk(A, m, p), b = mk(B, q, n);
+        DenseMatrix l = bk_limit(a, b, mk(C, m, n), mk(X0, p, q));
+        std::memcpy(out, l.data().data(), sizeof(double) * l.size());
+    });
+}
+
+int ref_rrn(const double* xk, const double* ref, size_t rows, size_t cols, double* out) {
+    return guarded(&g_an, [&] { *out = rrn(mk(xk, rows, cols), mk(ref, rows, cols)); });
+}
 
 }  // extern "C"

@@ -13,6 +13,9 @@ Fixtures (all produced by the reference's own code paths):
                  GRBK / RGRBK(0.25) / MWRBK / RBK / BK, solver seed 42, refresh 1000:
                  iterations, α, final RRN, the run() trace's selected rows, final X
   kat_small.npz  test_solver.cpp-style small systems: 30-step row sequences and X
+  analysis.npz   decomp.hpp svd / pseudoinverse and analysis.hpp reference_solution /
+                 bk_limit on the shapes test_decomp.cpp / test_analysis.cpp use
+                 (inputs from numpy default_rng, stored with the outputs)
 """
 import hashlib
 import os
@@ -78,7 +81,73 @@ def main():
             out[f"s{k}_{name}_alpha"] = s.alpha
         out[f"s{k}_shape"] = np.array([m, p, q, n, seed])
     np.savez_compressed(os.path.join(HERE, "kat_small.npz"), **out)
+    analysis_fixtures(ref)
+
+
+def analysis_cases(seed=2408):
+    """Inputs for analysis.npz: (name, A, B, C, X0, rank_tol)."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal
+
+    def stacked(rows, cols):  # stack_rows_twice (test_analysis.cpp:12-20): rank `rows`
+        h = g((rows, cols))
+        return np.vstack([h, h])
+
+    cases = []
+    I4 = np.eye(4)
+    cases.append(("identity", I4, I4, g((4, 4)), np.zeros((4, 4)), -1.0))
+    for name, A, B in [("unique", g((6, 3)), g((3, 6))),            # kind 0
+                       ("rowcol", g((3, 7)), g((8, 4))),            # kind 1
+                       ("general", stacked(2, 5), g((4, 6))),       # kind 2
+                       ("medium", g((48, 32)), g((24, 40))),        # kind 0
+                       ("medium_def", stacked(10, 24), g((16, 30)))]:  # kind 2
+        X = g((A.shape[1], B.shape[0]))
+        cases.append((name, A, B, A @ X @ B, g(X.shape), -1.0))
+    A = stacked(2, 5)
+    B = g((4, 6))
+    cases.append(("general_tol", A, B, A @ g((5, 4)) @ B, g((5, 4)), 1e-6))
+    cases.append(("inconsistent", stacked(2, 4), g((3, 5)), g((4, 5)), np.zeros((4, 3)), -1.0))
+    return cases
+
+
+def svd_cases(seed=2409):
+    rng = np.random.default_rng(seed)
+    out = [("diag", np.array([[2.0, 0.0], [0.0, 0.0]]))]
+    for r, c in [(8, 5), (5, 8), (7, 7), (12, 4), (33, 20)]:
+        out.append((f"u{r}x{c}", rng.uniform(-1.0, 1.0, (r, c))))
+    h = rng.uniform(-1.0, 1.0, (9, 3))
+    out.append(("dupcols", np.hstack([h, h])))  # rank 3 (test_decomp.cpp:59-69)
+    return out
+
+
+def analysis_fixtures(ref):
+    an = O.Analysis(ref)
+    out = {}
+    for name, M in svd_cases():
+        U, s, V, rank = an.svd(M)
+        out.update({f"svd_{name}_M": M, f"svd_{name}_U": U, f"svd_{name}_s": s,
+                    f"svd_{name}_V": V, f"svd_{name}_rank": rank,
+                    f"svd_{name}_pinv": an.pseudoinverse(M)})
+    for name, A, B, Cm, X0, tol in analysis_cases():
+        out.update({f"rs_{name}_A": A, f"rs_{name}_B": B, f"rs_{name}_C": Cm,
+                    f"rs_{name}_X0": X0, f"rs_{name}_tol": tol})
+        try:
+            X, kind, res = an.reference_solution(A, B, Cm, tol)
+            out.update({f"rs_{name}_X": X, f"rs_{name}_kind": kind, f"rs_{name}_res": res,
+                        f"rs_{name}_code": 0})
+        except O.OracleError as e:
+            out.update({f"rs_{name}_code": e.code, f"rs_{name}_msg": str(e)})
+        try:
+            out[f"rs_{name}_bk"] = an.bk_limit(A, B, Cm, X0)
+        except O.OracleError:
+            pass
+    out["names"] = np.array([c[0] for c in analysis_cases()])
+    out["svd_names"] = np.array([c[0] for c in svd_cases()])
+    np.savez_compressed(os.path.join(HERE, "analysis.npz"), **out)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["analysis"]:
+        analysis_fixtures(O.ref())
+    else:
+        main()

@@ -430,3 +430,97 @@ class Rng(C.Structure):
 
     _fields_ = [("s", C.c_uint64 * 4), ("seed", C.c_uint64), ("spare", C.c_double),
                 ("has_spare", C.c_int32)]
+
+
+# ---------------------------------------------------------------------------
+# Reference solutions (decomp.hpp / analysis.hpp)
+
+UNIQUE_FULL_RANK, LEAST_NORM_FULL_ROW_COL, LEAST_NORM_GENERAL = range(3)
+SHAPE_ERROR, DOMAIN_ERROR = 1, 2
+DECOMPOSITION_ERROR = 9
+
+
+class Analysis:
+    """svd / pseudoinverse / reference_solution / bk_limit / rrn through either
+    the restatement (``Analysis(oracle())``) or the reference (``Analysis(ref())``)."""
+
+    def __init__(self, lib):
+        self.lib = lib
+        self.is_ref = isinstance(lib, RefLib)
+        S, d = C.c_size_t, C.c_double
+        pre = "ref_" if self.is_ref else "orc_"
+        L = lib.lib
+
+        def f(name, args):
+            fn = getattr(L, pre + name)
+            fn.restype = C.c_int
+            fn.argtypes = args + ([] if self.is_ref else [C.c_char_p])
+            return fn
+
+        self._svd = f("svd", [_dp, S, S, S, _dp, _dp, _dp, C.POINTER(S)])
+        self._pinv = f("pseudoinverse", [_dp, S, S, d, _dp])
+        self._refsol = f("reference_solution",
+                         [_dp, S, S, _dp, S, S, _dp, d, _dp, C.POINTER(C.c_int), _dp])
+        self._bk = f("bk_limit", [_dp, S, S, _dp, S, S, _dp, _dp, _dp])
+        if self.is_ref:
+            self._rrn = f("rrn", [_dp, _dp, S, S, _dp])
+            L.ref_analysis_error.restype = C.c_char_p
+        else:
+            self._rrn = f("rrn", [_dp, _dp, S, _dp])
+
+    def _call(self, fn, *args):
+        if self.is_ref:
+            code = fn(*args)
+            msg = self.lib.lib.ref_analysis_error().decode() if code else ""
+        else:
+            buf = C.create_string_buffer(256)
+            code = fn(*args, buf)
+            msg = buf.value.decode()
+        if code:
+            raise OracleError(code, msg)
+
+    @staticmethod
+    def _c(a):
+        return np.ascontiguousarray(a, dtype=np.float64)
+
+    def svd(self, M, max_sweeps=64):
+        M = self._c(M)
+        rows, cols = M.shape
+        r = min(rows, cols)
+        U, s, V = np.empty((rows, r)), np.empty(r), np.empty((cols, r))
+        rank = C.c_size_t()
+        self._call(self._svd, _ptr(M), rows, cols, max_sweeps, _ptr(U), _ptr(s), _ptr(V),
+                   C.byref(rank))
+        return U, s, V, rank.value
+
+    def pseudoinverse(self, M, rank_tol=-1.0):
+        M = self._c(M)
+        P = np.empty((M.shape[1], M.shape[0]))
+        self._call(self._pinv, _ptr(M), M.shape[0], M.shape[1], rank_tol, _ptr(P))
+        return P
+
+    def reference_solution(self, A, B, Cm, rank_tol=-1.0):
+        A, B, Cm = self._c(A), self._c(B), self._c(Cm)
+        (m, p), (q, n) = A.shape, B.shape
+        X = np.empty((p, q))
+        kind, res = C.c_int(), C.c_double()
+        self._call(self._refsol, _ptr(A), m, p, _ptr(B), q, n, _ptr(Cm), rank_tol, _ptr(X),
+                   C.byref(kind), C.byref(res))
+        return X, kind.value, res.value
+
+    def bk_limit(self, A, B, Cm, X0):
+        A, B, Cm, X0 = self._c(A), self._c(B), self._c(Cm), self._c(X0)
+        (m, p), (q, n) = A.shape, B.shape
+        out = np.empty((p, q))
+        self._call(self._bk, _ptr(A), m, p, _ptr(B), q, n, _ptr(Cm), _ptr(X0), _ptr(out))
+        return out
+
+    def rrn(self, xk, reference):
+        xk, reference = self._c(xk), self._c(reference)
+        out = C.c_double()
+        if self.is_ref:
+            self._call(self._rrn, _ptr(xk), _ptr(reference), xk.shape[0], xk.shape[1],
+                       C.byref(out))
+        else:
+            self._call(self._rrn, _ptr(xk), _ptr(reference), xk.size, C.byref(out))
+        return out.value
