@@ -40,7 +40,8 @@ typedef enum {
     AXB_INVARIANT_ERROR = 5,   /* axb::InvariantError   errors.hpp:70-72 */
     AXB_CONVERGENCE_ERROR = 6, /* axb::ConvergenceError errors.hpp:53-57 */
     AXB_CUDA_ERROR = 7,        /* device / runtime failure (no reference analogue) */
-    AXB_CAPACITY_ERROR = 8     /* axb::CapacityError    errors.hpp:25-27 (HBM exhausted) */
+    AXB_CAPACITY_ERROR = 8,    /* axb::CapacityError    errors.hpp:25-27 (HBM exhausted) */
+    AXB_DECOMPOSITION_ERROR = 9 /* axb::DecompositionError errors.hpp:48-50 */
 } axb_status;
 
 /* MethodTag (solver.hpp:16) */
@@ -229,6 +230,42 @@ int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]);
 /* Enable per-kernel CUDA-event timing of K2 inside steps()/run() (adds events to
  * the captured graph; off by default). */
 int axb_solver_set_profiling(axb_solver* s, int32_t on);
+
+/* ------------------------------------------------------------------------
+ * Reference solutions on the device — the X* producers of
+ * analysis.hpp / decomp.hpp, one-sided Jacobi in round-robin order plus DMMA
+ * GEMMs (csrc/axb_analysis.cu).  Host pointers in and out, dense row-major;
+ * `device` is the CUDA ordinal.  Failures return the status of the reference's
+ * exception and leave the message in axb_last_create_error().
+ * ------------------------------------------------------------------------ */
+/* ReferenceCase (analysis.hpp:18) */
+enum { AXB_REF_UNIQUE_FULL_RANK = 0, AXB_REF_LEAST_NORM_FULL_ROW_COL = 1,
+       AXB_REF_LEAST_NORM_GENERAL = 2 };
+
+/* svd(M, max_sweeps) — decomp.hpp:113-157.  r = min(rows, cols): sigma[r]
+ * nonincreasing, U rows×r, V cols×r (any output may be NULL), numeric_rank at
+ * the cutoff 8·max(rows,cols)·σ_max·2⁻⁵² (:30-33).  ShapeError on an empty M,
+ * DecompositionError when max_sweeps sweeps do not converge. */
+int axb_svd(const double* M, uint64_t rows, uint64_t cols, uint64_t max_sweeps, int32_t device,
+            double* U, double* sigma, double* V, uint64_t* numeric_rank);
+/* pseudoinverse(M, rank_tol) — decomp.hpp:161-177; P is cols×rows; rank_tol < 0
+ * selects the default cutoff. */
+int axb_pseudoinverse(const double* M, uint64_t rows, uint64_t cols, double rank_tol,
+                      int32_t device, double* P);
+/* reference_solution(A, B, C, rank_tol) — analysis.hpp:48-91: X p×q, kind one of
+ * AXB_REF_*, residual_check = ‖A·X·B − C‖_F; DomainError when the residual
+ * exceeds 1e-8·(1 + ‖C‖_F) (X is not written then). */
+int axb_reference_solution(const axb_matrix* A, const axb_matrix* B, const double* C,
+                           double rank_tol, int32_t device, double* X, int32_t* kind,
+                           double* residual_check);
+/* bk_limit(A, B, C, X0) — analysis.hpp:95-104: A⁺CB⁺ + X0 − A⁺AX0BB⁺, p×q. */
+int axb_bk_limit(const axb_matrix* A, const axb_matrix* B, const double* C, const double* X0,
+                 int32_t device, double* X);
+/* rrn(Xk, reference) — analysis.hpp:107-111 (squared relative error). */
+int axb_rrn(const double* Xk, const double* ref, uint64_t len, int32_t device, double* out);
+/* Jacobi sweeps of the last call's factorisations on this thread (A, B) and its
+ * device time in ms (CUDA events, inputs already resident). */
+int axb_analysis_stats(uint64_t sweeps[2], double* device_ms);
 
 #ifdef __cplusplus
 }

@@ -5,10 +5,12 @@ Drop-in for the per-iteration path of the reference's ``axb::Solver``
 ME-RBK / ME-BK baselines, on hand-written sm_100a CUDA behind the C-ABI in
 ``include/axb_b200.h``.  See DESIGN.md.
 """
-from . import errors
+from . import analysis, errors
 from ._lib import LIB_PATH, device_available
-from .errors import (CapacityError, ConfigError, ConvergenceError, CudaError, DivergenceError,
-                     DomainError, Error, InvariantError, ShapeError)
+from .analysis import (ReferenceCase, ReferenceSolution, SvdFactors, bk_limit, pseudoinverse,
+                       reference_solution, rrn, svd)
+from .errors import (CapacityError, ConfigError, ConvergenceError, CudaError, DecompositionError,
+                     DivergenceError, DomainError, Error, InvariantError, ShapeError)
 from .solver import (AlphaRule, Method, MethodTag, Options, SolveConfig, SolveReport, Solver,
                      StopRule, Terminated, TracePoint, kDriftGuardScale, solve, trace_point_due)
 
@@ -16,5 +18,7 @@ __all__ = [
     "AlphaRule", "Method", "MethodTag", "Options", "SolveConfig", "SolveReport", "Solver",
     "StopRule", "Terminated", "TracePoint", "kDriftGuardScale", "solve", "trace_point_due",
     "Error", "ShapeError", "DomainError", "ConfigError", "DivergenceError", "InvariantError",
-    "ConvergenceError", "CapacityError", "CudaError", "errors", "LIB_PATH", "device_available",
+    "ConvergenceError", "CapacityError", "CudaError", "DecompositionError", "errors", "LIB_PATH",
+    "device_available", "analysis", "ReferenceCase", "ReferenceSolution", "SvdFactors",
+    "reference_solution", "bk_limit", "rrn", "svd", "pseudoinverse",
 ]

@@ -146,6 +146,17 @@ SIGNATURES = [
     ("axb_solver_kernel_times", C.c_int, [_H, _dp]),
     ("axb_solver_debug_state", C.c_int, [_H, _u64p]),
     ("axb_solver_set_profiling", C.c_int, [_H, C.c_int32]),
+    # reference solutions
+    ("axb_svd", C.c_int, [_dp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, _dp, _dp, _dp,
+                          _u64p]),
+    ("axb_pseudoinverse", C.c_int, [_dp, C.c_uint64, C.c_uint64, C.c_double, C.c_int32, _dp]),
+    ("axb_reference_solution", C.c_int,
+     [C.POINTER(AxbMatrix), C.POINTER(AxbMatrix), _dp, C.c_double, C.c_int32, _dp,
+      C.POINTER(C.c_int32), _dp]),
+    ("axb_bk_limit", C.c_int,
+     [C.POINTER(AxbMatrix), C.POINTER(AxbMatrix), _dp, _dp, C.c_int32, _dp]),
+    ("axb_rrn", C.c_int, [_dp, _dp, C.c_uint64, C.c_int32, _dp]),
+    ("axb_analysis_stats", C.c_int, [_u64p, _dp]),
 ]
 
 _lib = None

@@ -12,7 +12,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ["axb_iter.cu", "axb_gemm.cu", "axb_solver.cu"]
+SOURCES = ["axb_iter.cu", "axb_gemm.cu", "axb_solver.cu", "axb_analysis.cu"]
 OUT = os.path.join(PKG, "libaxb_b200.so")
 
 NVCC_FLAGS = [

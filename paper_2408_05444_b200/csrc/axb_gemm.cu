@@ -271,10 +271,12 @@ __global__ void k_mirror_lower(double* D, long long nn, long long ld) {
 template <bool BT, bool V>
 void launch_t(const GemmArgs& g, cudaStream_t s) {
     const size_t smem = sizeof(double) * (size_t)STAGES * (A_STAGE + B_STAGE);
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};  // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
         cudaFuncSetAttribute(k_dgemm<BT, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
     k_dgemm<BT, V><<<grid, THREADS, smem, s>>>(g);

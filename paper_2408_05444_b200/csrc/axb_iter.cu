@@ -1952,10 +1952,12 @@ void launch_zx(const Params& P, cudaStream_t s) {
 void launch_r(const Params& P, cudaStream_t s, bool update) {
     if (P.r_tma) {
         const size_t smem = tma_smem_bytes(P);
-        static size_t attr_set = 0;
-        if (attr_set < smem) {  // opt in up to (device limit − static smem)
-            int dev = 0, optin = 0;
-            cudaGetDevice(&dev);
+        static size_t attr_set[64] = {};  // function attributes are per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        size_t& done = attr_set[dev & 63];
+        if (done < smem) {  // opt in up to (device limit − static smem)
+            int optin = 0;
             cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
             cudaFuncAttributes fa{};
             cudaFuncGetAttributes(&fa, k_r_tma<true>);
@@ -1972,7 +1974,7 @@ void launch_r(const Params& P, cudaStream_t s, bool update) {
             cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             cudaFuncSetAttribute(k_yg, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             cudaFuncSetAttribute(k_zx, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-            attr_set = (size_t)dyn;
+            done = (size_t)dyn;
         }
         if (update) launch_pdl(k_r_tma<true>, P.r_grid, kTmaThreads, smem, s, P);
         else k_r_tma<false><<<P.r_grid, kTmaThreads, smem, s>>>(P);

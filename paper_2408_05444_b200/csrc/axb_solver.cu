@@ -1334,6 +1334,15 @@ int expand(const axb_matrix* M, std::vector<double>& out, const char* name) {
 }
 }  // namespace
 
+extern "C++" {
+namespace axb_dev {  // shared with axb_analysis.cu
+std::string& handleless_error() { return g_create_err; }
+int expand_matrix(const axb_matrix* M, std::vector<double>& out, const char* name) {
+    return expand(M, out, name);
+}
+}  // namespace axb_dev
+}
+
 int axb_solver_create_ex(const axb_matrix* A, const axb_matrix* B, const double* C,
                          const double* X0, const axb_config* cfg, const axb_options* opt,
                          axb_solver** out) {

@@ -42,6 +42,10 @@ class DivergenceError(Error):
         self.residual_norm = residual_norm
 
 
+class DecompositionError(Error):
+    """errors.hpp:48-50 — Jacobi sweep cap, basis completion, singular LU."""
+
+
 class InvariantError(Error):
     """errors.hpp:70-72."""
 
@@ -59,6 +63,7 @@ _BY_CODE = {
     6: ConvergenceError,
     7: CudaError,
     8: CapacityError,
+    9: DecompositionError,
 }
 
 

@@ -22,6 +22,7 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
+from .analysis import reference_solution
 from .errors import ConfigError, DivergenceError
 from .solver import AlphaRule, Method, MethodTag, Options, SolveConfig, Solver, StopRule, Terminated
 
@@ -45,7 +46,7 @@ class BenchProblem:
     A: np.ndarray
     B: np.ndarray
     C: np.ndarray
-    X_star: Optional[np.ndarray] = None  # reference solution for solution_rrn stopping
+    X_star: Optional[np.ndarray] = None  # solution_rrn reference; None → device reference_solution
 
 
 @dataclass
@@ -82,6 +83,15 @@ def benchmark(problems: List[BenchProblem], methods: List[Method],
         raise ConfigError("benchmark: trials must be >= 1")
     for m in methods:
         m.validate()
+    # per-problem references, as the reference harness computes them up front
+    # (analysis.hpp:261-264) — on the device here
+    references = []
+    for i, pb in enumerate(problems):
+        if pb.X_star is not None:
+            references.append(pb.X_star)
+        else:
+            dev = opt.devices[i % len(opt.devices)]
+            references.append(reference_solution(pb.A, pb.B, pb.C, device=dev).X_star)
     tasks = [(p, mi, t) for p in range(len(problems)) for mi in range(len(methods))
              for t in range(opt.trials)]
     outcomes = [None] * len(tasks)
@@ -90,9 +100,7 @@ def benchmark(problems: List[BenchProblem], methods: List[Method],
         p, mi, t = tasks[idx]
         pb = problems[p]
         if opt.stop_kind == StopRule.Kind.SolutionRrn:
-            if pb.X_star is None:
-                raise ConfigError(f"problem {pb.id}: solution_rrn stopping needs X_star")
-            stop = StopRule.solution_rrn(opt.tol, pb.X_star)
+            stop = StopRule.solution_rrn(opt.tol, references[p])
         else:
             stop = StopRule.residual_rel(opt.tol)
         cfg = SolveConfig(method=methods[mi], alpha_rule=opt.alpha_rule,
