@@ -146,6 +146,7 @@ void launch_coldot(const double* M, long long rows, long long cols, const double
 void launch_power_step(const double* v_in, const double* w, double* v_out, long long dim,
                        double* out2, cudaStream_t s);
 void launch_fill(double* p, long long n, double v, cudaStream_t s);
+constexpr int kZxWarps = 8;  // warps per k_zx CTA (X rows per CTA)
 void launch_power_step2(double* v, const double* w, long long dim, double* ps, double tol,
                         double max_iter, cudaStream_t s);
 void launch_transpose(const double* in, long long rows, long long cols, double* out,

@@ -35,6 +35,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+static_assert(kWarps == kZxWarps, "k_zx geometry assumes kZxWarps warps per CTA");
 
 // Programmatic dependent launch: the iteration kernels are launched with the
 // programmatic-stream-serialization attribute so the next kernel's CTAs are
@@ -274,11 +275,13 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
     pdl_trigger();
     DevState* st = P.st;
     if (halted(st)) return;
-    const int nzc = P.z_nslab * P.z_nj;
     const int tid = threadIdx.x;
-    if ((int)blockIdx.x < nzc) {
-        const int slab = blockIdx.x % P.z_nslab;
-        const int jc = blockIdx.x / P.z_nslab;
+    // CTAs [0, x_ctas) update X (the larger units, dispatched first), the rest
+    // form z — small slab × row-chunk units that even out the tail
+    if ((int)blockIdx.x >= P.x_ctas) {
+        const int zb = (int)blockIdx.x - P.x_ctas;
+        const int slab = zb % P.z_nslab;
+        const int jc = zb / P.z_nslab;
         const long long j0 = (long long)jc * P.z_jrows;
         const long long j1 = min(P.q, j0 + P.z_jrows);
         const long long c = P.c0 + (long long)slab * (2 * kThreads) + 2 * tid;
@@ -288,10 +291,25 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
             if (c < cend) {
                 const double2* Bc = reinterpret_cast<const double2*>(P.B + c);
                 const long long ld2 = P.n >> 1;
-#pragma unroll 8
-                for (long long j = j0; j < j1; ++j) {
+                long long j = j0;
+                // 4 rows of B in flight per thread: all loads first, then the
+                // FMAs in row order (same sums as the one-row loop)
+                for (; j + 4 <= j1; j += 4) {
+                    double2 b[4];
+                    double yv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) b[u] = __ldcs(Bc + (j + u) * ld2);  // last use of B
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) yv[u] = __ldg(P.y + j + u);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        a0 += yv[u] * b[u].x;
+                        a1 += yv[u] * b[u].y;
+                    }
+                }
+                for (; j < j1; ++j) {
                     const double yj = __ldg(P.y + j);
-                    const double2 b = __ldcs(Bc + j * ld2);  // last use of B this iteration
+                    const double2 b = __ldcs(Bc + j * ld2);
                     a0 += yj * b.x;
                     a1 += yj * b.y;
                 }
@@ -326,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
         return;
     }
     // ---- X update (solver.hpp:272-290): one warp per row t of X ----
-    const int xb = blockIdx.x - nzc;
+    const int xb = blockIdx.x;
     const double* Ai = P.pack ? P.pack + P.n : P.A + (st->sel - P.row0) * P.p;
     const double coef = P.pack ? P.pack[P.n + P.p + 1] : st->coef;
     const bool track = P.Xref != nullptr;
@@ -343,8 +361,28 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
             const double2* y2 = reinterpret_cast<const double2*>(P.y);
             const double2* f2 = reinterpret_cast<const double2*>(rr);
             const long long h = q >> 1;
-#pragma unroll 4
-            for (long long k = lane; k < h; k += 32) {
+            long long k = lane;
+            // 2 segments per lane in flight: loads first, then update + store
+            for (; k + 32 < h; k += 64) {
+                double2 x[2], yy[2], rf[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    x[u] = x2[k + 32 * u];
+                    yy[u] = __ldg(y2 + k + 32 * u);
+                    if (track) rf[u] = __ldg(f2 + k + 32 * u);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    x[u].x = __dadd_rn(x[u].x, __dmul_rn(f, yy[u].x));
+                    x[u].y = __dadd_rn(x[u].y, __dmul_rn(f, yy[u].y));
+                    x2[k + 32 * u] = x[u];
+                    if (track) {
+                        const double d0 = x[u].x - rf[u].x, d1 = x[u].y - rf[u].y;
+                        acc += d0 * d0 + d1 * d1;
+                    }
+                }
+            }
+            for (; k < h; k += 32) {
                 double2 x = x2[k];
                 const double2 yy = __ldg(y2 + k);
                 x.x = __dadd_rn(x.x, __dmul_rn(f, yy.x));

@@ -580,17 +580,21 @@ struct axb_solver {
             const uint64_t blocks = (q + rpc(q) - 1) / rpc(q) + (gram_cached ? 0 : (m + rpc(m) - 1) / rpc(m));
             P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, blocks));
         }
-        P.z_nslab = (int)std::max<long long>(1, (P.c1 - P.c0 + 511) / 512);
-        const int ztarget = env_int("AXB_Z_TARGET", 148 * 8);  // z-part CTAs
-        int nj = (int)std::max<uint64_t>(1, std::min<uint64_t>((ztarget + P.z_nslab - 1) / P.z_nslab,
-                                                                (q + 7) / 8));
-        P.z_jrows = (int)((q + nj - 1) / nj);
-        P.z_nj = (int)((q + P.z_jrows - 1) / P.z_jrows);
-        P.x_ctas = (int)std::max<long long>(1, std::min<long long>(296, (P.x1r - P.x0r + 7) / 8));
+        {
+            // K4b+K5 in small units over several waves, so the tail evens out:
+            // X one row per warp (8 rows per CTA), z slabs of 512 columns ×
+            // chunks of AXB_Z_JROWS (128) rows of the B slice
+            const long long xrows = P.x1r - P.x0r;
+            P.x_ctas = (int)std::max<long long>(1, (xrows + kZxWarps - 1) / kZxWarps);
+            P.z_nslab = (int)std::max<long long>(1, (P.c1 - P.c0 + 511) / 512);
+            const long long jr = std::max(1, env_int("AXB_Z_JROWS", 128));
+            P.z_jrows = (int)std::min<long long>((long long)q, jr);
+            P.z_nj = (int)((q + P.z_jrows - 1) / P.z_jrows);
+        }
         zpart.alloc((size_t)P.z_nj * n, "zpart");
         zcnt.alloc(P.z_nslab, "zcnt");
         ck(cudaMemsetAsync(zcnt.p, 0, sizeof(unsigned) * P.z_nslab, stream), "zcnt");
-        xpart.alloc(2 * 1184, "xpart");
+        xpart.alloc(std::max<size_t>(2 * 1184, (size_t)P.x_ctas), "xpart");
         rrec.alloc(P.r_grid, "rrec");
         tr_row.alloc(trace_cap, "trace");
         forced.alloc(trace_cap, "forced rows");
