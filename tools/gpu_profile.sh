@@ -1,6 +1,6 @@
 # GPU round trip: parity tests, default bench, reference arm, launch list, one ncu --set full capture.
 set -x
-timeout 300 python -m pytest tests/ -x -q -m gpu > gpurun_out/pytest.log 2>&1; echo pytest_exit=$?; tail -3 gpurun_out/pytest.log
+timeout 1200 python -m pytest tests/ -x -q -m gpu > gpurun_out/pytest.log 2>&1; echo pytest_exit=$?; tail -3 gpurun_out/pytest.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_exit=$?
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_exit=$?
 B="python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e --no-tol"
