@@ -215,6 +215,16 @@ int axb_solver_get_a_sq(axb_solver* s, double* out);     /* m */
 int axb_solver_dims(const axb_solver* s, uint64_t dims[4]); /* m, p, q, n */
 
 /* ---- measurement hooks (bench.py) ---- */
+/* run() on many independent handles of one device at once — the benchmark
+ * pool's problem × method × trial sweep (analysis.hpp:255-356).
+ * Small systems (those on the persistent-kernel path) advance together in ONE
+ * launch per refresh segment, one CTA per system (k_persist_batch); larger ones
+ * run their own launches in turn.  Each handle's result is exactly what
+ * axb_solver_run would give: reps[i], x_outs[i] (may be NULL, or hold NULLs),
+ * statuses[i] (its status code; message in axb_solver_last_error(hs[i])).
+ * Returns AXB_OK unless the batch itself could not run. */
+int axb_solvers_run(axb_solver* const* hs, uint32_t count, axb_report* reps,
+                    double* const* x_outs, int32_t* statuses);
 /* Device time (ms) of the last run()/steps() loop, CUDA events on the solver's
  * stream, and the summed device time of the residual-update kernel (K2) inside
  * it, with its launch count. */

@@ -12,11 +12,13 @@ from .analysis import (ReferenceCase, ReferenceSolution, SvdFactors, bk_limit, p
 from .errors import (CapacityError, ConfigError, ConvergenceError, CudaError, DecompositionError,
                      DivergenceError, DomainError, Error, InvariantError, ShapeError)
 from .solver import (AlphaRule, Method, MethodTag, Options, SolveConfig, SolveReport, Solver,
-                     StopRule, Terminated, TracePoint, kDriftGuardScale, solve, trace_point_due)
+                     StopRule, Terminated, TracePoint, kDriftGuardScale, run_many, solve,
+                     trace_point_due)
 
 __all__ = [
     "AlphaRule", "Method", "MethodTag", "Options", "SolveConfig", "SolveReport", "Solver",
     "StopRule", "Terminated", "TracePoint", "kDriftGuardScale", "solve", "trace_point_due",
+    "run_many",
     "Error", "ShapeError", "DomainError", "ConfigError", "DivergenceError", "InvariantError",
     "ConvergenceError", "CapacityError", "CudaError", "DecompositionError", "errors", "LIB_PATH",
     "device_available", "analysis", "ReferenceCase", "ReferenceSolution", "SvdFactors",

@@ -164,6 +164,8 @@ void launch_sel1(const Params& P, cudaStream_t s, bool update);
 void launch_sel2(const Params& P, cudaStream_t s);
 // persistent cooperative batch kernel for small systems; returns a cudaError_t
 int launch_persist(const Params& P, cudaStream_t s);
+// many independent small systems, one CTA each (dPs: device array of Params)
+int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStream_t s);
 
 // ---- DMMA GEMM (axb_gemm.cu) ----
 // D = (Cin ? Cin − A·op(B) : A·op(B)); op(B) = B (K×N) or Bᵀ (B is N×K) when b_trans.

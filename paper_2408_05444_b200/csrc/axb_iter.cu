@@ -129,8 +129,10 @@ __device__ double rng_unit(unsigned long long* s) {
 
 // dot of a row with a vector by one warp; lane-strided partials then a
 // shuffle tree (deterministic).  vec2: both pointers 16-byte aligned, len even.
+// coherent_v: v is written inside the running kernel (R_i in the persistent
+// kernel), so it is read through L2 (ld.cg) instead of the non-coherent path.
 __device__ double warp_dot(const double* __restrict__ row, const double* __restrict__ v,
-                           long long len, int lane, bool vec2) {
+                           long long len, int lane, bool vec2, bool coherent_v = false) {
     double acc = 0.0;
     if (vec2) {
         const double2* r2 = reinterpret_cast<const double2*>(row);
@@ -139,15 +141,53 @@ __device__ double warp_dot(const double* __restrict__ row, const double* __restr
 #pragma unroll 4
         for (long long k = lane; k < h; k += 32) {
             const double2 a = __ldg(r2 + k);
-            const double2 b = __ldg(v2 + k);
+            const double2 b = coherent_v ? __ldcg(v2 + k) : __ldg(v2 + k);
             acc += a.x * b.x;
             acc += a.y * b.y;
         }
     } else {
 #pragma unroll 4
-        for (long long k = lane; k < len; k += 32) acc += __ldg(row + k) * __ldg(v + k);
+        for (long long k = lane; k < len; k += 32)
+            acc += __ldg(row + k) * (coherent_v ? __ldcg(v + k) : __ldg(v + k));
     }
     return warp_sum(acc);
+}
+
+// two row dots against one vector by one warp (row1 may be null): the vector
+// segment is loaded once for both rows; per row the same lane-strided partials
+// and shuffle tree as warp_dot.
+__device__ void warp_dot_pair(const double* __restrict__ row0, const double* __restrict__ row1,
+                              const double* __restrict__ v, long long len, int lane, bool vec2,
+                              bool coherent_v, double& out0, double& out1) {
+    double acc0 = 0.0, acc1 = 0.0;
+    const bool two = row1 != nullptr;
+    if (vec2) {
+        const double2* r0 = reinterpret_cast<const double2*>(row0);
+        const double2* r1 = reinterpret_cast<const double2*>(two ? row1 : row0);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const long long h = len >> 1;
+#pragma unroll 4
+        for (long long k = lane; k < h; k += 32) {
+            const double2 b = coherent_v ? __ldcg(v2 + k) : __ldg(v2 + k);
+            const double2 a = __ldg(r0 + k);
+            acc0 += a.x * b.x;
+            acc0 += a.y * b.y;
+            if (two) {
+                const double2 c = __ldg(r1 + k);
+                acc1 += c.x * b.x;
+                acc1 += c.y * b.y;
+            }
+        }
+    } else {
+#pragma unroll 4
+        for (long long k = lane; k < len; k += 32) {
+            const double b = coherent_v ? __ldcg(v + k) : __ldg(v + k);
+            acc0 += __ldg(row0 + k) * b;
+            if (two) acc1 += __ldg(row1 + k) * b;
+        }
+    }
+    out0 = warp_sum(acc0);
+    out1 = two ? warp_sum(acc1) : 0.0;
 }
 
 // ------------------------------------------------------------------------
@@ -429,8 +469,8 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
 // Writes *out_row; returns an axb_status (0 ok).  All threads must call it.
 struct SelShared {
     double scan[kThreads];
-    double redv[kWarps];
-    long long redi[kWarps];
+    double redv[32];  // per-warp slots for blocks of up to 1024 threads
+    long long redi[32];
     double target;
     double u;
     long long cand;
@@ -1421,9 +1461,25 @@ __global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
 //   and, at the end, the state.
 constexpr int kPersistThreads = 256;
 
-__global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
+// Execution groups of the persistent iteration: a cooperative grid working on
+// one system (k_persist), or one CTA owning a whole small system
+// (k_persist_batch, SURVEY §8 F3 — many independent solves in one launch).
+struct GridGroup {
+    cooperative_groups::grid_group g;
+    __device__ int rank() const { return (int)blockIdx.x; }
+    __device__ int size() const { return (int)gridDim.x; }
+    __device__ void sync() { g.sync(); }
+};
+struct SoloGroup {
+    __device__ int rank() const { return 0; }
+    __device__ int size() const { return 1; }
+    __device__ void sync() { __syncthreads(); }
+};
+
+template <class Grp, int kT>
+__device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
+    constexpr int kW = kT / 32;
+    constexpr int kSub = kT / kPersistThreads;  // 256-thread sub-blocks (z items)
     extern __shared__ double pscratch[];  // selection scratch: ⌈m/32⌉ group sums
     __shared__ DevState lst;
     __shared__ SelShared sh;
@@ -1431,8 +1487,8 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
     __shared__ long long redi[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long m = P.m, n = P.n, p = P.p, q = P.q;
-    const long long gw = (long long)blockIdx.x * kWarps + warp;  // global warp
-    const long long nw = (long long)gridDim.x * kWarps;
+    const long long gw = (long long)grid.rank() * kW + warp;  // global warp
+    const long long nw = (long long)grid.size() * kW;
     if (tid == 0) lst = *P.st;
     __syncthreads();
     for (;;) {
@@ -1463,24 +1519,44 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
         const double* Ri = P.R + sel * n;
         const double* Ai = P.A + sel * p;
         // ---- y = B·R_iᵀ (+ g = A·A_iᵀ) ----
-        const long long items = q + (P.G ? 0 : m);
-        for (long long it = gw; it < items; it += nw) {
-            if (it < q) {
-                const double a = warp_dot(P.B + it * n, Ri, n, lane, (n & 1) == 0);
-                if (lane == 0) P.y[it] = a;
-            } else {
-                const double a = warp_dot(P.A + (it - q) * p, Ai, p, lane, (p & 1) == 0);
-                if (lane == 0) P.g[it - q] = a;
+        // two rows per warp pass sharing the vector loads (y rows, then g rows)
+        {
+            double* const yo = P.y;
+            double* const go = P.g;
+            const double* const Bb = P.B;
+            const double* const Ab = P.A;
+            for (long long it = gw; it < q; it += 2 * nw) {
+                const long long it1 = it + nw;
+                double a0, a1;
+                warp_dot_pair(Bb + it * n, it1 < q ? Bb + it1 * n : nullptr, Ri, n, lane,
+                              (n & 1) == 0, true, a0, a1);
+                if (lane == 0) {
+                    yo[it] = a0;
+                    if (it1 < q) yo[it1] = a1;
+                }
+            }
+            if (!P.G) {
+                for (long long it = gw; it < m; it += 2 * nw) {
+                    const long long it1 = it + nw;
+                    double a0, a1;
+                    warp_dot_pair(Ab + it * p, it1 < m ? Ab + it1 * p : nullptr, Ai, p, lane,
+                                  (p & 1) == 0, false, a0, a1);
+                    if (lane == 0) {
+                        go[it] = a0;
+                        if (it1 < m) go[it1] = a1;
+                    }
+                }
             }
         }
         grid.sync();
         // ---- z = yᵀ·B, stage 1: (column slab × row chunk) partials; X update ----
         {
             const int items = P.z_nslab * P.z_nj;
-            for (int itm = blockIdx.x; itm < items; itm += gridDim.x) {
+            const int sub = tid / kPersistThreads, stid = tid % kPersistThreads;
+            for (int itm = grid.rank() * kSub + sub; itm < items; itm += grid.size() * kSub) {
                 const int slab = itm % P.z_nslab, jc = itm / P.z_nslab;
                 const long long j0 = (long long)jc * P.z_jrows, j1 = min(q, j0 + P.z_jrows);
-                const long long c = (long long)slab * (2 * kPersistThreads) + 2 * tid;
+                const long long c = (long long)slab * (2 * kPersistThreads) + 2 * stid;
                 double a0 = 0.0, a1 = 0.0;
                 if (c < n) {
 #pragma unroll 8
@@ -1496,10 +1572,13 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
             }
         }
         double xacc = 0.0;
+        const double* const yb = P.y;
+        double* const Xb = P.X;
+        const double* const Xrefb = P.Xref;
         for (long long t = gw; t < p; t += nw) {
             const double f = __dmul_rn(coef, Ai[t]);
-            double* xr = P.X + t * q;
-            const double* rr = P.Xref ? P.Xref + t * q : nullptr;
+            double* xr = Xb + t * q;
+            const double* rr = Xrefb ? Xrefb + t * q : nullptr;
             for (long long k0 = lane; k0 < q; k0 += 32 * 4) {
                 double xv[4], yv[4], rv[4];
 #pragma unroll
@@ -1507,7 +1586,7 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
                     const long long k = k0 + 32 * u;
                     if (k < q) {
                         xv[u] = xr[k];
-                        yv[u] = __ldcg(P.y + k);
+                        yv[u] = __ldcg(yb + k);
                         rv[u] = rr ? rr[k] : 0.0;
                     }
                 }
@@ -1526,54 +1605,146 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
             }
         }
         xacc = block_sum(xacc, red);
-        if (tid == 0) P.xpart[blockIdx.x] = xacc;
+        if (tid == 0) P.xpart[grid.rank()] = xacc;
         grid.sync();
         // ---- z stage 2: fixed-order combine of the row-chunk partials ----
-        for (long long c = (long long)blockIdx.x * kPersistThreads + tid; c < n;
-             c += (long long)gridDim.x * kPersistThreads) {
+        for (long long c = (long long)grid.rank() * kT + tid; c < n;
+             c += (long long)grid.size() * kT) {
             double a = 0.0;
             for (int k = 0; k < P.z_nj; ++k) a += __ldcg(P.zpart + (long long)k * n + c);
             P.z[c] = a;
         }
         grid.sync();
         // ---- R update + row norms (warp per row, static mapping) ----
+        // Pointers are hoisted into registers: P may live in shared memory
+        // (k_persist_batch) and a generic store could alias it otherwise.
         double wsum = 0.0, wmax = -INFINITY;
         long long warg = LLONG_MAX;
-        for (long long l = gw; l < m; l += nw) {
-            const double gl = P.G ? __ldcg(P.G + sel * m + l) : __ldcg(P.g + l);
-            double rs;
-            if (gl == 0.0) {  // R_l unchanged (sparse-G semantics, solver.hpp:294-295)
-                rs = __ldcg(P.r_sq + l);
-            } else {
-                const double f = __dmul_rn(coef, gl);
-                double* row = P.R + l * n;
-                double acc = 0.0;
-                for (long long k0 = lane; k0 < n; k0 += 32 * 4) {
-                    double rv[4], zv[4];
+        double* const Rb = P.R;
+        const double* const zb = P.z;
+        const double* const Gsel = P.G ? P.G + sel * m : nullptr;
+        const double* const gv = P.g;
+        double* const rsq = P.r_sq;
+        const double* const asq = P.a_sq;
+        auto coef_of = [&](long long l) { return Gsel ? __ldcg(Gsel + l) : __ldcg(gv + l); };
+        auto record = [&](long long l, double rs) {
+            wsum += rs;
+            const double as = asq[l];
+            if (as > 0.0) maxidx_merge(wmax, warg, __ddiv_rn(rs, as), l);
+        };
+        if ((n & 1) == 0) {
+            // two rows per warp pass (l, l + nw — the warp's own next row), 16-byte
+            // accesses, 4 segments per lane in flight: 12 loads outstanding per lane
+            const long long h = n >> 1;
+            const double2* z2 = reinterpret_cast<const double2*>(zb);
+            // the Gram coefficients of the warp's next 32 rows are fetched in one
+            // round trip (lane j holds row gw + (t0 + j)·nw) and shuffled out
+            double gpre = 0.0;
+            long long t = 0;  // index of l0 among the warp's rows
+            for (long long l0 = gw; l0 < m; l0 += 2 * nw, t += 2) {
+                if ((t & 31) == 0) {
+                    const long long lr = gw + (t + lane) * nw;
+                    gpre = lr < m ? coef_of(lr) : 0.0;
+                }
+                const long long l1 = l0 + nw;
+                const bool has1 = l1 < m;
+                const double g0 = __shfl_sync(0xffffffffu, gpre, (int)(t & 31));
+                const double g1v = __shfl_sync(0xffffffffu, gpre, (int)((t + 1) & 31));
+                const double g1 = has1 ? g1v : 0.0;
+                const bool up0 = g0 != 0.0, up1 = g1 != 0.0;  // sparse-G skip (:294-295)
+                const double f0 = __dmul_rn(coef, g0), f1 = __dmul_rn(coef, g1);
+                double2* row0 = reinterpret_cast<double2*>(Rb + l0 * n);
+                double2* row1 = reinterpret_cast<double2*>(Rb + (has1 ? l1 : l0) * n);
+                double acc0 = 0.0, acc1 = 0.0;
+                if (up0 || up1) {
+                    for (long long k0 = lane; k0 < h; k0 += 32 * 4) {
+                        double2 zv[4], r0[4], r1[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const long long k = k0 + 32 * u;
-                        if (k < n) {
-                            rv[u] = row[k];
-                            zv[u] = __ldcg(P.z + k);
+                        for (int u = 0; u < 4; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < h) {
+                                zv[u] = __ldcg(z2 + k);
+                                if (up0) r0[u] = row0[k];
+                                if (up1) r1[u] = row1[k];
+                            }
                         }
-                    }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const long long k = k0 + 32 * u;
-                        if (k < n) {
-                            const double r = __dsub_rn(rv[u], __dmul_rn(f, zv[u]));
-                            row[k] = r;
-                            acc += r * r;
+                        for (int u = 0; u < 4; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < h) {
+                                if (up0) {
+                                    double2 r;
+                                    r.x = __dsub_rn(r0[u].x, __dmul_rn(f0, zv[u].x));
+                                    r.y = __dsub_rn(r0[u].y, __dmul_rn(f0, zv[u].y));
+                                    row0[k] = r;
+                                    acc0 += r.x * r.x;
+                                    acc0 += r.y * r.y;
+                                }
+                                if (up1) {
+                                    double2 r;
+                                    r.x = __dsub_rn(r1[u].x, __dmul_rn(f1, zv[u].x));
+                                    r.y = __dsub_rn(r1[u].y, __dmul_rn(f1, zv[u].y));
+                                    row1[k] = r;
+                                    acc1 += r.x * r.x;
+                                    acc1 += r.y * r.y;
+                                }
+                            }
                         }
                     }
                 }
-                rs = warp_sum(acc);
-                if (lane == 0) P.r_sq[l] = rs;
+                double rs0, rs1 = 0.0;
+                if (up0) {
+                    rs0 = warp_sum(acc0);
+                    if (lane == 0) rsq[l0] = rs0;
+                } else {
+                    rs0 = __ldcg(rsq + l0);
+                }
+                if (has1) {
+                    if (up1) {
+                        rs1 = warp_sum(acc1);
+                        if (lane == 0) rsq[l1] = rs1;
+                    } else {
+                        rs1 = __ldcg(rsq + l1);
+                    }
+                }
+                record(l0, rs0);
+                if (has1) record(l1, rs1);
             }
-            wsum += rs;
-            const double as = P.a_sq[l];
-            if (as > 0.0) maxidx_merge(wmax, warg, __ddiv_rn(rs, as), l);
+        } else {
+            for (long long l = gw; l < m; l += nw) {
+                const double gl = coef_of(l);
+                double rs;
+                if (gl == 0.0) {  // R_l unchanged (sparse-G semantics, solver.hpp:294-295)
+                    rs = __ldcg(rsq + l);
+                } else {
+                    const double f = __dmul_rn(coef, gl);
+                    double* row = Rb + l * n;
+                    double acc = 0.0;
+                    for (long long k0 = lane; k0 < n; k0 += 32 * 4) {
+                        double rv[4], zv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < n) {
+                                rv[u] = row[k];
+                                zv[u] = __ldcg(zb + k);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < n) {
+                                const double r = __dsub_rn(rv[u], __dmul_rn(f, zv[u]));
+                                row[k] = r;
+                                acc += r * r;
+                            }
+                        }
+                    }
+                    rs = warp_sum(acc);
+                    if (lane == 0) rsq[l] = rs;
+                }
+                record(l, rs);
+            }
         }
         // per-CTA record: warp partials combined in warp order (fixed mapping)
         __syncthreads();
@@ -1586,11 +1757,11 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
         if (tid == 0) {
             double a = 0.0, mx = -INFINITY;
             long long ax = LLONG_MAX;
-            for (int w = 0; w < kWarps; ++w) {
+            for (int w = 0; w < kW; ++w) {
                 a += red[w];
                 maxidx_merge(mx, ax, sh.scan[w], redi[w]);
             }
-            P.rrec[blockIdx.x] = RowRecord{a, mx, ax, 0.0};
+            P.rrec[grid.rank()] = RowRecord{a, mx, ax, 0.0};
         }
         grid.sync();
         // ---- every CTA: reduce the records + the ‖X−X_ref‖² partials (block-
@@ -1598,7 +1769,7 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
         {
             double ps = 0.0, pe = 0.0, pm = -INFINITY;
             long long pa = LLONG_MAX;
-            for (int b = tid; b < (int)gridDim.x; b += kPersistThreads) {
+            for (int b = tid; b < grid.size(); b += kT) {
                 const double* rp = reinterpret_cast<const double*>(P.rrec + b);
                 ps += __ldcg(rp);
                 maxidx_merge(pm, pa, __ldcg(rp + 1), __ldcg(reinterpret_cast<const long long*>(rp + 2)));
@@ -1634,7 +1805,7 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
                 const unsigned long long k = lst.k;
                 const double metric = P.stop_kind == 0 ? e / P.ref_sq : rel;
                 const unsigned long long slot = k - lst.k0;
-                if (blockIdx.x == 0 && slot < P.trace_cap) {
+                if (grid.rank() == 0 && slot < P.trace_cap) {
                     P.trace_row[slot] = sel;
                     P.trace_metric[slot] = metric;
                     P.trace_rel[slot] = rel;
@@ -1650,8 +1821,24 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
         // written before the grid.sync above) and writes y, which nobody reads
         // until after the next grid.sync
     }
-    if (blockIdx.x == 0 && tid == 0) *P.st = lst;
+    if (grid.rank() == 0 && tid == 0) *P.st = lst;
 }
+
+__global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
+    persist_body<GridGroup, kPersistThreads>(P, GridGroup{cooperative_groups::this_grid()});
+}
+
+// One CTA per system: Ps[blockIdx.x] describes an independent solve (its own
+// buffers and DevState).  Grid barriers become CTA barriers.
+// 512 threads: one CTA must carry a whole system's memory parallelism
+constexpr int kBatchThreads = 512;
+__global__ void __launch_bounds__(kBatchThreads, 1) k_persist_batch(const Params* __restrict__ Ps) {
+    __shared__ Params sp;
+    if (threadIdx.x == 0) sp = Ps[blockIdx.x];
+    __syncthreads();
+    persist_body<SoloGroup, kBatchThreads>(sp, SoloGroup{});
+}
+
 
 int persist_grid(const Params& P) {
     int dev = 0, sms = 0, per = 0;
@@ -2106,6 +2293,14 @@ void launch_transpose(const double* in, long long rows, long long cols, double* 
                       cudaStream_t s) {
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
     k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out);
+}
+
+int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStream_t s) {
+    const size_t smem = sizeof(double) * (size_t)((max_m + 31) / 32);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_persist_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_persist_batch<<<count, kBatchThreads, smem, s>>>(dPs);
+    return (int)cudaGetLastError();
 }
 
 int launch_persist(const Params& P, cudaStream_t s) {

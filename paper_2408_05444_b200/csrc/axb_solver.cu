@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -224,6 +225,7 @@ struct axb_solver {
     std::vector<cudaEvent_t> prof_ev;
     double loop_ms = 0.0, k2_ms = 0.0, yg_ms = 0.0, zx_ms = 0.0;
     uint64_t k2_launches = 0, kernel_launches = 0;
+    uint64_t last_nb = 0;  // iterations armed by the last batch_launch
 
     ~axb_solver() {
         if (graph) cudaGraphExecDestroy(graph);
@@ -850,8 +852,19 @@ struct axb_solver {
 
     // runs up to nb iterations from the current k; returns iterations executed
     uint64_t batch(uint64_t nb, int run_mode) {
+        batch_launch(nb, run_mode, false);
+        return batch_collect();
+    }
+    // a persistent-kernel handle whose kernel a multi-system launch runs
+    // (axb_solvers_run): only the control block is armed here
+    bool batchable() const { return P.persist && !profiling; }
+    void batch_launch(uint64_t nb, int run_mode, bool external) {
         launch_ctrl(st.p, k, k + nb, FIN_ITERATION, run_mode, 0, stream);
         ++kernel_launches;
+        if (external) {
+            ++kernel_launches;  // the shared k_persist_batch launch
+            return;
+        }
         if (P.persist && !profiling) {
             // the kernel selects at the top of each iteration itself
             const int e = launch_persist(P, stream);
@@ -895,6 +908,11 @@ struct axb_solver {
             for (uint64_t i = 0; i < launches; ++i) ck(cudaGraphLaunch(graph, stream), "graph launch");
             kernel_launches += (sharded ? 5 : 3) * nb;
         }
+        last_nb = nb;
+    }
+    uint64_t batch_collect() {
+        const uint64_t nb = last_nb;
+        (void)nb;
         pull_state();
         if (profiling) {
             const uint64_t done = hs->k - k;
@@ -1093,76 +1111,118 @@ struct axb_solver {
     }
 
     // ---------------------------------------------------------------- run()
-    void run(axb_report* rep, uint64_t* trace_k, double* trace_rrn, double* trace_rel,
-             uint64_t* trace_row, uint64_t trace_cap_out, double* x_out) {
-        std::memset(rep, 0, sizeof *rep);
-        rep->alpha = alpha;
-        rep->seed = cfg.seed;
-        rep->alpha_outside_bound = alpha_outside;
+    // run() (solver.hpp:337-372) as a resumable state machine, so that
+    // axb_solvers_run can advance many handles through one batched launch
+    struct RunCtx {
+        axb_report* rep = nullptr;
+        uint64_t *trace_k = nullptr, *trace_row = nullptr;
+        double *trace_rrn = nullptr, *trace_rel = nullptr, *x_out = nullptr;
+        uint64_t trace_cap_out = 0, ntrace = 0, k_before = 0, nb = 0;
+        bool converged = false, done = false;
+        std::chrono::steady_clock::time_point t0;
+    };
+    void run_begin(RunCtx& c) {
+        std::memset(c.rep, 0, sizeof *c.rep);
+        c.rep->alpha = alpha;
+        c.rep->seed = cfg.seed;
+        c.rep->alpha_outside_bound = alpha_outside;
         reset_status();
-        uint64_t ntrace = 0;
-        bool converged = exact_metric() <= cfg.tol;  // :344
-        const auto t0 = std::chrono::steady_clock::now();
+        c.ntrace = 0;
+        c.converged = exact_metric() <= cfg.tol;  // :344
+        c.t0 = std::chrono::steady_clock::now();
         cudaEventRecord(ev0, stream);
-        try {
-            while (!converged && k < cfg.max_iter) {
-                pull_state();
-                if (!(hs->r_fro_sq > 0.0)) break;  // :347
-                uint64_t nb = std::min<uint64_t>(cfg.max_iter - k, trace_cap);
-                const uint64_t ri = cfg.refresh_interval;
-                if (ri > 0) nb = std::min<uint64_t>(nb, ri - k % ri);
-                const uint64_t k_before = k;
-                const uint64_t done = batch(nb, 1);
-                if (cfg.record_trace) {
-                    for (uint64_t t = 0; t < done; ++t) {
-                        const uint64_t kk = k_before + t;
-                        if (!trace_point_due(kk)) continue;  // :349-350
-                        if (ntrace < trace_cap_out) {
-                            if (trace_k) trace_k[ntrace] = kk;
-                            if (trace_rrn) trace_rrn[ntrace] = h_trace_metric[t];
-                            if (trace_rel) trace_rel[ntrace] = h_trace_rel[t];
-                            if (trace_row) trace_row[ntrace] = (uint64_t)h_trace_row[t];
-                        }
-                        ++ntrace;
-                    }
-                }
-                if (hs->status == ST_ZERO) {
-                    launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 1, stream);
-                    break;
-                }
-                if (hs->status == ST_PAUSE) {  // :351-358
-                    launch_ctrl(st.p, k, k, FIN_ITERATION, 1, 1, stream);
-                    if (exact_metric() <= cfg.tol) converged = true;
-                    else resync();
-                }
-                if (!converged && ri > 0 && k % ri == 0) checkpoint();  // :359-360
-            }
-        } catch (AxbError& e) {
-            rep->iterations = k;
-            rep->diverged_iteration = e.k;
-            rep->diverged_residual = e.val;
-            throw;
+        c.done = c.converged || k >= cfg.max_iter;
+    }
+    // next segment length, or false when the loop ends here (:346-347)
+    bool run_segment(RunCtx& c) {
+        if (c.done) return false;
+        pull_state();
+        if (!(hs->r_fro_sq > 0.0)) {  // :347
+            c.done = true;
+            return false;
         }
+        uint64_t nb = std::min<uint64_t>(cfg.max_iter - k, trace_cap);
+        const uint64_t ri = cfg.refresh_interval;
+        if (ri > 0) nb = std::min<uint64_t>(nb, ri - k % ri);
+        c.k_before = k;
+        c.nb = nb;
+        return true;
+    }
+    void run_after(RunCtx& c, uint64_t done) {
+        if (cfg.record_trace) {
+            for (uint64_t t = 0; t < done; ++t) {
+                const uint64_t kk = c.k_before + t;
+                if (!trace_point_due(kk)) continue;  // :349-350
+                if (c.ntrace < c.trace_cap_out) {
+                    if (c.trace_k) c.trace_k[c.ntrace] = kk;
+                    if (c.trace_rrn) c.trace_rrn[c.ntrace] = h_trace_metric[t];
+                    if (c.trace_rel) c.trace_rel[c.ntrace] = h_trace_rel[t];
+                    if (c.trace_row) c.trace_row[c.ntrace] = (uint64_t)h_trace_row[t];
+                }
+                ++c.ntrace;
+            }
+        }
+        const uint64_t ri = cfg.refresh_interval;
+        if (hs->status == ST_ZERO) {
+            launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 1, stream);
+            c.done = true;
+            return;
+        }
+        if (hs->status == ST_PAUSE) {  // :351-358
+            launch_ctrl(st.p, k, k, FIN_ITERATION, 1, 1, stream);
+            if (exact_metric() <= cfg.tol) c.converged = true;
+            else resync();
+        }
+        if (!c.converged && ri > 0 && k % ri == 0) checkpoint();  // :359-360
+        c.done = c.converged || k >= cfg.max_iter;
+    }
+    void run_fail(RunCtx& c, const AxbError& e) {
+        c.rep->iterations = k;
+        c.rep->diverged_iteration = e.k;
+        c.rep->diverged_residual = e.val;
+        c.done = true;
+    }
+    void run_end(RunCtx& c) {
         cudaEventRecord(ev1, stream);
         sync("run");
         const auto t1 = std::chrono::steady_clock::now();
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev0, ev1);
         loop_ms = ms;
+        axb_report* rep = c.rep;
         rep->iterations = k;
-        rep->wall_seconds = std::chrono::duration<double>(t1 - t0).count();
-        rep->terminated_by = converged ? AXB_TERMINATED_TOLERANCE : AXB_TERMINATED_MAX_ITER;
+        rep->wall_seconds = std::chrono::duration<double>(t1 - c.t0).count();
+        rep->terminated_by = c.converged ? AXB_TERMINATED_TOLERANCE : AXB_TERMINATED_MAX_ITER;
         rep->final_rrn = exact_metric();
         rep->final_residual_rel = exact_residual_rel();
         pull_state();
         rep->skipped_zero_rows = hs->skipped_zero_rows;
-        rep->trace_len = ntrace;
-        if (x_out) {
+        rep->trace_len = c.ntrace;
+        if (c.x_out) {
             gather_X();
-            ck(cudaMemcpyAsync(x_out, X.p, sizeof(double) * p * q, cudaMemcpyDeviceToHost, stream),
+            ck(cudaMemcpyAsync(c.x_out, X.p, sizeof(double) * p * q, cudaMemcpyDeviceToHost, stream),
                "X out");
             sync("X out");
         }
+    }
+    void run(axb_report* rep, uint64_t* trace_k, double* trace_rrn, double* trace_rel,
+             uint64_t* trace_row, uint64_t trace_cap_out, double* x_out) {
+        RunCtx c;
+        c.rep = rep;
+        c.trace_k = trace_k;
+        c.trace_rrn = trace_rrn;
+        c.trace_rel = trace_rel;
+        c.trace_row = trace_row;
+        c.trace_cap_out = trace_cap_out;
+        c.x_out = x_out;
+        run_begin(c);
+        try {
+            while (run_segment(c)) run_after(c, batch(c.nb, 1));
+        } catch (AxbError& e) {
+            run_fail(c, e);
+            throw;
+        }
+        run_end(c);
     }
 
     // ---------------------------------------------------------------- public selects
@@ -1384,6 +1444,150 @@ int axb_solver_run(axb_solver* s, axb_report* rep, uint64_t* trace_k, double* tr
                    double* trace_rel, uint64_t* trace_row, uint64_t trace_cap, double* x_out) {
     return guarded(s, [&] { s->run(rep, trace_k, trace_rrn, trace_rel, trace_row, trace_cap, x_out); });
 }
+namespace {
+// per-device launch resources of axb_solvers_run
+struct BatchRes {
+    cudaStream_t s = nullptr;
+    Params* dP = nullptr;
+    Params* hP = nullptr;  // pinned staging
+    size_t cap = 0;
+};
+std::mutex g_batch_mu;
+BatchRes g_batch[64];
+
+int record_failure(axb_solver* s, const AxbError& e) {
+    s->err = e.msg;
+    s->err_k = e.k;
+    s->err_val = e.val;
+    return e.code;
+}
+}  // namespace
+
+int axb_solvers_run(axb_solver* const* hs, uint32_t count, axb_report* reps,
+                    double* const* x_outs, int32_t* statuses) {
+    if (count == 0) return AXB_OK;
+    if (!hs || !reps || !statuses) {
+        g_create_err = "axb_solvers_run: null argument";
+        return AXB_CONFIG_ERROR;
+    }
+    for (uint32_t i = 0; i < count; ++i) {
+        if (!hs[i]) {
+            g_create_err = "axb_solvers_run: null handle";
+            return AXB_CONFIG_ERROR;
+        }
+        if (hs[i]->opt.device != hs[0]->opt.device) {
+            g_create_err = "axb_solvers_run: all handles must live on one device";
+            return AXB_CONFIG_ERROR;
+        }
+        if (hs[i]->sharded) {
+            g_create_err = "axb_solvers_run: sharded handles run on their own (axb_solver_run)";
+            return AXB_CONFIG_ERROR;
+        }
+        for (uint32_t j = 0; j < i; ++j)
+            if (hs[j] == hs[i]) {
+                g_create_err = "axb_solvers_run: duplicate handle";
+                return AXB_CONFIG_ERROR;
+            }
+    }
+    const int dev = hs[0]->opt.device;
+    std::lock_guard<std::mutex> lock(g_batch_mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(dev) != cudaSuccess) {
+        g_create_err = "axb_solvers_run: cudaSetDevice failed";
+        return AXB_CUDA_ERROR;
+    }
+    BatchRes& br = g_batch[dev & 63];
+    std::vector<axb_solver::RunCtx> ctx(count);
+    std::vector<char> active(count, 0);
+    for (uint32_t i = 0; i < count; ++i) {
+        statuses[i] = AXB_OK;
+        ctx[i].rep = &reps[i];
+        ctx[i].x_out = x_outs ? x_outs[i] : nullptr;
+        try {
+            hs[i]->run_begin(ctx[i]);
+            active[i] = 1;
+        } catch (const AxbError& e) {
+            statuses[i] = record_failure(hs[i], e);
+        }
+    }
+    auto fail_one = [&](uint32_t i, const AxbError& e) {
+        hs[i]->run_fail(ctx[i], e);
+        statuses[i] = record_failure(hs[i], e);
+        active[i] = 0;
+    };
+    int rc = AXB_OK;
+    try {
+        for (;;) {
+            std::vector<uint32_t> group;
+            bool any = false;
+            for (uint32_t i = 0; i < count; ++i) {
+                if (!active[i]) continue;
+                axb_solver* h = hs[i];
+                try {
+                    if (!h->run_segment(ctx[i])) {
+                        h->run_end(ctx[i]);
+                        active[i] = 0;
+                        continue;
+                    }
+                    any = true;
+                    if (h->batchable()) {
+                        h->batch_launch(ctx[i].nb, 1, true);
+                        group.push_back(i);
+                    } else {  // large systems keep their own launch path
+                        h->run_after(ctx[i], h->batch(ctx[i].nb, 1));
+                    }
+                } catch (const AxbError& e) {
+                    fail_one(i, e);
+                }
+            }
+            if (!any) break;
+            if (group.empty()) continue;
+            // every armed control block must land before the shared launch reads it
+            for (uint32_t i : group) ck(cudaStreamSynchronize(hs[i]->stream), "arm");
+            if (!br.s) ck(cudaStreamCreateWithFlags(&br.s, cudaStreamNonBlocking), "batch stream");
+            if (br.cap < group.size()) {
+                if (br.dP) cudaFree(br.dP);
+                if (br.hP) cudaFreeHost(br.hP);
+                br.dP = nullptr;
+                br.hP = nullptr;
+                br.cap = 0;
+                const size_t want = std::max<size_t>(group.size(), 256);
+                ck(cudaMalloc(&br.dP, sizeof(Params) * want), "batch params");
+                ck(cudaMallocHost(&br.hP, sizeof(Params) * want), "batch params");
+                br.cap = want;
+            }
+            long long max_m = 1;
+            for (size_t j = 0; j < group.size(); ++j) {
+                br.hP[j] = hs[group[j]]->P;
+                max_m = std::max<long long>(max_m, hs[group[j]]->P.m);
+            }
+            ck(cudaMemcpyAsync(br.dP, br.hP, sizeof(Params) * group.size(), cudaMemcpyHostToDevice,
+                               br.s), "batch params");
+            const int e = launch_persist_batch(br.dP, (int)group.size(), max_m, br.s);
+            if (e != 0) ck(static_cast<cudaError_t>(e), "batched persistent kernel launch");
+            ck(cudaStreamSynchronize(br.s), "batched persistent kernel");
+            for (uint32_t i : group) {
+                try {
+                    hs[i]->run_after(ctx[i], hs[i]->batch_collect());
+                } catch (const AxbError& e) {
+                    fail_one(i, e);
+                }
+            }
+        }
+    } catch (const AxbError& e) {  // launch-level failure: every open run fails
+        g_create_err = e.msg;
+        rc = e.code;
+        for (uint32_t i = 0; i < count; ++i)
+            if (active[i]) {
+                hs[i]->run_fail(ctx[i], e);
+                statuses[i] = record_failure(hs[i], e);
+            }
+    }
+    cudaSetDevice(prev);
+    return rc;
+}
+
 int axb_solver_select_cyclic(axb_solver* s, uint64_t* row) {
     return guarded(s, [&] { *row = s->select_consume(AXB_BK, 0.5); });
 }

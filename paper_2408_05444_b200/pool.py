@@ -7,11 +7,13 @@ wall time are averaged over converged trials, divergent or budget-exhausted
 trials are counted as failures, and each row reports its speed-up against the
 RBK row of the same problem (:315-354).
 
-Where the reference runs one solve per CPU thread, tasks here are spread over
-``jobs`` host threads driving independent solver handles (each with its own CUDA
-stream) on ``devices`` round-robin: the small, latency-bound solves of the
-harness overlap on one GPU instead of queueing.  The C-ABI
-releases the GIL for the duration of each call.
+Where the reference runs one solve per CPU thread, the device path batches
+(SURVEY §8(f) F3): per device, the task handles are created by ``jobs`` host
+threads and then advanced together by ``run_many`` (axb_solvers_run) — every
+small system is one CTA of a single persistent launch per refresh segment, so
+hundreds of latency-bound trials share the GPU instead of queueing.  With
+``batched=False`` each of ``jobs`` threads drives its own handle's run()
+(one stream each).  The C-ABI releases the GIL for the duration of each call.
 """
 from __future__ import annotations
 
@@ -24,7 +26,8 @@ import numpy as np
 
 from .analysis import reference_solution
 from .errors import ConfigError, DivergenceError
-from .solver import AlphaRule, Method, MethodTag, Options, SolveConfig, Solver, StopRule, Terminated
+from .solver import (AlphaRule, Method, MethodTag, Options, SolveConfig, Solver, StopRule,
+                     Terminated, run_many)
 
 _M64 = (1 << 64) - 1
 
@@ -61,6 +64,8 @@ class BenchmarkOptions:  # analysis.hpp BenchmarkOptions
     jobs: int = 4
     devices: Sequence[int] = (0,)
     options: dict = field(default_factory=dict)  # extra solver Options fields
+    batched: bool = True      # run_many per device (one CTA per small system)
+    batch_size: int = 1184    # handles per run_many call (bounds device memory)
 
 
 @dataclass
@@ -96,7 +101,7 @@ def benchmark(problems: List[BenchProblem], methods: List[Method],
              for t in range(opt.trials)]
     outcomes = [None] * len(tasks)
 
-    def run_task(idx):
+    def make_task(idx):
         p, mi, t = tasks[idx]
         pb = problems[p]
         if opt.stop_kind == StopRule.Kind.SolutionRrn:
@@ -107,38 +112,68 @@ def benchmark(problems: List[BenchProblem], methods: List[Method],
                           alpha_value=opt.alpha_value, stop=stop, max_iter=opt.max_iter,
                           seed=substream_seed(opt.seed, t))
         dev = opt.devices[idx % len(opt.devices)]
+        return Solver(pb.A, pb.B, pb.C, None, cfg, Options(device=dev, **opt.options))
+
+    def run_task(idx):
         try:
-            rep = Solver(pb.A, pb.B, pb.C, None, cfg, Options(device=dev, **opt.options)).run()
+            rep = make_task(idx).run()
             outcomes[idx] = (float(rep.iterations), rep.wall_seconds,
                              rep.terminated_by == Terminated.MaxIter)
         except DivergenceError:
             outcomes[idx] = (0.0, 0.0, True)
 
     jobs = max(1, min(opt.jobs, len(tasks)))
-    nxt = [0]
-    lock = threading.Lock()
-    errors = []
 
-    def worker():
-        while True:
-            with lock:
-                i = nxt[0]
-                nxt[0] += 1
-            if i >= len(tasks):
-                return
-            try:
-                run_task(i)
-            except Exception as e:  # surface after the pool drains
-                errors.append(e)
-                return
+    def pool_map(fn, items):
+        """fn over items on `jobs` host threads; first error re-raised."""
+        nxt = [0]
+        lock = threading.Lock()
+        errors = []
 
-    threads = [threading.Thread(target=worker) for _ in range(jobs)]
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join()
-    if errors:
-        raise errors[0]
+        def worker():
+            while True:
+                with lock:
+                    i = nxt[0]
+                    nxt[0] += 1
+                if i >= len(items):
+                    return
+                try:
+                    fn(items[i])
+                except Exception as e:  # surface after the pool drains
+                    errors.append(e)
+                    return
+
+        threads = [threading.Thread(target=worker) for _ in range(min(jobs, len(items)))]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        if errors:
+            raise errors[0]
+
+    if opt.batched:
+        for d, dev in enumerate(opt.devices):
+            mine = [i for i in range(len(tasks)) if i % len(opt.devices) == d]
+            for c0 in range(0, len(mine), max(1, opt.batch_size)):
+                chunk = mine[c0:c0 + max(1, opt.batch_size)]
+                handles = [None] * len(chunk)
+
+                def build(j):
+                    handles[j] = make_task(chunk[j])
+
+                pool_map(build, list(range(len(chunk))))
+                results = run_many(handles, return_exceptions=True)
+                for idx, res in zip(chunk, results):
+                    if isinstance(res, DivergenceError):
+                        outcomes[idx] = (0.0, 0.0, True)
+                    elif isinstance(res, Exception):
+                        raise res
+                    else:
+                        outcomes[idx] = (float(res.iterations), res.wall_seconds,
+                                         res.terminated_by == Terminated.MaxIter)
+                del handles
+    else:
+        pool_map(run_task, list(range(len(tasks))))
 
     rows, rbk_wall = [], [-1.0] * len(problems)
     for p, pb in enumerate(problems):

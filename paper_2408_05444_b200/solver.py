@@ -406,6 +406,15 @@ class Solver:
             X=X, alpha=rep.alpha, seed=rep.seed, method_label=self.cfg.method.label(),
             alpha_outside_bound=bool(rep.alpha_outside_bound), skipped_zero_rows=rep.skipped_zero_rows)
 
+    def _report(self, rep, X, trace=()):
+        return SolveReport(
+            iterations=rep.iterations, wall_seconds=rep.wall_seconds, final_rrn=rep.final_rrn,
+            final_residual_rel=rep.final_residual_rel, terminated_by=Terminated(rep.terminated_by),
+            trace=list(trace), X=X, alpha=rep.alpha, seed=rep.seed,
+            method_label=self.cfg.method.label(),
+            alpha_outside_bound=bool(rep.alpha_outside_bound),
+            skipped_zero_rows=rep.skipped_zero_rows)
+
     # -- accessors (solver.hpp:376-436) --
     def iteration(self):
         return int(self._lib.axb_solver_iteration(self._h))
@@ -480,6 +489,39 @@ class Solver:
         self._lib.axb_solver_last_timing(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
         return {"loop_ms": a.value, "k2_ms": b.value, "k2_launches": c.value,
                 "kernel_launches": d.value}
+
+
+def run_many(solvers: List["Solver"], return_exceptions: bool = False) -> list:
+    """run() on many independent solvers of one device in one batch
+    (axb_solvers_run): small systems advance together, one CTA each, through a
+    single launch per refresh segment.  Each result equals that
+    solver's own run(), without the trace.  A failed solve raises its
+    reference exception — or, with return_exceptions, is returned in its slot."""
+    if not solvers:
+        return []
+    lib = _lib.load()
+    k = len(solvers)
+    hs = (C.c_void_p * k)(*[s._h for s in solvers])
+    reps = (_lib.AxbReport * k)()
+    xs = [np.empty((s.p, s.q)) for s in solvers]
+    xp = (_dp * k)(*[x.ctypes.data_as(_dp) for x in xs])
+    sts = (C.c_int32 * k)()
+    st = lib.axb_solvers_run(hs, k, reps, xp, sts)
+    if st:
+        raise_status(st, lib.axb_last_create_error().decode())
+    out = []
+    for i, s in enumerate(solvers):
+        if sts[i]:
+            try:
+                s._chk(sts[i], iteration=reps[i].diverged_iteration,
+                       residual_norm=reps[i].diverged_residual)
+            except Exception as e:  # noqa: BLE001
+                if not return_exceptions:
+                    raise
+                out.append(e)
+            continue
+        out.append(s._report(reps[i], xs[i]))
+    return out
 
 
 def solve(A, B, C_, X0, cfg: SolveConfig, options: Optional[Options] = None) -> SolveReport:
