@@ -420,7 +420,8 @@ def main():
     per_iter_ms = ms / args.steps
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_r_tma<true> (fused R update + row norms + next-row select, TMA ring)",
+                "kernel": "k_r_tma<true> (fused R update + row norms, TMA ring) timed together with "
+                          "k_sel_greedy (next-row greedy select across the SMs)",
                 "algorithmic_bytes_per_launch": kb, "k2_ms": round(k2_ms, 5),
                 "peak_kind": peak_kind,
                 "k2_share_of_step": round(k2_ms / per_iter_ms, 4),

@@ -59,7 +59,7 @@ struct alignas(16) DevState {
     double err_sq;               // ‖X − X_ref‖²_F (fresh, solution_rrn)
     double metric;               // current stop metric
     int32_t x_finite;            // X all finite (checkpoint guard, solver.hpp:428)
-    int32_t _pad0;
+    int32_t sel_pending;         // K2 left the greedy pre-selection to k_sel_greedy
     // query results (greedy_threshold / max_residual_ratio)
     double q_zeta;
     long long q_row;
@@ -68,7 +68,7 @@ struct alignas(16) DevState {
     unsigned int cnt_r;
     unsigned int cnt_x;
     unsigned int cnt_red;
-    unsigned int _pad1;
+    unsigned int cnt_sel;        // k_sel_greedy last-block counter
     unsigned long long r_next;   // dynamic row counter of the TMA residual kernel
     int32_t replay;              // 1: select from Params::forced_rows (index-stream replay)
     int32_t packed;              // sharded: this rank's pack_send holds the last row
@@ -128,12 +128,15 @@ struct Params {
     int persist, persist_grid;   // small systems: one cooperative kernel per batch
     int yg_grid;
     int z_nslab, z_nj, z_jrows, x_ctas;
+    int sel_split, sel_grid;     // greedy pre-selection across sel_grid CTAs (k_sel_greedy)
 };
 
 // ---- launchers (axb_iter.cu) ----
 void launch_yg(const Params& P, cudaStream_t s, bool with_g);
 void launch_zx(const Params& P, cudaStream_t s);
 void launch_r(const Params& P, cudaStream_t s, bool update);
+// greedy pre-selection of the next row after K2 when P.sel_split (PDL-chained)
+void launch_sel_greedy(const Params& P, cudaStream_t s);
 void launch_select(const Params& P, cudaStream_t s, int method, double theta, int consume);
 void launch_query(const Params& P, cudaStream_t s, double theta, int want_set);
 void launch_rollback(const Params& P, cudaStream_t s);

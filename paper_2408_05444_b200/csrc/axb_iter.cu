@@ -506,14 +506,17 @@ __device__ Member make_member(const Params& P, const DevState* st, double theta)
     return mm;
 }
 
-// gs[g] = Σ member masses of rows [32g, 32g+32): coalesced, branch-free loads
-// (8 groups × 2 arrays in flight per warp, every warp of the block), warp trees
-__device__ void grbk_group_sums(const Member& mem, long long m, double* gs) {
+// gs[g] = Σ member masses of rows [32g, 32g+32) for g in [g_begin, g_end):
+// coalesced, branch-free loads (8 groups × 2 arrays in flight per warp, every
+// warp of the block), warp trees.  A group's sum does not depend on which CTA
+// forms it, so one CTA (K2's last) or many (k_sel_greedy) give identical gs.
+__device__ void grbk_group_sums(const Member& mem, long long m, double* gs,
+                                long long g_begin = 0, long long g_end = -1) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = (int)(blockDim.x >> 5);
-    const long long ng = (m + 31) / 32;
+    const long long ng = g_end < 0 ? (m + 31) / 32 : g_end;
     constexpr int kG = 8;
-    for (long long gb = warp; gb < ng; gb += (long long)nw * kG) {
+    for (long long gb = g_begin + warp; gb < ng; gb += (long long)nw * kG) {
         double as[kG], rs[kG];
 #pragma unroll
         for (int u = 0; u < kG; ++u) {
@@ -629,6 +632,9 @@ __device__ long long grbk_search(const Member& mem, long long m, const double* g
     return pick;
 }
 
+__device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const double* gs,
+                         long long* out_row, SelShared& sh);
+
 __device__ int select_rows(const Params& P, DevState* st, int method, double theta,
                            long long* out_row, SelShared& sh, double* scratch,
                            long long scratch_cap) {
@@ -700,6 +706,15 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
     const Member mem = make_member(P, st, theta);
     double* gs = (scratch != nullptr && (m + 31) / 32 <= scratch_cap) ? scratch : P.gsum;
     grbk_group_sums(mem, m, gs);
+    return grbk_pick(P, st, mem, gs, out_row, sh);
+}
+
+// The greedy draw once the group sums gs are in place: ordered prefix, one
+// uniform, two-level search with the tie guard, exact sequential fallback.
+__device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const double* gs,
+                         long long* out_row, SelShared& sh) {
+    const int tid = threadIdx.x;
+    const long long m = P.m;
     if (tid == 0) AXB_STAMP(1);
     long long g0, g1;
     double excl;
@@ -754,10 +769,8 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
     return 0;
 }
 
-// block-level finalize + selection shared by k_r's last block and k_select
-__device__ void finish_select(const Params& P, DevState* st, SelShared& sh, double* scratch,
-                              long long scratch_cap) {
-    long long row = 0;
+// snapshot before a speculative pre-selection (rolled back by k_rollback)
+__device__ void sel_snapshot(DevState* st, SelShared& sh) {
     if (threadIdx.x == 0) {
         for (int k = 0; k < 4; ++k) st->rng_snap[k] = st->rng[k];
         st->cyclic_snap = st->cyclic_pos;
@@ -765,6 +778,28 @@ __device__ void finish_select(const Params& P, DevState* st, SelShared& sh, doub
         sh.err = 0;
     }
     __syncthreads();
+}
+
+__device__ void sel_commit(const Params& P, DevState* st, int err, long long row) {
+    if (threadIdx.x == 0) {
+        if (err) {
+            st->status = ST_ERROR;
+            st->err_code = err;
+            st->err_k = st->k;
+            st->sel_valid = 0;
+        } else {
+            st->sel = row;
+            st->coef = __ddiv_rn(P.alpha, P.a_sq[row - P.row0]);
+            st->sel_valid = 1;
+        }
+    }
+}
+
+// block-level finalize + selection shared by k_r's last block and k_select
+__device__ void finish_select(const Params& P, DevState* st, SelShared& sh, double* scratch,
+                              long long scratch_cap) {
+    long long row = 0;
+    sel_snapshot(st, sh);
     const int err = select_rows(P, st, P.method, P.theta, &row, sh, scratch, scratch_cap);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -838,8 +873,13 @@ __device__ void finalize(const Params& P, DevState* st, double s, double mx, lon
         }
     }
     __syncthreads();
-    if (mode == FIN_ITERATION && st->status == ST_RUN && st->k < st->k_limit)
-        finish_select(P, st, sh, scratch, scratch_cap);
+    if (mode == FIN_ITERATION && st->status == ST_RUN && st->k < st->k_limit) {
+        if (P.sel_split && (P.method == 2 || P.method == 3) && !st->replay) {
+            if (tid == 0) st->sel_pending = 1;  // k_sel_greedy (next launch) selects
+        } else {
+            finish_select(P, st, sh, scratch, scratch_cap);
+        }
+    }
 }
 
 template <bool UPDATE>
@@ -1459,6 +1499,50 @@ __global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
 //   own shared-memory copy of DevState (same xoshiro stream, same inputs →
 //   identical results), so no fourth barrier is needed; CTA 0 writes the trace
 //   and, at the end, the state.
+// ------------------------------------------------------------------------
+// K3 split: the greedy pre-selection of the next row across sel_grid CTAs.
+// K2's last CTA publishes ‖R‖², max ratio and argmax and sets sel_pending; here
+// every CTA forms the member-mass sums of its slice of the 32-row groups and
+// the last CTA to finish runs the ordered prefix, the draw and the search —
+// the same arithmetic as the single-CTA path (grbk_group_sums / grbk_pick),
+// with the O(m) membership pass spread over the SMs.
+__global__ void __launch_bounds__(kThreads) k_sel_greedy(Params P) {
+    __shared__ SelShared sh;
+    __shared__ bool last;
+    pdl_wait();
+    pdl_trigger();
+    DevState* st = P.st;
+    if (!st->sel_pending) return;
+    const long long m = P.m, ng = (m + 31) / 32;
+    const bool live = st->r_fro_sq > 0.0;
+    if (live) {
+        const Member mem = make_member(P, st, P.theta);
+        const long long per = (ng + gridDim.x - 1) / gridDim.x;
+        const long long gb = (long long)blockIdx.x * per;
+        grbk_group_sums(mem, m, P.gsum, gb, min(ng, gb + per));
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&st->cnt_sel, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    sel_snapshot(st, sh);
+    long long row = 0;
+    int err = 2;  // "greedy threshold: zero residual"
+    if (live) {
+        const Member mem = make_member(P, st, P.theta);
+        err = grbk_pick(P, st, mem, P.gsum, &row, sh);
+    }
+    __syncthreads();
+    sel_commit(P, st, err, row);
+    if (threadIdx.x == 0) {
+        st->sel_pending = 0;
+        st->cnt_sel = 0u;
+    }
+}
+
 constexpr int kPersistThreads = 256;
 
 // Execution groups of the persistent iteration: a cooperative grid working on
@@ -2293,6 +2377,10 @@ void launch_transpose(const double* in, long long rows, long long cols, double* 
                       cudaStream_t s) {
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
     k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out);
+}
+
+void launch_sel_greedy(const Params& P, cudaStream_t s) {
+    launch_pdl(k_sel_greedy, P.sel_grid, kThreads, 0, s, P);
 }
 
 int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStream_t s) {

@@ -628,6 +628,16 @@ struct axb_solver {
         P.method = cfg.method;
         P.stop_kind = cfg.stop_kind;
         P.tie_guard = (opt.tie_guard && !sharded) ? 1 : 0;  // exact replay needs all rows
+        {
+            // greedy pre-selection spread over the SMs (k_sel_greedy) once the
+            // O(m) membership pass outweighs one more PDL-chained launch
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
+            const long long ng = (long long)(m + 31) / 32;
+            const bool greedy = cfg.method == AXB_GRBK || cfg.method == AXB_RGRBK;
+            P.sel_split = (!sharded && greedy && env_int("AXB_SEL_SPLIT", ng >= 64 ? 1 : 0)) ? 1 : 0;
+            P.sel_grid = (int)std::max<long long>(1, std::min<long long>(sms, (ng + 3) / 4));
+        }
         // small systems (per-iteration working set L2-resident): one persistent
         // cooperative kernel per batch instead of a graph of 3 kernels/iteration
         {
@@ -828,6 +838,7 @@ struct axb_solver {
         launch_zx(P, stream);
         if (sharded) allgather_inplace(z.p, n_loc);
         launch_r(P, stream, true);
+        if (P.sel_split) launch_sel_greedy(P, stream);
         if (sharded) {
             allgather_inplace(recs.p, 4);
             launch_sel1(P, stream, true);
@@ -836,9 +847,10 @@ struct axb_solver {
             allreduce(pack_send.p, pack.p, n + p + 2);
         }
     }
+    int launches_per_iteration() const { return sharded ? 5 : (P.sel_split ? 4 : 3); }
     void launch_iteration() {
         enqueue_iteration();
-        kernel_launches += sharded ? 5 : 3;
+        kernel_launches += launches_per_iteration();
     }
 
     void build_graph() {
@@ -890,6 +902,7 @@ struct axb_solver {
                 if (sharded) allgather_inplace(z.p, n_loc);
                 ck(cudaEventRecord(prof_ev[4 * i + 2], stream), "ev");
                 launch_r(P, stream, true);
+                if (P.sel_split) launch_sel_greedy(P, stream);  // timed with K2: its tail
                 ck(cudaEventRecord(prof_ev[4 * i + 3], stream), "ev");
                 if (sharded) {
                     allgather_inplace(recs.p, 4);
@@ -898,7 +911,7 @@ struct axb_solver {
                     launch_sel2(P, stream);
                     allreduce(pack_send.p, pack.p, n + p + 2);
                 }
-                kernel_launches += sharded ? 5 : 3;
+                kernel_launches += launches_per_iteration();
             }
         } else if (nb < (uint64_t)graph_iters) {
             for (uint64_t i = 0; i < nb; ++i) launch_iteration();
@@ -906,7 +919,7 @@ struct axb_solver {
             if (!graph) build_graph();
             const uint64_t launches = (nb + graph_iters - 1) / graph_iters;
             for (uint64_t i = 0; i < launches; ++i) ck(cudaGraphLaunch(graph, stream), "graph launch");
-            kernel_launches += (sharded ? 5 : 3) * nb;
+            kernel_launches += (uint64_t)launches_per_iteration() * nb;
         }
         last_nb = nb;
     }

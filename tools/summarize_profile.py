@@ -22,9 +22,9 @@ for r in rows[hi + 1:]:
 unit = rows[hi + 1][iunit]
 out.append("## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`)\n")
 out.append("Cold-cache, serialised per-launch times: compare shares, not absolutes.\n")
-out.append("| kernel | launches | mean | share of one iteration (K4+K4b+K2) |")
+out.append("| kernel | launches | mean | share of one iteration (K4+K4b+K2+K3) |")
 out.append("|---|---|---|---|")
-it_kernels = {k: sum(v) / len(v) for k, v in agg.items() if any(x in k for x in ("k_yg", "k_zx", "k_r_tma<1>", "k_r<1"))}
+it_kernels = {k: sum(v) / len(v) for k, v in agg.items() if any(x in k for x in ("k_yg", "k_zx", "k_r_tma<1>", "k_r<1", "k_sel_greedy"))}
 it_total = sum(it_kernels.values())
 for k, v in agg.items():
     mean = sum(v) / len(v)
