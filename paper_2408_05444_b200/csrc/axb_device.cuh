@@ -126,6 +126,9 @@ struct Params {
     // launch geometry
     int r_grid, r_rows_per_cta, r_chunk, r_tma, r_stages, r_zstage;
     int persist, persist_grid;   // small systems: one cooperative kernel per batch
+    int persist_lat;             // latency body (threads per CTA, 0 = off): selection state in
+                                 // shared memory, 2 barriers per iteration (m ≤ kPersistLatRows)
+    const double* BtB;           // n×n BᵀB (solver.hpp:172) for z = BᵀB·R_iᵀ in one phase, or null
     int yg_grid;
     int z_nslab, z_nj, z_jrows, x_ctas;
     int sel_split, sel_grid;     // greedy pre-selection across sel_grid CTAs (k_sel_greedy)
@@ -169,6 +172,9 @@ void launch_sel2(const Params& P, cudaStream_t s);
 int launch_persist(const Params& P, cudaStream_t s);
 // many independent small systems, one CTA each (dPs: device array of Params)
 int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStream_t s);
+// rows up to which the latency body runs (every CTA re-reads r_sq each iteration and
+// selects from shared memory; above this the per-CTA records of the general body win)
+constexpr long long kPersistLatRows = 2048;
 
 // ---- DMMA GEMM (axb_gemm.cu) ----
 // D = (Cin ? Cin − A·op(B) : A·op(B)); op(B) = B (K×N) or Bᵀ (B is N×K) when b_trans.

@@ -190,6 +190,69 @@ __device__ void warp_dot_pair(const double* __restrict__ row0, const double* __r
     out1 = two ? warp_sum(acc1) : 0.0;
 }
 
+// warp_dot_pair with kU vector loads per lane issued before the FMAs (one L2
+// round trip per 32·kU elements instead of per 32·4)
+template <int kU>
+__device__ void warp_dot_pair_u(const double* __restrict__ row0, const double* __restrict__ row1,
+                                const double* __restrict__ v, long long len, int lane, bool vec2,
+                                bool coherent_v, double& out0, double& out1) {
+    double acc0 = 0.0, acc1 = 0.0;
+    const bool two = row1 != nullptr;
+    if (vec2) {
+        const double2* r0 = reinterpret_cast<const double2*>(row0);
+        const double2* r1 = reinterpret_cast<const double2*>(two ? row1 : row0);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const long long h = len >> 1;
+        for (long long k0 = lane; k0 < h; k0 += 32 * kU) {
+            double2 a[kU], b[kU], c[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const long long k = k0 + 32 * u;
+                if (k < h) {
+                    b[u] = coherent_v ? __ldcg(v2 + k) : __ldg(v2 + k);
+                    a[u] = __ldg(r0 + k);
+                    if (two) c[u] = __ldg(r1 + k);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const long long k = k0 + 32 * u;
+                if (k < h) {
+                    acc0 += a[u].x * b[u].x;
+                    acc0 += a[u].y * b[u].y;
+                    if (two) {
+                        acc1 += c[u].x * b[u].x;
+                        acc1 += c[u].y * b[u].y;
+                    }
+                }
+            }
+        }
+    } else {
+        for (long long k0 = lane; k0 < len; k0 += 32 * kU) {
+            double a[kU], b[kU], c[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const long long k = k0 + 32 * u;
+                if (k < len) {
+                    b[u] = coherent_v ? __ldcg(v + k) : __ldg(v + k);
+                    a[u] = __ldg(row0 + k);
+                    if (two) c[u] = __ldg(row1 + k);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const long long k = k0 + 32 * u;
+                if (k < len) {
+                    acc0 += a[u] * b[u];
+                    if (two) acc1 += c[u] * b[u];
+                }
+            }
+        }
+    }
+    out0 = warp_sum(acc0);
+    out1 = two ? warp_sum(acc1) : 0.0;
+}
+
 // ------------------------------------------------------------------------
 // K4: y = B·R_iᵀ (solver.hpp:270) [+ g = A·A_iᵀ, the Gram column of :294].
 // A CTA computes 8 row dots (one per warp) against the shared vector, which is
@@ -468,6 +531,9 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
 // K3: row selection for the next iteration, executed by one 256-thread block.
 // Writes *out_row; returns an axb_status (0 ok).  All threads must call it.
 struct SelShared {
+#ifdef AXB_TRACE_PERSIST
+    unsigned long long t_groups;  // globaltimer after the greedy group sums
+#endif
     double scan[kThreads];
     double redv[32];  // per-warp slots for blocks of up to 1024 threads
     long long redi[32];
@@ -486,10 +552,12 @@ struct Member {
     const double* r_sq;
     long long row0, argmax;
     double zeta, r_fro;
+    int smem;  // a_sq / r_sq point at shared-memory copies (persistent kernel)
+    __device__ double rs_at(long long i) const { return smem ? r_sq[i] : __ldcg(r_sq + i); }
     __device__ double operator()(long long i) const {
         const double as = a_sq[i];
         if (as <= 0.0) return -1.0;
-        const double rs = __ldcg(r_sq + i);
+        const double rs = rs_at(i);
         return (row0 + i == argmax || rs >= __dmul_rn(__dmul_rn(zeta, as), r_fro)) ? rs : -1.0;
     }
 };
@@ -498,6 +566,7 @@ __device__ Member make_member(const Params& P, const DevState* st, double theta)
     Member mm;
     mm.a_sq = P.a_sq;
     mm.r_sq = P.r_sq;
+    mm.smem = 0;
     mm.row0 = P.row0;
     mm.argmax = st->argmax;
     mm.r_fro = st->r_fro_sq;
@@ -523,18 +592,19 @@ __device__ void grbk_group_sums(const Member& mem, long long m, double* gs,
             const long long g = gb + (long long)u * nw;
             const long long i = g * 32 + lane;
             const bool ok = g < ng && i < m;
-            as[u] = ok ? __ldg(mem.a_sq + i) : 0.0;
-            rs[u] = ok ? __ldcg(mem.r_sq + i) : 0.0;
+            as[u] = ok ? mem.a_sq[i] : 0.0;
+            rs[u] = ok ? mem.rs_at(i) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < kG; ++u) {
             const long long g = gb + (long long)u * nw;
+            if (g >= ng) break;  // warp-uniform
             const long long i = g * 32 + lane;
             const bool member =
                 as[u] > 0.0 && (mem.row0 + i == mem.argmax ||
                                 rs[u] >= __dmul_rn(__dmul_rn(mem.zeta, as[u]), mem.r_fro));
             const double v = warp_sum(member ? rs[u] : 0.0);
-            if (lane == 0 && g < ng) gs[g] = v;
+            if (lane == 0) gs[g] = v;
         }
     }
     __syncthreads();
@@ -637,7 +707,8 @@ __device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const
 
 __device__ int select_rows(const Params& P, DevState* st, int method, double theta,
                            long long* out_row, SelShared& sh, double* scratch,
-                           long long scratch_cap) {
+                           long long scratch_cap, const double* as_sm = nullptr,
+                           const double* rs_sm = nullptr, const double* cum_sm = nullptr) {
     const int tid = threadIdx.x;
     const long long m = P.m;
     if (st->replay) {
@@ -679,7 +750,7 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
     }
     if (method == 1) {  // RBK: categorical_cdf on the static ‖A_i‖² CDF (solver.hpp:209)
         if (tid == 0) {
-            const double* cum = P.rbk_cum;
+            const double* cum = cum_sm ? cum_sm : P.rbk_cum;
             const double total = cum[m - 1];
             sh.err = 0;
             if (!(total > 0.0)) {
@@ -703,31 +774,134 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
     // GRBK / RGRBK (solver.hpp:212-254): ζ, membership, member-mass draw.
     if (!(st->r_fro_sq > 0.0)) return 2;  // "greedy threshold: zero residual"
     if (tid == 0) AXB_STAMP(0);
-    const Member mem = make_member(P, st, theta);
+    Member mem = make_member(P, st, theta);
+    if (as_sm) {
+        mem.a_sq = as_sm;
+        mem.r_sq = rs_sm;
+        mem.smem = 1;
+    }
     double* gs = (scratch != nullptr && (m + 31) / 32 <= scratch_cap) ? scratch : P.gsum;
     grbk_group_sums(mem, m, gs);
+#ifdef AXB_TRACE_PERSIST
+    if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh.t_groups));
+#endif
     return grbk_pick(P, st, mem, gs, out_row, sh);
 }
 
 // The greedy draw once the group sums gs are in place: ordered prefix, one
 // uniform, two-level search with the tie guard, exact sequential fallback.
+// Up to 1024 groups (m ≤ 32768) the whole draw runs in warp 0 with shuffles —
+// contiguous runs of groups per lane, a shuffle scan across the runs, the run
+// search, then the in-group rescan — and the block meets at one barrier.  The
+// arithmetic is grbk_prefix/grbk_search's with a different (fixed) association
+// of the group sums; the tie guard covers the rounding difference exactly as
+// it does between those and the reference's sequential walk.
+__device__ long long grbk_pick_warp(const Params& P, DevState* st, const Member& mem,
+                                    const double* gs, long long ng, SelShared& sh) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const long long m = P.m;
+    if (tid < 32) {
+        const long long gseg = (ng + 31) / 32;
+        const long long g0 = min(ng, (long long)lane * gseg), g1 = min(ng, g0 + gseg);
+        double local = 0.0;
+        for (long long g = g0; g < g1; ++g) local = __dadd_rn(local, gs[g]);
+        double incl = local;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl = __dadd_rn(t, incl);
+        }
+        const double total = __shfl_sync(0xffffffffu, incl, 31);
+        double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = 0.0;
+        int err = 0;
+        long long cand = -1;
+        if (!(total > 0.0)) {
+            err = 2;  // mass on zero rows only (solver.hpp:249-252)
+        } else {
+            double u = 0.0;
+            if (lane == 0) u = rng_unit(st->rng);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            const double target = __dmul_rn(u, total);
+            const double slack = P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
+            long long my_g = -1;
+            double my_before = 0.0, cum = excl;
+            for (long long g = g0; g < g1; ++g) {
+                const double nc = __dadd_rn(cum, gs[g]);
+                if (nc > target) {
+                    my_g = g;
+                    my_before = cum;
+                    break;
+                }
+                cum = nc;
+            }
+            const unsigned hitl = __ballot_sync(0xffffffffu, my_g >= 0);
+            if (hitl == 0u) {
+                err = -1;
+            } else {
+                const int fl = __ffs(hitl) - 1;
+                const long long G = __shfl_sync(0xffffffffu, my_g, fl);
+                const double before = __shfl_sync(0xffffffffu, my_before, fl);
+                const long long i = G * 32 + lane;
+                const double w = (i < m) ? mem(i) : -1.0;
+                double v = w > 0.0 ? w : 0.0;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const double t = __shfl_up_sync(0xffffffffu, v, off);
+                    if (lane >= off) v = __dadd_rn(v, t);
+                }
+                const double c = __dadd_rn(before, v);
+                double prev = __shfl_up_sync(0xffffffffu, c, 1);
+                if (lane == 0) prev = before;
+                const unsigned hit = __ballot_sync(0xffffffffu, w >= 0.0 && c > target);
+                if (hit == 0u) {
+                    err = -1;  // the two rounding paths disagree
+                } else {
+                    const int first = __ffs(hit) - 1;
+                    const double hi = __shfl_sync(0xffffffffu, c, first);
+                    const double lo = __shfl_sync(0xffffffffu, prev, first);
+                    cand = G * 32 + first;
+                    if (slack >= 0.0 && (hi - target <= slack || target - lo <= slack)) err = -1;
+                }
+            }
+            if (lane == 0) sh.u = u;
+        }
+        if (lane == 0) {
+            sh.err = err;
+            sh.cand = cand;
+        }
+    }
+    __syncthreads();
+    const long long r = sh.err == 2 ? -2 : (sh.err == -1 ? -1 : sh.cand);
+    __syncthreads();
+    return r;
+}
+
 __device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const double* gs,
                          long long* out_row, SelShared& sh) {
     const int tid = threadIdx.x;
     const long long m = P.m;
+    const long long ng = (m + 31) / 32;
     if (tid == 0) AXB_STAMP(1);
-    long long g0, g1;
-    double excl;
-    const double total = grbk_prefix(gs, (m + 31) / 32, sh, g0, g1, excl);
-    if (tid == 0) AXB_STAMP(2);
-    if (!(total > 0.0)) return 2;  // mass on zero rows only (solver.hpp:249-252)
-    if (tid == 0) {
-        sh.u = rng_unit(st->rng);
-        sh.target = __dmul_rn(sh.u, total);
+    long long pick;
+    if (ng <= 1024) {
+        pick = grbk_pick_warp(P, st, mem, gs, ng, sh);
+        if (tid == 0) AXB_STAMP(2);
+        if (pick == -2) return 2;
+    } else {
+        long long g0, g1;
+        double excl;
+        const double total = grbk_prefix(gs, ng, sh, g0, g1, excl);
+        if (tid == 0) AXB_STAMP(2);
+        if (!(total > 0.0)) return 2;  // mass on zero rows only (solver.hpp:249-252)
+        if (tid == 0) {
+            sh.u = rng_unit(st->rng);
+            sh.target = __dmul_rn(sh.u, total);
+        }
+        __syncthreads();
+        const double slack = P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
+        pick = grbk_search(mem, m, gs, g0, g1, excl, sh.target, slack, sh);
     }
-    __syncthreads();
-    const double slack = P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
-    long long pick = grbk_search(mem, m, gs, g0, g1, excl, sh.target, slack, sh);
     if (tid == 0) {
         AXB_STAMP(3);
         st->dbg[5] += 1;  // selections
@@ -1560,8 +1734,36 @@ struct SoloGroup {
     __device__ void sync() { __syncthreads(); }
 };
 
+// per-phase time of the persistent body (CTA 0, thread 0) into DevState::dbg:
+// select, y, z-partials+X, z-combine, R update, finalize, barrier waits, iterations
+// (build with -DAXB_TRACE_PERSIST; read with axb_solver_debug_state)
+#ifdef AXB_TRACE_PERSIST
+#define PT_DECL unsigned long long pt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt_t = 0
+#define PT_MARK(slot)                                          \
+    do {                                                       \
+        if (tid == 0 && grid.rank() == 0) {                    \
+            unsigned long long t_;                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+            if ((slot) >= 0 && pt_t) pt_acc[(slot)] += t_ - pt_t; \
+            pt_t = t_;                                         \
+        }                                                      \
+    } while (0)
+#define PT_ITER() (pt_acc[7] += (tid == 0 && grid.rank() == 0))
+#define PT_STORE()                                                   \
+    do {                                                             \
+        if (tid == 0 && grid.rank() == 0)                            \
+            for (int s_ = 0; s_ < 8; ++s_) P.st->dbg[s_] = pt_acc[s_]; \
+    } while (0)
+#else
+#define PT_DECL
+#define PT_MARK(slot) ((void)0)
+#define PT_ITER() ((void)0)
+#define PT_STORE() ((void)0)
+#endif
+
 template <class Grp, int kT>
 __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
+    PT_DECL;
     constexpr int kW = kT / 32;
     constexpr int kSub = kT / kPersistThreads;  // 256-thread sub-blocks (z items)
     extern __shared__ double pscratch[];  // selection scratch: ⌈m/32⌉ group sums
@@ -1577,6 +1779,8 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
     __syncthreads();
     for (;;) {
         if (lst.status != ST_RUN || lst.k >= lst.k_limit) break;
+        PT_MARK(-1);
+        PT_ITER();
         if (!lst.sel_valid) {  // K3 (every CTA, identically)
             long long row = 0;
             if (tid == 0) sh.err = 0;
@@ -1598,6 +1802,7 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             __syncthreads();
             if (lst.status != ST_RUN) break;
         }
+        PT_MARK(0);
         const long long sel = lst.sel;
         const double coef = lst.coef;
         const double* Ri = P.R + sel * n;
@@ -1632,7 +1837,9 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
                 }
             }
         }
+        PT_MARK(1);
         grid.sync();
+        PT_MARK(6);
         // ---- z = yᵀ·B, stage 1: (column slab × row chunk) partials; X update ----
         {
             const int items = P.z_nslab * P.z_nj;
@@ -1690,7 +1897,9 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         }
         xacc = block_sum(xacc, red);
         if (tid == 0) P.xpart[grid.rank()] = xacc;
+        PT_MARK(2);
         grid.sync();
+        PT_MARK(6);
         // ---- z stage 2: fixed-order combine of the row-chunk partials ----
         for (long long c = (long long)grid.rank() * kT + tid; c < n;
              c += (long long)grid.size() * kT) {
@@ -1698,7 +1907,9 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             for (int k = 0; k < P.z_nj; ++k) a += __ldcg(P.zpart + (long long)k * n + c);
             P.z[c] = a;
         }
+        PT_MARK(3);
         grid.sync();
+        PT_MARK(6);
         // ---- R update + row norms (warp per row, static mapping) ----
         // Pointers are hoisted into registers: P may live in shared memory
         // (k_persist_batch) and a generic store could alias it otherwise.
@@ -1847,7 +2058,9 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             }
             P.rrec[grid.rank()] = RowRecord{a, mx, ax, 0.0};
         }
+        PT_MARK(4);
         grid.sync();
+        PT_MARK(6);
         // ---- every CTA: reduce the records + the ‖X−X_ref‖² partials (block-
         // parallel loads, fixed-order trees → identical in every CTA), finalize ----
         {
@@ -1901,11 +2114,13 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             }
         }
         __syncthreads();
+        PT_MARK(5);
         // no barrier needed before the next y phase: it only reads R/B (last
         // written before the grid.sync above) and writes y, which nobody reads
         // until after the next grid.sync
     }
     if (grid.rank() == 0 && tid == 0) *P.st = lst;
+    PT_STORE();
 }
 
 __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
@@ -1923,6 +2138,377 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_persist_batch(const Params
     persist_body<SoloGroup, kBatchThreads>(sp, SoloGroup{});
 }
 
+// ------------------------------------------------------------------------
+// Latency body for small systems (m ≤ kPersistLatRows, BᵀB cached).  A tiny
+// system's iteration is a chain of L2 round trips and barriers, not bytes, so
+// this body minimises both:
+//   * the selection state (r_sq, a_sq, the RBK CDF, the greedy group sums)
+//     lives in shared memory; every CTA refreshes r_sq with one batched L2
+//     pass per iteration, reduces ‖R‖², max/argmax and ‖X−X_ref‖² from it in a
+//     fixed order (identical in every CTA), and selects from shared memory;
+//   * z = BᵀB·R_iᵀ with the cached n×n BᵀB — the reference's own formula
+//     (solver.hpp:172, :293) — so y and z are both dots with R_i and share one
+//     phase, and an iteration needs two grid barriers:
+//         [select] y, z (, g) ─sync─ R update ∥ X update ─sync─ [reduce]
+//   * loads are issued 8 per lane ahead of the arithmetic (one round trip per
+//     row at config-1 widths); X rows go to the last warps, R rows to the first.
+// ------------------------------------------------------------------------
+__host__ __device__ __forceinline__ size_t persist_lat_smem_doubles(long long m, int) {
+    return (size_t)((m + 31) / 32) + 3 * (size_t)m;
+}
+
+template <class Grp, int kT>
+__device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
+    PT_DECL;
+    constexpr int kW = kT / 32;
+    constexpr int kU = kT <= 256 ? 8 : 4;  // loads in flight per lane (register budget)
+    constexpr int kR = 4;  // R-row pairs: 3 streams per lane
+    extern __shared__ __align__(16) double psm[];
+    __shared__ DevState lst;
+    __shared__ SelShared sh;
+    __shared__ double red[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long m = P.m, n = P.n, p = P.p, q = P.q;
+    const long long ng = (m + 31) / 32;
+    double* const gs = psm;
+    double* const rs_s = gs + ng;
+    double* const as_s = rs_s + m;
+    double* const cum_s = as_s + m;
+    const int G = grid.size(), rank = grid.rank();
+    const long long gw = (long long)rank * kW + warp;
+    const long long nw = (long long)G * kW;
+    // pointers hoisted into registers: P may live in shared memory
+    const double* const Bb = P.B;
+    const double* const BtB = P.BtB;
+    const double* const Ab = P.A;
+    const double* const Gm = P.G;
+    const double* const asq_g = P.a_sq;
+    double* const Rb = P.R;
+    double* const Xb = P.X;
+    const double* const Xrefb = P.Xref;
+    double* const yo = P.y;
+    double* const zo = P.z;
+    double* const go = P.g;
+    double* const rsq = P.r_sq;
+    double* const xpart = P.xpart;
+    const bool vec2 = (n & 1) == 0;
+    const int method = P.method;
+    if (tid == 0) lst = *P.st;
+    for (long long i = tid; i < m; i += kT) {
+        as_s[i] = asq_g[i];
+        rs_s[i] = __ldcg(rsq + i);
+        cum_s[i] = method == 1 ? P.rbk_cum[i] : 0.0;
+    }
+    __syncthreads();
+
+    // X_t += (coef·A_it)·y (solver.hpp:272-289), warp per row, rows taken from the
+    // LAST warps (the R rows start at the first), so a warp rarely does both;
+    // each warp's Σ (X − X_ref)² goes to xpart[gw] (fixed slots, fixed order)
+    auto x_update = [&](const double* Ai, double coef) {
+        double xacc = 0.0;
+        for (long long t = nw - 1 - gw; t < p; t += nw) {
+            const double f = __dmul_rn(coef, Ai[t]);
+            double* xr = Xb + t * q;
+            const double* rr = Xrefb ? Xrefb + t * q : nullptr;
+            for (long long k0 = lane; k0 < q; k0 += 32 * kR) {
+                double xv[kR], yv[kR], rv[kR];
+#pragma unroll
+                for (int u = 0; u < kR; ++u) {
+                    const long long k = k0 + 32 * u;
+                    if (k < q) {
+                        xv[u] = xr[k];
+                        yv[u] = __ldcg(yo + k);
+                        rv[u] = rr ? rr[k] : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kR; ++u) {
+                    const long long k = k0 + 32 * u;
+                    if (k < q) {
+                        const double x1 = __dadd_rn(xv[u], __dmul_rn(f, yv[u]));
+                        xr[k] = x1;
+                        if (rr) {
+                            const double d1 = x1 - rv[u];
+                            xacc += d1 * d1;
+                        }
+                    }
+                }
+            }
+        }
+        xacc = warp_sum(xacc);
+        // slot = the warp's first X row: only the min(p, nw) X-owning warps write
+        if (lane == 0 && nw - 1 - gw < p) xpart[nw - 1 - gw] = xacc;
+    };
+
+    for (;;) {
+        if (lst.status != ST_RUN || lst.k >= lst.k_limit) break;
+        PT_MARK(-1);
+        PT_ITER();
+        if (!lst.sel_valid) {  // K3 from shared memory (every CTA, identically)
+            long long row = 0;
+            if (tid == 0) sh.err = 0;
+            __syncthreads();
+            const int err = select_rows(P, &lst, method, P.theta, &row, sh, gs, ng, as_s, rs_s,
+                                        method == 1 ? cum_s : nullptr);
+            __syncthreads();
+            if (tid == 0) {
+                if (err) {
+                    lst.status = ST_ERROR;
+                    lst.err_code = err;
+                    lst.err_k = lst.k;
+                } else {
+                    lst.sel = row;
+                    lst.coef = __ddiv_rn(P.alpha, as_s[row]);
+                    lst.sel_valid = 1;
+                }
+            }
+            __syncthreads();
+            if (lst.status != ST_RUN) break;
+#ifdef AXB_TRACE_PERSIST
+            if (tid == 0 && rank == 0 && (method == 2 || method == 3)) {
+                unsigned long long t_;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+                pt_acc[3] += t_ - sh.t_groups;
+            }
+#endif
+        }
+        PT_MARK(0);
+        const long long sel = lst.sel;
+        const double coef = lst.coef;
+        const double* Ri = Rb + sel * n;
+        const double* Ai = Ab + sel * p;
+        // ---- phase A: y = B·R_iᵀ and z = BᵀB·R_iᵀ (dots with R_i), g = A·A_iᵀ ----
+        {
+            const long long nd = q + n;
+            for (long long it = gw; it < nd; it += 2 * nw) {
+                const long long it1 = it + nw;
+                const double* r0 = it < q ? Bb + it * n : BtB + (it - q) * n;
+                const double* r1 =
+                    it1 < nd ? (it1 < q ? Bb + it1 * n : BtB + (it1 - q) * n) : nullptr;
+                double a0, a1;
+                warp_dot_pair_u<kU>(r0, r1, Ri, n, lane, vec2, true, a0, a1);
+                if (lane == 0) {
+                    if (it < q) yo[it] = a0;
+                    else zo[it - q] = a0;
+                    if (r1) {
+                        if (it1 < q) yo[it1] = a1;
+                        else zo[it1 - q] = a1;
+                    }
+                }
+            }
+            if (!Gm) {
+                for (long long it = gw; it < m; it += 2 * nw) {
+                    const long long it1 = it + nw;
+                    double a0, a1;
+                    warp_dot_pair(Ab + it * p, it1 < m ? Ab + it1 * p : nullptr, Ai, p, lane,
+                                  (p & 1) == 0, false, a0, a1);
+                    if (lane == 0) {
+                        go[it] = a0;
+                        if (it1 < m) go[it1] = a1;
+                    }
+                }
+            }
+        }
+        PT_MARK(1);
+        grid.sync();
+        PT_MARK(6);
+        // ---- phase C: R_l −= (coef·G_il)·z, ‖R_l‖² (solver.hpp:294-305); X ----
+        {
+            const double* const Gsel = Gm ? Gm + sel * m : nullptr;
+            auto coef_of = [&](long long l) { return Gsel ? __ldg(Gsel + l) : __ldcg(go + l); };
+            if (vec2) {
+                const long long h = n >> 1;
+                const double2* z2 = reinterpret_cast<const double2*>(zo);
+                for (long long l0 = gw; l0 < m; l0 += 2 * nw) {
+                    const long long l1 = l0 + nw;
+                    const bool has1 = l1 < m;
+                    const double g0 = coef_of(l0);
+                    const double g1 = has1 ? coef_of(l1) : 0.0;
+                    const bool up0 = g0 != 0.0, up1 = g1 != 0.0;  // sparse-G skip (:294-295)
+                    if (!(up0 || up1)) continue;
+                    const double f0 = __dmul_rn(coef, g0), f1 = __dmul_rn(coef, g1);
+                    double2* row0 = reinterpret_cast<double2*>(Rb + l0 * n);
+                    double2* row1 = reinterpret_cast<double2*>(Rb + (has1 ? l1 : l0) * n);
+                    double acc0 = 0.0, acc1 = 0.0;
+                    for (long long k0 = lane; k0 < h; k0 += 32 * kR) {
+                        double2 zv[kR], r0[kR], r1[kR];
+#pragma unroll
+                        for (int u = 0; u < kR; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < h) {
+                                zv[u] = __ldcg(z2 + k);
+                                if (up0) r0[u] = __ldcg(row0 + k);
+                                if (up1) r1[u] = __ldcg(row1 + k);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kR; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < h) {
+                                if (up0) {
+                                    double2 r;
+                                    r.x = __dsub_rn(r0[u].x, __dmul_rn(f0, zv[u].x));
+                                    r.y = __dsub_rn(r0[u].y, __dmul_rn(f0, zv[u].y));
+                                    row0[k] = r;
+                                    acc0 += r.x * r.x;
+                                    acc0 += r.y * r.y;
+                                }
+                                if (up1) {
+                                    double2 r;
+                                    r.x = __dsub_rn(r1[u].x, __dmul_rn(f1, zv[u].x));
+                                    r.y = __dsub_rn(r1[u].y, __dmul_rn(f1, zv[u].y));
+                                    row1[k] = r;
+                                    acc1 += r.x * r.x;
+                                    acc1 += r.y * r.y;
+                                }
+                            }
+                        }
+                    }
+                    if (up0) {
+                        const double rs0 = warp_sum(acc0);
+                        if (lane == 0) rsq[l0] = rs0;
+                    }
+                    if (up1) {
+                        const double rs1 = warp_sum(acc1);
+                        if (lane == 0) rsq[l1] = rs1;
+                    }
+                }
+            } else {
+                for (long long l = gw; l < m; l += nw) {
+                    const double gl = coef_of(l);
+                    if (gl == 0.0) continue;  // R_l unchanged (solver.hpp:294-295)
+                    const double f = __dmul_rn(coef, gl);
+                    double* row = Rb + l * n;
+                    double acc = 0.0;
+                    for (long long k0 = lane; k0 < n; k0 += 32 * kU) {
+                        double rv[kU], zv[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < n) {
+                                rv[u] = __ldcg(row + k);
+                                zv[u] = __ldcg(zo + k);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const long long k = k0 + 32 * u;
+                            if (k < n) {
+                                const double r = __dsub_rn(rv[u], __dmul_rn(f, zv[u]));
+                                row[k] = r;
+                                acc += r * r;
+                            }
+                        }
+                    }
+                    const double rs = warp_sum(acc);
+                    if (lane == 0) rsq[l] = rs;
+                }
+            }
+            x_update(Ai, coef);
+        }
+        PT_MARK(4);
+        grid.sync();
+        PT_MARK(6);
+        // ---- phase D (every CTA): refresh r_sq, fixed-order reductions, finalize ----
+        {
+            double ps = 0.0, pm = -INFINITY, pe = 0.0;
+            long long pa = LLONG_MAX;
+            // loads batched 8 per thread ahead of the arithmetic: one L2 round
+            // trip per 8·kT rows instead of one per kT
+            for (long long i0 = tid; i0 < m; i0 += 8 * kT) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const long long i = i0 + (long long)u * kT;
+                    v[u] = i < m ? __ldcg(rsq + i) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const long long i = i0 + (long long)u * kT;
+                    if (i < m) {
+                        rs_s[i] = v[u];
+                        ps += v[u];
+                        const double as = as_s[i];
+                        if (as > 0.0) maxidx_merge(pm, pa, __ddiv_rn(v[u], as), i);
+                    }
+                }
+            }
+            const long long nx = min(p, nw);
+            for (long long b0 = tid; b0 < nx; b0 += 4 * kT) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const long long b = b0 + (long long)u * kT;
+                    v[u] = b < nx ? __ldcg(xpart + b) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) pe += v[u];
+            }
+            // one fused pass: warp trees, then thread 0 over the warps in order
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ps += __shfl_xor_sync(0xffffffffu, ps, o);
+                pe += __shfl_xor_sync(0xffffffffu, pe, o);
+                const double ov = __shfl_xor_sync(0xffffffffu, pm, o);
+                const long long oi = __shfl_xor_sync(0xffffffffu, pa, o);
+                maxidx_merge(pm, pa, ov, oi);
+            }
+            if (lane == 0) {
+                red[warp] = ps;
+                sh.scan[warp] = pe;
+                sh.redv[warp] = pm;
+                sh.redi[warp] = pa;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                ps = 0.0;
+                pe = 0.0;
+                pm = -INFINITY;
+                pa = LLONG_MAX;
+                for (int w = 0; w < kW; ++w) {
+                    ps += red[w];
+                    pe += sh.scan[w];
+                    maxidx_merge(pm, pa, sh.redv[w], sh.redi[w]);
+                }
+                lst.r_fro_sq = ps;
+                lst.max_ratio = pm;
+                lst.argmax = pa;
+                lst.err_sq = pe;
+                lst.sel_valid = 0;
+                const double cf = P.c_fro > 0.0 ? P.c_fro : 1.0;
+                const double rel = sqrt(ps > 0.0 ? ps : 0.0) / cf;
+                if (!isfinite(ps)) {  // solver.hpp:306-307
+                    lst.status = ST_ERROR;
+                    lst.err_code = 4;
+                    lst.err_k = lst.k;
+                    lst.err_val = sqrt(fabs(ps));
+                } else {
+                    const unsigned long long k = lst.k;
+                    const double metric = P.stop_kind == 0 ? pe / P.ref_sq : rel;
+                    const unsigned long long slot = k - lst.k0;
+                    if (rank == 0 && slot < P.trace_cap) {
+                        P.trace_row[slot] = sel;
+                        P.trace_metric[slot] = metric;
+                        P.trace_rel[slot] = rel;
+                    }
+                    lst.k = k + 1;
+                    lst.metric = metric;
+                    if (lst.run_mode && metric <= P.tol) lst.status = ST_PAUSE;
+                    else if (lst.run_mode && !(ps > 0.0)) lst.status = ST_ZERO;
+                }
+            }
+            __syncthreads();
+        }
+        PT_MARK(5);
+    }
+    if (rank == 0 && tid == 0) *P.st = lst;
+    PT_STORE();
+}
+
+template <int kT>
+__global__ void __launch_bounds__(kT, 1) k_persist_lat(Params P) {
+    persist_body_lat<GridGroup, kT>(P, GridGroup{cooperative_groups::this_grid()});
+}
 
 int persist_grid(const Params& P) {
     int dev = 0, sms = 0, per = 0;
@@ -2383,6 +2969,8 @@ void launch_sel_greedy(const Params& P, cudaStream_t s) {
     launch_pdl(k_sel_greedy, P.sel_grid, kThreads, 0, s, P);
 }
 
+// (batched systems run the general body: one CTA owns a system, so the latency
+// body's per-CTA refresh of every r_sq buys nothing there — measured slower)
 int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStream_t s) {
     const size_t smem = sizeof(double) * (size_t)((max_m + 31) / 32);
     if (smem > 48 * 1024)
@@ -2392,6 +2980,22 @@ int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStre
 }
 
 int launch_persist(const Params& P, cudaStream_t s) {
+    if (P.persist_lat) {
+        const int threads = P.persist_lat == 128 ? 128 : 256;
+        const void* fn = threads == 128 ? (const void*)k_persist_lat<128> : (const void*)k_persist_lat<256>;
+        const size_t smem = sizeof(double) * persist_lat_smem_doubles(P.m, threads);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
+        const int grid = std::min(P.persist_grid, std::max(1, sms * std::min(per, 1)));
+        Params Pc = P;
+        void* args[] = {&Pc};
+        return (int)cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(threads), args,
+                                                smem, s);
+    }
     const int grid = std::min(P.persist_grid, persist_grid(P));
     const size_t smem = sizeof(double) * (size_t)((P.m + 31) / 32);
     Params Pc = P;

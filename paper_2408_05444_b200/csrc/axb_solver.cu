@@ -190,7 +190,7 @@ struct axb_solver {
     axb_options opt{};
     cudaStream_t stream = nullptr;
     DevBuf<double> A, B, C, R, X, Xref, a_sq, rbk_cum, r_sq, G, g, y, z, zpart, xpart, T,
-        gemm_sq, gemm_diff, scal, tr_metric, tr_rel, sq_part, gsum;
+        gemm_sq, gemm_diff, scal, tr_metric, tr_rel, sq_part, gsum, BtB;
     DevBuf<unsigned int> zcnt;
     DevBuf<RowRecord> rrec;
     DevBuf<long long> tr_row, forced;
@@ -649,6 +649,39 @@ struct axb_solver {
             // grid: enough SMs for the L2 bandwidth of R, few enough for cheap grid syncs
             const int want = (int)std::min<double>(sms, std::max(64.0, (double)m * n / 16384.0));
             P.persist_grid = env_int("AXB_PERSIST_GRID", want);
+            // latency body (selection state in shared memory, z = BᵀB·R_iᵀ, two grid
+            // barriers per iteration) when BᵀB is small enough to cache: tiny
+            // systems such as config 1.  AXB_PERSIST_LAT = threads per CTA (256 or
+            // 128), 0 = off; AXB_PERSIST_BTB = 1 forces it for larger n.
+            const int lat_env = env_int("AXB_PERSIST_LAT", 256);
+            const int bforce = env_int("AXB_PERSIST_BTB", -1);
+            const bool btb_ok = bforce == 1 || (bforce < 0 && 8.0 * (double)n * (double)n <= 4e6);
+            P.persist_lat = (P.persist && (long long)m <= kPersistLatRows && lat_env != 0 && btb_ok)
+                                ? (lat_env == 128 ? 128 : 256) : 0;
+            // latency-bound: every SM's load parallelism, barrier cost barely grows
+            if (P.persist_lat) P.persist_grid = env_int("AXB_PERSIST_GRID", sms);
+        }
+        // z = BᵀB·R_iᵀ in the latency body (btb_, solver.hpp:172, :293): y and z
+        // then share one phase; cached when BᵀB is small (L2-resident)
+        P.BtB = nullptr;
+        if (P.persist_lat) {
+            {
+                BtB.alloc(n * n, "BtB");
+                DevBuf<double> Bt;
+                Bt.alloc(q * n, "B transposed");
+                launch_transpose(B.p, (long long)q, (long long)n, Bt.p, stream);
+                GemmArgs ga{};
+                ga.M = n; ga.N = n; ga.K = q;
+                ga.A = Bt.p; ga.lda = q;
+                ga.B = Bt.p; ga.ldb = q; ga.b_trans = 1;
+                ga.D = BtB.p; ga.ldd = n;
+                ga.store = 1;
+                ga.sym = 1;
+                launch_gemm(ga, stream);
+                launch_mirror_lower(BtB.p, (long long)n, (long long)n, stream);
+                sync("BtB");  // Bt released at scope end
+                P.BtB = BtB.p;
+            }
         }
         P.vec2 = (n % 2) == 0;
 

@@ -46,12 +46,15 @@ def pair(axb, orc, A, B, Cm, X0, tag, theta=None, seed=0, Xref=None, refresh=0, 
     return so, sg
 
 
-@pytest.fixture(params=["persistent", "graph"])
+@pytest.fixture(params=["persistent", "cooperative", "graph"])
 def path(request, monkeypatch):
-    """Small systems default to the persistent cooperative kernel; "graph" forces
-    the CUDA-graph path (K4/K4b/TMA-K2 launches) on the same inputs."""
+    """Small systems default to the persistent kernel (tiny ones — cached BᵀB —
+    on its latency body); "cooperative" forces the general persistent body,
+    "graph" the CUDA-graph path (K4/K4b/TMA-K2 launches), same inputs."""
     if request.param == "graph":
         monkeypatch.setenv("AXB_PERSIST", "0")
+    if request.param == "cooperative":
+        monkeypatch.setenv("AXB_PERSIST_LAT", "0")
     return request.param
 
 
