@@ -19,9 +19,10 @@ iterations / max-over-ranks device time.  A is generated in 8 fixed row blocks,
 so the global system is bit-identical at N = 1, 2, 4, 8.  --shard forces the
 sharded code path on one GPU (1-rank communicator).
 
---impl reference: the reference's per-iteration algorithm on the host cores (the
-oracle C port, bitwise-pinned to the reference; kind "port"), one solver per core
-as the reference's benchmark pool runs trials (analysis.hpp:295-313).
+--impl reference: the reference's own engine on the host cores — the unmodified
+axb::Solver compiled from /root/reference into oracle/_ref (kind "reference"; the
+bitwise-equal C port only where _ref is absent) — one solver per core as the
+reference's benchmark pool runs trials (analysis.hpp:295-313).
 """
 from __future__ import annotations
 
@@ -240,47 +241,76 @@ def cpu_baseline(cfg, budget_s=15.0):
 
 
 def reference_arm(args, cfg):
+    """The reference's own CPU implementation of the path on the host cores: the
+    UNMODIFIED reference engine (axb::Solver from /root/reference/proj/include,
+    compiled with its Release flags into oracle/_ref/libaxbref.so; kind
+    "reference"), one solver per host thread as the reference's benchmark pool
+    runs trials (analysis.hpp:295-313).  Falls back to the bitwise-equal C port
+    (kind "port") only where _ref was not built.  Config 5 runs on the exact
+    1/8-per-dimension instance (its own constructor: G = A·Aᵀ, BᵀB, R0, ‖B‖₂ by
+    the reference's power iteration), time extrapolated ×64."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
     import oracle_lib as O
 
-    orc = O.oracle()
     T = max(1, min(os.cpu_count() or 1, args.ref_threads))
-    log(f"[reference] preparing {cfg['desc']} on the host; {T} solver threads")
+    kind = "reference" if O.ref_available() else "port"
     scfg, factor = cpu_sample_cfg(cfg)
+    log(f"[reference] {cfg['desc']}: {kind} engine, {T} solver threads, instance "
+        f"{scfg['m']}x{scfg['p']}.{scfg['q']}x{scfg['n']}")
     state = cpu_prepared_state(scfg, 7)
-    solvers = [cpu_solver(O, orc, state, 42 + t) for t in range(T)]
-    per = max(1, math.ceil(args.steps / T))
-    budget = args.ref_budget_s
+    solvers = [None] * T
+    if kind == "reference":
+        lib = O.ref()
+        X0 = None if not np.any(state["X0"]) else state["X0"]
+
+        def build(t):
+            cfg_o = O.make_config(method=O.GRBK, stop_kind=O.SOLUTION_RRN, tol=1e-12,
+                                  reference=state["Xs"], seed=42 + t, refresh_interval=0)
+            solvers[t] = O.Solver(lib, state["A"], state["B"], state["C"], X0, cfg_o)
+    else:
+        orc = O.oracle()
+
+        def build(t):
+            solvers[t] = cpu_solver(O, orc, state, 42 + t)[0]
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=build, args=(t,)) for t in range(T)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    log(f"[reference] {T} constructors in {time.perf_counter() - t0:.1f}s")
     # warmup (W iterations spread over the pool)
     wper = max(1, math.ceil(args.warmup / T))
-    for s, _ in solvers:
+    for s in solvers:
         s.steps(wper)
     # calibrate: bound the sample so the run stays within the budget
     t0 = time.perf_counter()
-    solvers[0][0].steps(1)
+    solvers[0].steps(1)
     one = time.perf_counter() - t0
-    per = max(1, min(per, int(budget / max(one, 1e-9) / 1.5)))
+    per = max(1, math.ceil(args.steps / T))
+    per = max(1, min(per, int(args.ref_budget_s / max(one, 1e-9) / 1.5)))
     per = max(per, min(int(10.0 / max(one, 1e-9)), 10 ** 6))  # at least ~10 s of CPU work
     counts = [0] * T
 
     def work(t):
-        s = solvers[t][0]
-        s.steps(per)
+        solvers[t].steps(per)
         counts[t] = per
 
     threads = [threading.Thread(target=work, args=(t,)) for t in range(T)]
     t0 = time.perf_counter()
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join()
+    for x in threads:
+        x.start()
+    for x in threads:
+        x.join()
     dt = time.perf_counter() - t0
     total = sum(counts)
     value = total / dt / factor
-    cores = T
     shape = f"{scfg['m']}x{scfg['p']}.{scfg['q']}x{scfg['n']}"
     extra = (f"; instance {shape} (every dimension /{cfg['cpu_div']}), time extrapolated "
              f"x{factor}" if factor > 1 else "")
+    engine = ("unmodified reference axb::Solver::step() (oracle/_ref, -O3 -DNDEBUG)"
+              if kind == "reference" else "oracle C port of solver.hpp step()")
     line = {
         "impl": "reference",
         "metric": "kaczmarz_iterations_per_sec", "value": value, "unit": "iter/s",
@@ -290,10 +320,9 @@ def reference_arm(args, cfg):
         "data": "synthetic (numpy seeded N(0,1))",
         "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
                    "n": cfg["n"], "method": "grbk", "parallelism": f"{T} independent solves"},
-        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": T, "kind": kind,
                          "sample": f"{T} concurrent solves x {per} iterations (reference "
-                                   f"benchmark-pool pattern), oracle C port of solver.hpp "
-                                   f"step(), {dt:.1f}s wall{extra}"},
+                                   f"benchmark-pool pattern), {engine}, {dt:.1f}s wall{extra}"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
