@@ -356,3 +356,25 @@ def test_odd_width_register_streaming_path(axb, orc, tag, path):
     assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
     assert rel(sg.X(), so.X()) <= RTOL_X
     assert rel(sg.R(), so.R()) <= 1e-9
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1, 1), (3, 2, 5, 7), (40, 1500, 2, 6), (33, 5, 3, 1)])
+@pytest.mark.parametrize("tag", [O.GRBK, O.MWRBK, O.RBK])
+def test_degenerate_shapes(axb, orc, shape, tag, path):
+    """Edge shapes on every path: a 1×1 system, odd tiny widths, more X rows than
+    the persistent grid has warps (p = 1500), single-column R."""
+    m, p, q, n = shape
+    A, B, X, Cm = O.generate(orc, 17, m, p, q, n)
+    so, sg = pair(axb, orc, A, B, Cm, None, tag, seed=6, Xref=X)
+    try:
+        ro = so.steps(300)
+    except Exception as e:  # 1×1 GRBK: R = 0 after one step → DomainError (solver.hpp:235)
+        assert getattr(e, "code", None) == 2, e
+        with pytest.raises(axb.DomainError):
+            sg.steps(300)
+        assert sg.iteration() == so.iteration
+        return
+    rg = sg.steps(300)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
