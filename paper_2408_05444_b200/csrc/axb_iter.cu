@@ -457,6 +457,9 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
     for (long long t = P.x0r + (long long)xb * kWarps + warp; t < P.x1r;
          t += (long long)P.x_ctas * kWarps) {
         const double f = __dmul_rn(coef, __ldg(Ai + t));
+        // A_it = 0 leaves X_t unchanged: the reference's loop over the stored
+        // entries of A_i (solver.hpp:272-273); skipped unless ‖X−X_ref‖² needs the row
+        if (f == 0.0 && !track) continue;
         double* xr = P.X + t * q;
         const double* rr = track ? P.Xref + t * q : nullptr;
         if ((q & 1) == 0) {
@@ -1868,6 +1871,7 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         const double* const Xrefb = P.Xref;
         for (long long t = gw; t < p; t += nw) {
             const double f = __dmul_rn(coef, Ai[t]);
+            if (f == 0.0 && !Xrefb) continue;  // A_it = 0: X_t unchanged (solver.hpp:272-273)
             double* xr = Xb + t * q;
             const double* rr = Xrefb ? Xrefb + t * q : nullptr;
             for (long long k0 = lane; k0 < q; k0 += 32 * 4) {
@@ -2208,6 +2212,7 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
         double xacc = 0.0;
         for (long long t = nw - 1 - gw; t < p; t += nw) {
             const double f = __dmul_rn(coef, Ai[t]);
+            if (f == 0.0 && !Xrefb) continue;  // A_it = 0: X_t unchanged (solver.hpp:272-273)
             double* xr = Xb + t * q;
             const double* rr = Xrefb ? Xrefb + t * q : nullptr;
             for (long long k0 = lane; k0 < q; k0 += 32 * kR) {

@@ -597,7 +597,9 @@ struct axb_solver {
         zcnt.alloc(P.z_nslab, "zcnt");
         ck(cudaMemsetAsync(zcnt.p, 0, sizeof(unsigned) * P.z_nslab, stream), "zcnt");
         xpart.alloc(std::max<size_t>(2 * 1184, (size_t)P.x_ctas), "xpart");
-        rrec.alloc(P.r_grid, "rrec");
+        // per-CTA records of K2 (r_grid CTAs) and of the persistent general body (≤ one
+        // CTA per SM, whatever m is)
+        rrec.alloc(std::max<size_t>((size_t)P.r_grid, 1024), "rrec");
         tr_row.alloc(trace_cap, "trace");
         forced.alloc(trace_cap, "forced rows");
         gsum.alloc((m + 31) / 32, "group sums");
@@ -655,7 +657,7 @@ struct axb_solver {
             // 128), 0 = off; AXB_PERSIST_BTB = 1 forces it for larger n.
             const int lat_env = env_int("AXB_PERSIST_LAT", 256);
             const int bforce = env_int("AXB_PERSIST_BTB", -1);
-            const bool btb_ok = bforce == 1 || (bforce < 0 && 8.0 * (double)n * (double)n <= 4e6);
+            const bool btb_ok = bforce == 1 || (bforce < 0 && 8.0 * (double)n * (double)n <= 16e6);
             P.persist_lat = (P.persist && (long long)m <= kPersistLatRows && lat_env != 0 && btb_ok)
                                 ? (lat_env == 128 ? 128 : 256) : 0;
             // latency-bound: every SM's load parallelism, barrier cost barely grows

@@ -358,23 +358,27 @@ def test_odd_width_register_streaming_path(axb, orc, tag, path):
     assert rel(sg.R(), so.R()) <= 1e-9
 
 
-@pytest.mark.parametrize("shape", [(1, 1, 1, 1), (3, 2, 5, 7), (40, 1500, 2, 6), (33, 5, 3, 1)])
+@pytest.mark.parametrize("shape,steps", [((1, 1, 1, 1), 300), ((3, 2, 5, 7), 300),
+                                         ((40, 1500, 2, 6), 300), ((33, 5, 3, 1), 20)])
 @pytest.mark.parametrize("tag", [O.GRBK, O.MWRBK, O.RBK])
-def test_degenerate_shapes(axb, orc, shape, tag, path):
+def test_degenerate_shapes(axb, orc, shape, steps, tag, path):
     """Edge shapes on every path: a 1×1 system, odd tiny widths, more X rows than
-    the persistent grid has warps (p = 1500), single-column R."""
+    the persistent grid has warps (p = 1500), single-column R.  The single-column
+    system's residual collapses to rounding noise (1e-14 of its start by step 30,
+    1e-30 by step 70), where the reference's own running ‖R‖² drifts and greedy
+    membership is decided by noise; it is compared over its first 20 steps."""
     m, p, q, n = shape
     A, B, X, Cm = O.generate(orc, 17, m, p, q, n)
     so, sg = pair(axb, orc, A, B, Cm, None, tag, seed=6, Xref=X)
     try:
-        ro = so.steps(300)
+        ro = so.steps(steps)
     except Exception as e:  # 1×1 GRBK: R = 0 after one step → DomainError (solver.hpp:235)
         assert getattr(e, "code", None) == 2, e
         with pytest.raises(axb.DomainError):
-            sg.steps(300)
+            sg.steps(steps)
         assert sg.iteration() == so.iteration
         return
-    rg = sg.steps(300)
+    rg = sg.steps(steps)
     mism = np.nonzero(ro != rg)[0]
     assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
     assert rel(sg.X(), so.X()) <= RTOL_X
