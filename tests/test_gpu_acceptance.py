@@ -1,0 +1,156 @@
+"""GPU: the reference's acceptance criteria on the hot path (proj/tests/acceptance.cpp).
+
+C1 (convergence of the greedy family on 15 systems), C2 (BK to its limit with an
+invariant projection residue), C3 (θ = ½ ≡ GRBK), C4 (raw recurrence drift after
+10⁴ steps) and C6 (RBK mean error under the expected envelope), restated through
+the C-ABI.  Fixtures: seeded numpy Gaussians with the reference's shapes (its
+testsup::random_gaussian stream is mt19937 and not part of the hot path).
+"""
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def gauss(rows, cols, seed):
+    return np.random.default_rng(seed).standard_normal((rows, cols))
+
+
+def make_system(rank_case, seed):
+    """acceptance.cpp:71-90: full column/row rank, full row/column rank, both deficient."""
+    if rank_case == 0:
+        A, B = gauss(100, 15, seed), gauss(18, 110, seed + 1000)
+    elif rank_case == 1:
+        A, B = gauss(15, 100, seed), gauss(110, 18, seed + 1000)
+    else:
+        g = gauss(30, 70, seed)
+        A = np.vstack([g, g])
+        h = gauss(40, 12, seed + 1000)
+        B = np.hstack([h, h])
+    X = gauss(A.shape[1], B.shape[0], seed + 2000)
+    return A, B, A @ X @ B
+
+
+def x_star(A, B, C):
+    """reference_solution's A⁺CB⁺ (analysis.hpp:48-91; every rank case)."""
+    return np.linalg.pinv(A) @ C @ np.linalg.pinv(B)
+
+
+def rrn(x, ref):
+    return float(np.sum((x - ref) ** 2) / np.sum(ref ** 2))  # analysis.hpp:107-111
+
+
+def test_c1_greedy_family_converges_on_all_rank_cases(axb):
+    """acceptance.cpp:112-152: GRBK, RGRBK(0.8), MWRBK reach (squared) RRN ≤ 1e-6
+    against X* on 15 systems within 10⁶ iterations; the reference's budget for
+    the whole criterion is 60 s."""
+    t0 = time.perf_counter()
+    for rank_case in range(3):
+        for trial in range(5):
+            A, B, C = make_system(rank_case, 10 * (trial + 1) + rank_case)
+            xs = x_star(A, B, C)
+            for method in (axb.Method.grbk(), axb.Method.rgrbk(0.8), axb.Method.mwrbk()):
+                cfg = axb.SolveConfig(method=method, alpha_rule=axb.AlphaRule.Safe,
+                                      stop=axb.StopRule.solution_rrn(1e-6, xs), max_iter=10 ** 6,
+                                      seed=7 * trial + rank_case)
+                rep = axb.solve(A, B, C, np.zeros((A.shape[1], B.shape[0])), cfg)
+                assert rep.terminated_by == axb.Terminated.Tolerance, (rank_case, trial, method)
+                assert rrn(rep.X, xs) <= 1e-6
+    assert time.perf_counter() - t0 < 60.0
+
+
+def test_c2_bk_reaches_its_limit_with_invariant_residue(axb):
+    """acceptance.cpp:157-204: BK from 1e-5·I converges to X_lim = A⁺CB⁺ + X0 −
+    A⁺AX0BB⁺ and X − A⁺(AXB)B⁺ never moves."""
+    for trial in range(3):
+        g = gauss(15, 40, 40 + trial)
+        A = np.vstack([g, g])
+        h = gauss(12, 30, 50 + trial)
+        B = np.vstack([h, h])
+        C = A @ gauss(40, 24, 60 + trial) @ B
+        X0 = 1e-5 * np.eye(40, 24)
+        Ap, Bp = np.linalg.pinv(A), np.linalg.pinv(B)
+        limit = Ap @ C @ Bp + X0 - Ap @ A @ X0 @ B @ Bp  # bk_limit (analysis.hpp:95-104)
+        residue = lambda x: x - Ap @ (A @ x @ B) @ Bp  # noqa: E731
+        r0 = residue(X0)
+        cfg = axb.SolveConfig(method=axb.Method.bk(), alpha_rule=axb.AlphaRule.Safe,
+                              stop=axb.StopRule.solution_rrn(1e-6, limit), max_iter=10 ** 6)
+        s = axb.Solver(A, B, C, X0, cfg)
+        assert np.linalg.norm(residue(s.X()) - r0) <= 1e-8
+        s.steps(100)
+        assert np.linalg.norm(residue(s.X()) - r0) <= 1e-8
+        s.steps(9900)
+        assert np.linalg.norm(residue(s.X()) - r0) <= 1e-8
+        rep = s.run()
+        assert rep.terminated_by == axb.Terminated.Tolerance
+        assert rrn(rep.X, limit) <= 1e-6
+
+
+def test_c3_relaxed_half_is_greedy(axb):
+    """acceptance.cpp:216-241: same rows, same iteration count, X within 1e-15."""
+    for trial in range(10):
+        A = gauss(15 + trial, 6, 80 + trial)
+        B = gauss(5, 20 + trial, 90 + trial)
+        C = A @ gauss(6, 5, 100 + trial) @ B
+        mk = lambda m: axb.SolveConfig(method=m, alpha_rule=axb.AlphaRule.Safe,  # noqa: E731
+                                       stop=axb.StopRule.residual_rel(1e-10), max_iter=500,
+                                       seed=1234 + trial, record_trace=True)
+        g = axb.solve(A, B, C, np.zeros((6, 5)), mk(axb.Method.grbk()))
+        r = axb.solve(A, B, C, np.zeros((6, 5)), mk(axb.Method.rgrbk(0.5)))
+        assert g.iterations == r.iterations
+        assert [t.selected_row for t in g.trace] == [t.selected_row for t in r.trace]
+        assert np.max(np.abs(g.X - r.X)) <= 1e-15
+
+
+@pytest.mark.parametrize("method", ["rbk", "grbk", "rgrbk", "mwrbk"])
+def test_c4_recurrence_drift_after_ten_thousand_steps(axb, method):
+    """acceptance.cpp:245-265: refresh off, 10⁴ incremental steps, then
+    ‖R_inc − (C − AXB)‖_F ≤ 1e-8·(1 + ‖C‖_F)."""
+    A, B = gauss(60, 20, 111), gauss(15, 40, 112)
+    C = A @ gauss(20, 15, 113) @ B
+    guard = 1e-8 * (1.0 + np.linalg.norm(C))
+    m = {"rbk": axb.Method.rbk(), "grbk": axb.Method.grbk(), "rgrbk": axb.Method.rgrbk(0.8),
+         "mwrbk": axb.Method.mwrbk()}[method]
+    cfg = axb.SolveConfig(method=m, alpha_rule=axb.AlphaRule.Safe,
+                          stop=axb.StopRule.residual_rel(0.0), max_iter=10000, seed=2024,
+                          refresh_interval=0)
+    s = axb.Solver(A, B, C, np.zeros((20, 15)), cfg)
+    done = 0
+    while done < 10000 and s.residual_fro_sq() > 0.0:
+        s.steps(1000)
+        done += 1000
+    assert s.residual_drift() <= guard
+
+
+def test_c6_rbk_mean_error_under_expected_envelope(axb):
+    """acceptance.cpp:269-312: over 500 RBK runs, mean ‖X_k − X*‖² ≤ 1.05·ρᵏ·‖X*‖²
+    at k = 10, 50, 100, with ρ = 1 − α(2 − α‖B‖²)σ²_min(A)σ²_min(B)/‖A‖²_F
+    (factor_bounds, analysis.hpp:163-195)."""
+    A, B = gauss(20, 8, 121), gauss(8, 25, 122)
+    C = A @ gauss(8, 8, 123) @ B
+    xs = x_star(A, B, C)
+    e0 = float(np.sum(xs ** 2))
+    mk = lambda seed: axb.SolveConfig(method=axb.Method.rbk(), alpha_rule=axb.AlphaRule.Safe,  # noqa: E731
+                                      stop=axb.StopRule.residual_rel(0.0), max_iter=100,
+                                      seed=seed, refresh_interval=0)
+    probe = axb.Solver(A, B, C, np.zeros((8, 8)), mk(0))
+    alpha = probe.alpha()
+    sa, sb = np.linalg.svd(A, compute_uv=False), np.linalg.svd(B, compute_uv=False)
+    d = 2.0 * alpha - alpha * alpha * sb[0] ** 2
+    rho = 1.0 - d * (sa[-1] ** 2) * (sb[-1] ** 2) / float(np.sum(A * A))
+    assert 0.0 < rho < 1.0
+    checkpoints = (10, 50, 100)
+    mean = np.zeros(3)
+    trials = 500
+    for t in range(trials):
+        s = axb.Solver(A, B, C, np.zeros((8, 8)), mk(5000 + t))
+        done = 0
+        for i, k in enumerate(checkpoints):
+            s.steps(k - done)
+            done = k
+            mean[i] += np.sum((s.X() - xs) ** 2)
+    mean /= trials
+    for i, k in enumerate(checkpoints):
+        assert mean[i] <= rho ** k * e0 * 1.05, (k, mean[i], rho ** k * e0)
