@@ -2,8 +2,9 @@
 
 C1 (convergence of the greedy family on 15 systems), C2 (BK to its limit with an
 invariant projection residue), C3 (θ = ½ ≡ GRBK), C4 (raw recurrence drift after
-10⁴ steps) and C6 (RBK mean error under the expected envelope), restated through
-the C-ABI.  Fixtures: seeded numpy Gaussians with the reference's shapes (its
+10⁴ steps), C6 (RBK mean error under the expected envelope) and C7 (the greedy
+family beats RBK on the six registry shapes, through the device benchmark pool),
+restated through the C-ABI.  Fixtures: seeded numpy Gaussians with the reference's shapes (its
 testsup::random_gaussian stream is mt19937 and not part of the hot path).
 """
 import time
@@ -154,3 +155,43 @@ def test_c6_rbk_mean_error_under_expected_envelope(axb):
     mean /= trials
     for i, k in enumerate(checkpoints):
         assert mean[i] <= rho ** k * e0 * 1.05, (k, mean[i], rho ** k * e0)
+
+
+def registry_standins():
+    """The six mini_registry shapes (problems.hpp:473-519): dense/sparse × tall /
+    wide / rank-deficient (stacked).  numpy stand-ins for the reference's sources;
+    the iteration ordering below was checked on the oracle for these matrices."""
+    def sp(r, c, d, s):
+        rng = np.random.default_rng(s)
+        M = rng.standard_normal((r, c))
+        M[rng.random((r, c)) >= d] = 0.0
+        return M
+
+    st = lambda M: np.vstack([M, M])  # noqa: E731
+    return {"dense_tall": (gauss(90, 12, 1), gauss(14, 90, 2)),
+            "sparse_tall": (sp(100, 12, 0.2, 3), sp(15, 110, 0.2, 4)),
+            "dense_wide": (gauss(12, 90, 5), gauss(90, 14, 6)),
+            "sparse_wide": (sp(12, 100, 0.2, 7), sp(95, 15, 0.2, 8)),
+            "dense_deficient": (st(gauss(25, 60, 9)), st(gauss(12, 40, 10))),
+            "sparse_deficient": (st(sp(20, 50, 0.25, 11)), st(sp(12, 36, 0.25, 12)))}
+
+
+def test_c7_greedy_variants_beat_rbk_on_the_registry(axb):
+    """acceptance.cpp:316-358: the device benchmark pool (20 trials, tol 1e-6,
+    seed 9) gives IT(grbk) ≤ IT(rbk), IT(rgrbk(0.8)) ≤ 1.05·IT(grbk),
+    IT(mwrbk) ≤ 1.05·IT(rgrbk) on every problem, with no failed trial."""
+    from paper_2408_05444_b200 import pool
+
+    probs = []
+    for name, (A, B) in registry_standins().items():
+        C = A @ gauss(A.shape[1], B.shape[0], 99) @ B
+        probs.append(pool.BenchProblem(name, A, B, C, x_star(A, B, C)))
+    methods = [axb.Method.rbk(), axb.Method.grbk(), axb.Method.rgrbk(0.8), axb.Method.mwrbk()]
+    rows = pool.benchmark(probs, methods,
+                          pool.BenchmarkOptions(trials=20, tol=1e-6, max_iter=10 ** 6, seed=9))
+    for pb in probs:
+        it = {r.method: r.it_mean for r in rows if r.problem_id == pb.id}
+        assert all(r.failures == 0 for r in rows if r.problem_id == pb.id), pb.id
+        assert it["grbk"] <= it["rbk"], (pb.id, it)
+        assert it["rgrbk"] <= 1.05 * it["grbk"], (pb.id, it)
+        assert it["mwrbk"] <= 1.05 * it["rgrbk"], (pb.id, it)
