@@ -122,6 +122,12 @@ int axb_nccl_unique_id(unsigned char out[128]);
 int axb_nccl_comm_create(int nranks, const unsigned char id[128], int rank, int device,
                          void** comm);
 int axb_nccl_comm_destroy(void* comm);
+/* Test infrastructure: `world` communicators of an in-process emulation of the
+ * collectives (ranks = host threads of this process, one solver handle each, all
+ * on one device; every collective synchronises at a host barrier).  Lets the
+ * row-sharded path run with world > 1 on a single GPU; destroy each with
+ * axb_nccl_comm_destroy.  Not for performance: iterations are not graph-captured. */
+int axb_nccl_emulated_group(int world, void** comms);
 int axb_abi_version(void);
 /* 1 when a device that can run the sm_100a kernels is visible. */
 int axb_device_available(void);

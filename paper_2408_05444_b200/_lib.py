@@ -100,6 +100,7 @@ SIGNATURES = [
     ("axb_nccl_comm_create", C.c_int, [C.c_int, C.c_char_p, C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p)]),
     ("axb_nccl_comm_destroy", C.c_int, [C.c_void_p]),
+    ("axb_nccl_emulated_group", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     ("axb_device_available", C.c_int, []),
     ("axb_solver_create", C.c_int,
      [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,

@@ -22,6 +22,10 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <condition_variable>
+#include <mutex>
+#include <set>
+
 #include "../../include/axb_b200.h"
 #include "axb_device.cuh"
 #include "axb_nccl.cuh"
@@ -53,6 +57,145 @@ const Api* api(const char** why) {
     }
     if (why) *why = reason;
     return state == 1 ? &a : nullptr;
+}
+
+// ---- in-process emulation of the collectives (test infrastructure) ----------
+// `world` ranks as host threads of ONE process on ONE GPU, each with its own
+// solver handle and stream.  A collective synchronises the caller's stream,
+// meets the other ranks at a host barrier, lets rank 0 combine the buffers (sums
+// in rank order, gathers by copy), and meets them again — so no rank's kernel
+// ever waits on another rank's kernel, and the sharded code path (every kernel,
+// every offset and owner decision) runs with world > 1 where only one GPU is
+// available.  Solvers on an emulated communicator launch iterations directly
+// (a host-synchronising collective cannot be captured into a CUDA graph).
+struct EmuGroup {
+    int world = 1;
+    int alive = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    struct Slot {
+        const void* send;
+        void* recv;
+        size_t count;
+    };
+    std::vector<Slot> slots;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const uint64_t g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+struct EmuComm {
+    EmuGroup* grp;
+    int rank;
+};
+std::mutex g_emu_mu;
+std::set<const void*> g_emu_comms;
+
+bool is_emulated(const void* comm) {
+    std::lock_guard<std::mutex> lk(g_emu_mu);
+    return g_emu_comms.count(comm) != 0;
+}
+
+ncclResult_t emu_allreduce(const void* send, void* recv, size_t count, ncclDataType_t dt,
+                           ncclRedOp_t op, ncclComm_t comm, cudaStream_t s) {
+    if (dt != ncclFloat64 || op != ncclSum) return ncclInvalidArgument;
+    auto* c = reinterpret_cast<EmuComm*>(comm);
+    EmuGroup* G = c->grp;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return ncclUnhandledCudaError;
+    G->slots[c->rank] = {send, recv, count};
+    G->barrier();
+    ncclResult_t rc = ncclSuccess;
+    if (c->rank == 0) {
+        std::vector<double> acc(count, 0.0), tmp(count);
+        for (int r = 0; r < G->world && rc == ncclSuccess; ++r) {
+            if (cudaMemcpy(tmp.data(), G->slots[r].send, count * sizeof(double),
+                           cudaMemcpyDeviceToHost) != cudaSuccess)
+                rc = ncclUnhandledCudaError;
+            for (size_t i = 0; i < count; ++i) acc[i] += tmp[i];
+        }
+        for (int r = 0; r < G->world && rc == ncclSuccess; ++r)
+            if (cudaMemcpy(G->slots[r].recv, acc.data(), count * sizeof(double),
+                           cudaMemcpyHostToDevice) != cudaSuccess)
+                rc = ncclUnhandledCudaError;
+        if (cudaDeviceSynchronize() != cudaSuccess) rc = ncclUnhandledCudaError;
+    }
+    G->barrier();
+    return rc;
+}
+
+ncclResult_t emu_allgather(const void* send, void* recv, size_t count, ncclDataType_t dt,
+                           ncclComm_t comm, cudaStream_t s) {
+    if (dt != ncclFloat64) return ncclInvalidArgument;
+    auto* c = reinterpret_cast<EmuComm*>(comm);
+    EmuGroup* G = c->grp;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return ncclUnhandledCudaError;
+    G->slots[c->rank] = {send, recv, count};
+    G->barrier();
+    ncclResult_t rc = ncclSuccess;
+    if (c->rank == 0) {
+        const size_t bytes = count * sizeof(double);
+        for (int r = 0; r < G->world; ++r)
+            for (int t = 0; t < G->world; ++t) {
+                char* dst = static_cast<char*>(G->slots[t].recv) + (size_t)r * bytes;
+                if (dst == G->slots[r].send) continue;  // in place
+                if (cudaMemcpy(dst, G->slots[r].send, bytes, cudaMemcpyDeviceToDevice) !=
+                    cudaSuccess)
+                    rc = ncclUnhandledCudaError;
+            }
+        if (cudaDeviceSynchronize() != cudaSuccess) rc = ncclUnhandledCudaError;
+    }
+    G->barrier();
+    return rc;
+}
+
+ncclResult_t emu_destroy(ncclComm_t comm) {
+    auto* c = reinterpret_cast<EmuComm*>(comm);
+    std::lock_guard<std::mutex> lk(g_emu_mu);
+    g_emu_comms.erase(c);
+    EmuGroup* G = c->grp;
+    delete c;
+    if (--G->alive == 0) delete G;
+    return ncclSuccess;
+}
+
+const char* emu_error(ncclResult_t r) {
+    return r == ncclSuccess ? "ok" : "emulated collective failed";
+}
+
+const Api* emulated_api() {
+    static Api e;
+    static bool init = false;
+    std::lock_guard<std::mutex> lk(g_emu_mu);
+    if (!init) {
+        e.AllReduce = emu_allreduce;
+        e.AllGather = emu_allgather;
+        e.CommDestroy = emu_destroy;
+        e.GetErrorString = emu_error;
+        init = true;
+    }
+    return &e;
+}
+
+void emulated_group(int world, void** comms) {
+    auto* G = new EmuGroup;
+    G->world = world;
+    G->alive = world;
+    G->slots.resize(world);
+    std::lock_guard<std::mutex> lk(g_emu_mu);
+    for (int r = 0; r < world; ++r) {
+        auto* c = new EmuComm{G, r};
+        g_emu_comms.insert(c);
+        comms[r] = c;
+    }
 }
 }  // namespace axb_nccl
 
@@ -196,6 +339,7 @@ struct axb_solver {
     DevBuf<long long> tr_row, forced;
     // row sharding (§8(e))
     bool sharded = false;
+    bool emulated = false;  // in-process collective emulation: no graph capture
     int world = 1, rank = 0;
     uint64_t m_g = 0, row0 = 0, p_loc = 0, n_loc = 0;
     ncclComm_t comm = nullptr;
@@ -345,7 +489,8 @@ struct axb_solver {
             m_g = opt.m_global ? opt.m_global : m * (uint64_t)world;
             row0 = opt.row_offset;
             const char* why = "";
-            nc = axb_nccl::api(&why);
+            emulated = axb_nccl::is_emulated(opt.nccl_comm);
+            nc = emulated ? axb_nccl::emulated_api() : axb_nccl::api(&why);
             if (!nc) fail(AXB_CUDA_ERROR, "row sharding needs NCCL: %s", why);
             comm = static_cast<ncclComm_t>(opt.nccl_comm);
             if (rank < 0 || rank >= world) fail(AXB_CONFIG_ERROR, "rank %d outside [0, %d)", rank, world);
@@ -948,7 +1093,7 @@ struct axb_solver {
                 }
                 kernel_launches += launches_per_iteration();
             }
-        } else if (nb < (uint64_t)graph_iters) {
+        } else if (nb < (uint64_t)graph_iters || emulated) {
             for (uint64_t i = 0; i < nb; ++i) launch_iteration();
         } else {
             if (!graph) build_graph();
@@ -1373,7 +1518,15 @@ int axb_nccl_comm_create(int nranks, const unsigned char id[128], int rank, int 
     return AXB_OK;
 }
 
+int axb_nccl_emulated_group(int world, void** comms) {
+    if (world < 1 || !comms) return AXB_CONFIG_ERROR;
+    axb_nccl::emulated_group(world, comms);
+    return AXB_OK;
+}
 int axb_nccl_comm_destroy(void* comm) {
+    if (comm && axb_nccl::is_emulated(comm))
+        return axb_nccl::emulated_api()->CommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess
+                   ? AXB_OK : AXB_CUDA_ERROR;
     const axb_nccl::Api* a = axb_nccl::api(nullptr);
     if (!a || !comm) return AXB_OK;
     return a->CommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? AXB_OK : AXB_CUDA_ERROR;

@@ -39,6 +39,17 @@ def nccl_comm_destroy(comm: int) -> None:
         _lib.load().axb_nccl_comm_destroy(C.c_void_p(comm))
 
 
+def emulated_comms(world: int) -> list:
+    """`world` communicators of the in-process collective emulation (test
+    infrastructure): one per rank, the ranks being host threads of this process
+    on one GPU (axb_nccl_emulated_group)."""
+    arr = (C.c_void_p * world)()
+    st = _lib.load().axb_nccl_emulated_group(world, arr)
+    if st:
+        raise CudaError("axb_nccl_emulated_group failed")
+    return [arr[i] for i in range(world)]
+
+
 def init_comm(device: int):
     """Collective over torch.distributed: rank 0 makes the id, all ranks join."""
     import torch.distributed as dist
