@@ -137,3 +137,40 @@ def test_sharded_world_x_and_run_to_tolerance(axb, orc, world):
         assert rel(Xr, so.X()) <= 1e-10
         assert rep.terminated_by == axb.Terminated.Tolerance
         assert abs(rep.iterations - 13483) <= 2
+
+
+def test_sharded_config5_shape_world8(axb, orc):
+    """Config 5's aspect ratio at 1/16 scale (A 4096×512, B 512×2048, Gaussian
+    scaled as config 5) over 8 emulated ranks: 512 rows per rank, 256-column
+    slices of B, 64-row slices of X; 300 GRBK steps match the oracle."""
+    from paper_2408_05444_b200 import shard
+
+    m, p, q, n, world = 4096, 512, 512, 2048, 8
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((m, p)) / np.sqrt(p)
+    B = rng.standard_normal((q, n)) / np.sqrt(n)
+    X = rng.standard_normal((p, q))
+    Cm = (A @ X) @ B
+    cfg_o = O.make_config(method=O.GRBK, seed=42, stop_kind=O.SOLUTION_RRN, tol=0.0,
+                          reference=X, refresh_interval=0)
+    so = O.Solver(orc, A, B, Cm, None, cfg_o)
+    ro = so.steps(300)
+    comms = shard.emulated_comms(world)
+    ml = m // world
+    try:
+        def rank(r):
+            sl = slice(r * ml, (r + 1) * ml)
+            cfg = axb.SolveConfig(method=axb.Method.grbk(), stop=axb.StopRule.solution_rrn(0.0, X),
+                                  seed=42, refresh_interval=0)
+            s = shard.sharded_solver(np.ascontiguousarray(A[sl]), B, np.ascontiguousarray(Cm[sl]),
+                                     None, cfg, comms[r], world, r)
+            return s.steps(300), s.X()
+
+        res = run_ranks(world, rank)
+    finally:
+        for c in comms:
+            shard.nccl_comm_destroy(c)
+    for rows, Xr in res:
+        mism = np.nonzero(rows != ro)[0]
+        assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+        assert rel(Xr, so.X()) <= 1e-10
