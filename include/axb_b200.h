@@ -93,7 +93,8 @@ typedef struct {
 typedef struct {
     int32_t device;            /* CUDA ordinal */
     int32_t inputs_on_device;  /* 1: A,B,C,X0 (and cfg.reference) are device pointers */
-    int32_t cache_gram;        /* -1 auto, 0 form g = A·A_iᵀ per step, 1 cache G = A·Aᵀ */
+    int32_t cache_gram;        /* -1 auto (fits in HBM and max_iter repays forming it),
+                                  0 form g = A·A_iᵀ per step, 1 cache G = A·Aᵀ */
     int32_t spectral_on_device;/* -1 auto, 0 host (bitwise reference α), 1 device */
     int32_t graph_iters;       /* iterations captured per CUDA graph (0 = default) */
     int32_t tie_guard;         /* 1 (default): exact sequential re-check of near-boundary draws */
@@ -212,6 +213,8 @@ uint64_t axb_solver_iteration(const axb_solver* s);
 double axb_solver_alpha(const axb_solver* s);
 double axb_solver_spectral_norm_b(const axb_solver* s);
 int axb_solver_alpha_outside_bound(const axb_solver* s);
+/* 1 when G = A·Aᵀ is cached (axb_options.cache_gram), 0 when g = A·A_iᵀ is formed per step */
+int axb_solver_gram_cached(const axb_solver* s);
 double axb_solver_a_fro_sq(const axb_solver* s);
 int axb_solver_residual_fro_sq(axb_solver* s, double* out);
 int axb_solver_get_X(axb_solver* s, double* out);        /* p×q */

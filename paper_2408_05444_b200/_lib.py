@@ -136,6 +136,7 @@ SIGNATURES = [
     ("axb_solver_alpha", C.c_double, [_H]),
     ("axb_solver_spectral_norm_b", C.c_double, [_H]),
     ("axb_solver_alpha_outside_bound", C.c_int, [_H]),
+    ("axb_solver_gram_cached", C.c_int, [_H]),
     ("axb_solver_a_fro_sq", C.c_double, [_H]),
     ("axb_solver_residual_fro_sq", C.c_int, [_H, _dp]),
     ("axb_solver_get_X", C.c_int, [_H, _dp]),

@@ -640,13 +640,21 @@ struct axb_solver {
             }
         }
 
-        // gram_ = gram_mmt(A) (solver.hpp:171): cached when it fits in HBM
+        // gram_ = gram_mmt(A) (solver.hpp:171): cached when it fits in HBM and the
+        // run is long enough to repay it.  Forming G costs m_g·m·p FLOP on the DMMA
+        // pipe (symmetric half, ~29 TFLOP/s); without it every iteration re-reads
+        // the local A for g = A·A_iᵀ (8·m·p bytes at ~6.4 TB/s).  The horizon is the
+        // solve's iteration budget (cfg.max_iter, the reference's 200000 by
+        // default): a short fixed budget skips G, a long solve caches it.
         size_t free_b = 0, total_b = 0;
         ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
         const double gbytes = 8.0 * (double)m_g * (double)m;
+        const double g_form_s = (double)m_g * (double)m * (double)p / (sharded ? 14.5e12 : 29e12);
+        const double g_step_s = 8.0 * (double)m * (double)p / 6.4e12;
+        const bool repays = (double)cfg.max_iter * g_step_s >= g_form_s;
         gram_cached = opt.cache_gram == 1 ||
                       (opt.cache_gram < 0 && gbytes < 0.45 * (double)free_b &&
-                       gbytes <= 48e9);
+                       gbytes <= 48e9 && repays);
         T.alloc(m * q, "T");
         const int gparts = gemm_num_ctas((long long)m, (long long)std::max(n, m));
         gemm_sq.alloc(gparts, "gemm parts");
@@ -1857,6 +1865,7 @@ uint64_t axb_solver_iteration(const axb_solver* s) { return s->k; }
 double axb_solver_alpha(const axb_solver* s) { return s->alpha; }
 double axb_solver_spectral_norm_b(const axb_solver* s) { return s->b_spec; }
 int axb_solver_alpha_outside_bound(const axb_solver* s) { return s->alpha_outside ? 1 : 0; }
+int axb_solver_gram_cached(const axb_solver* s) { return s->gram_cached ? 1 : 0; }
 double axb_solver_a_fro_sq(const axb_solver* s) { return s->a_fro_sq; }
 int axb_solver_residual_fro_sq(axb_solver* s, double* out) {
     return guarded(s, [&] {

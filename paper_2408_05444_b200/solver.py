@@ -428,6 +428,10 @@ class Solver:
     def alpha_outside_bound(self):
         return bool(self._lib.axb_solver_alpha_outside_bound(self._h))
 
+    def gram_cached(self):
+        """True when G = A·Aᵀ is cached; False when g = A·A_iᵀ is formed per step."""
+        return bool(self._lib.axb_solver_gram_cached(self._h))
+
     def _vec(self, fn, shape):
         out = np.empty(shape)
         self._chk(fn(self._h, out.ctypes.data_as(_dp)))
