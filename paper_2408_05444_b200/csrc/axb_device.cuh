@@ -129,7 +129,7 @@ struct Params {
     int persist_lat;             // latency body (threads per CTA, 0 = off): selection state in
                                  // shared memory, 2 barriers per iteration (m ≤ kPersistLatRows)
     const double* BtB;           // n×n BᵀB (solver.hpp:172) for z = BᵀB·R_iᵀ in one phase, or null
-    int yg_grid;
+    int yg_grid, yg_rbq, yg_rbm;  // K4 grid; B rows / A rows per CTA
     int z_nslab, z_nj, z_jrows, x_ctas;
     int sel_split, sel_grid;     // greedy pre-selection across sel_grid CTAs (k_sel_greedy)
 };

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
         Ai = P.A + il * P.p;
     }
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int rbq = yg_rows_per_cta(P.q), rbm = yg_rows_per_cta(P.m);
+    const int rbq = P.yg_rbq, rbm = P.yg_rbm;
     const long long nbq = (P.q + rbq - 1) / rbq;
     const long long nb = nbq + (with_g ? (P.m + rbm - 1) / rbm : 0);
     for (long long b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -371,9 +371,11 @@ __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
 // ------------------------------------------------------------------------
 // K4b + K5: z = yᵀ·B (column slabs × row chunks, deterministic last-block
 // combine) and the X row update with the fresh ‖X − X_ref‖² partial sums.
-__global__ void __launch_bounds__(kThreads) k_zx(Params P) {
+constexpr int kZxYStage = 512;  // y entries of one row chunk staged in shared memory
+__global__ void __launch_bounds__(kThreads, 4) k_zx(Params P) {
     __shared__ double red[kWarps];
     __shared__ bool last;
+    __shared__ double ys[kZxYStage];
     pdl_wait();
     pdl_trigger();
     DevState* st = P.st;
@@ -389,29 +391,34 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
         const long long j1 = min(P.q, j0 + P.z_jrows);
         const long long c = P.c0 + (long long)slab * (2 * kThreads) + 2 * tid;
         const long long cend = P.c1;
+        // the chunk's y once into shared memory (broadcast reads below)
+        const bool ystage = j1 - j0 <= kZxYStage;
+        if (ystage) {
+            for (long long j = j0 + tid; j < j1; j += kThreads) ys[j - j0] = __ldg(P.y + j);
+            __syncthreads();
+        }
+        auto yat = [&](long long j) { return ystage ? ys[j - j0] : __ldg(P.y + j); };
         double a0 = 0.0, a1 = 0.0;
         if ((P.n & 1) == 0) {
             if (c < cend) {
                 const double2* Bc = reinterpret_cast<const double2*>(P.B + c);
                 const long long ld2 = P.n >> 1;
                 long long j = j0;
-                // 4 rows of B in flight per thread: all loads first, then the
+                // 8 rows of B in flight per thread: all loads first, then the
                 // FMAs in row order (same sums as the one-row loop)
-                for (; j + 4 <= j1; j += 4) {
-                    double2 b[4];
-                    double yv[4];
+                for (; j + 8 <= j1; j += 8) {
+                    double2 b[8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) b[u] = __ldcs(Bc + (j + u) * ld2);  // last use of B
+                    for (int u = 0; u < 8; ++u) b[u] = __ldcs(Bc + (j + u) * ld2);  // last use of B
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) yv[u] = __ldg(P.y + j + u);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        a0 += yv[u] * b[u].x;
-                        a1 += yv[u] * b[u].y;
+                    for (int u = 0; u < 8; ++u) {
+                        const double yv = yat(j + u);
+                        a0 += yv * b[u].x;
+                        a1 += yv * b[u].y;
                     }
                 }
                 for (; j < j1; ++j) {
-                    const double yj = __ldg(P.y + j);
+                    const double yj = yat(j);
                     const double2 b = __ldcs(Bc + j * ld2);
                     a0 += yj * b.x;
                     a1 += yj * b.y;
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
             }
         } else {
             for (long long j = j0; j < j1; ++j) {
-                const double yj = __ldg(P.y + j);
+                const double yj = yat(j);
                 if (c < cend) a0 += yj * __ldg(P.B + j * P.n + c);
                 if (c + 1 < cend) a1 += yj * __ldg(P.B + j * P.n + c + 1);
             }
@@ -468,17 +475,17 @@ __global__ void __launch_bounds__(kThreads) k_zx(Params P) {
             const double2* f2 = reinterpret_cast<const double2*>(rr);
             const long long h = q >> 1;
             long long k = lane;
-            // 2 segments per lane in flight: loads first, then update + store
-            for (; k + 32 < h; k += 64) {
-                double2 x[2], yy[2], rf[2];
+            // 4 segments per lane in flight: loads first, then update + store
+            for (; k + 96 < h; k += 128) {
+                double2 x[4], yy[4], rf[4];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < 4; ++u) {
                     x[u] = x2[k + 32 * u];
                     yy[u] = __ldg(y2 + k + 32 * u);
                     if (track) rf[u] = __ldg(f2 + k + 32 * u);
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < 4; ++u) {
                     x[u].x = __dadd_rn(x[u].x, __dmul_rn(f, yy[u].x));
                     x[u].y = __dadd_rn(x[u].y, __dmul_rn(f, yy[u].y));
                     x2[k + 32 * u] = x[u];
@@ -2866,6 +2873,8 @@ void launch_r(const Params& P, cudaStream_t s, bool update) {
             cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             // one shared-memory carve-out for all three iteration kernels, so
             // consecutive (PDL-overlapped) launches never reconfigure L1/smem
+            // — sized for K2's CTAs only: a larger carve-out (room for the k_zx
+            // CTAs' y staging too) measured slower, k_zx wants the L1
             const int cps = std::max(1, (P.r_grid + 147) / 148);
             int pct = (int)((100.0 * cps * (smem + fa.sharedSizeBytes + 1024)) / optin + 0.999);
             pct = std::min(100, std::max(pct, 1));

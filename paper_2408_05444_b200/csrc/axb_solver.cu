@@ -732,7 +732,13 @@ struct axb_solver {
         }
         {
             auto rpc = [](uint64_t r) { return r >= 8 * 1184 ? 8 : r >= 4 * 1184 ? 4 : r >= 2 * 1184 ? 2 : 1; };
-            const uint64_t blocks = (q + rpc(q) - 1) / rpc(q) + (gram_cached ? 0 : (m + rpc(m) - 1) / rpc(m));
+            // rows per CTA (1, 2, 4, 8; AXB_YG_RB overrides for the B rows): with
+            // more than one, the shared vector is staged once per CTA and reused
+            int rbq = rpc(q);
+            if (const int e = env_int("AXB_YG_RB", 0); e == 1 || e == 2 || e == 4 || e == 8) rbq = e;
+            P.yg_rbq = rbq;
+            P.yg_rbm = rpc(m);
+            const uint64_t blocks = (q + rbq - 1) / rbq + (gram_cached ? 0 : (m + P.yg_rbm - 1) / P.yg_rbm);
             P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, blocks));
         }
         {
