@@ -8,7 +8,10 @@
 // is `mma.sync.m8n8k4.f64` (SASS DMMA.8x8x4); operands are staged global→shared
 // with cp.async in a 3-stage ring.
 //
-// CTA tile 128×128×16, 8 warps (2×4), warp tile 64×32 = 8×4 DMMA tiles.
+// CTA tile 64×128×16, 4 warps (2×2), warp tile 32×64 = 4×8 DMMA tiles, two CTAs
+// per SM (≤ 256 registers, 92 KB smem each).  Measured against the 128×128
+// one-CTA-per-SM tile (tools/gemm_variants.cu, config-3 / config-5 shapes):
+// 34.2 / 35.0 vs 31.5 / 32.2 TFLOP/s; cuBLAS DGEMM 35.8 / 36.0.
 // Epilogue fuses the "C −" subtraction, the Σ D² partials (‖R‖²) and the
 // Σ (R_old − D)² partials (the drift guard), so a checkpoint is one pass.
 #include <cmath>
@@ -19,7 +22,10 @@ namespace axb_dev {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, PAD = 4, STAGES = 3, THREADS = 256;
+constexpr int BM = 64, BN = 128, BK = 16, PAD = 4, STAGES = 3, THREADS = 128;
+constexpr int WARPS_N = 2, FM = 4, FN = 8;  // warp grid 2×2, warp tile (FM·8)×(FN·8)
+static_assert(BK == 16 && BN == 128, "load_stage's index math assumes BK = 16, BN = 128");
+static_assert(WARPS_N * FN * 8 == BN && (THREADS / 32 / WARPS_N) * FM * 8 == BM, "warp grid");
 constexpr int A_LD = BK + PAD;       // A tile: BM × (BK+PAD), k contiguous
 constexpr int BN_LD = BN + PAD;      // B tile (K×N source): BK × (BN+PAD)
 constexpr int BT_LD = BK + PAD;      // B tile (N×K source): BN × (BK+PAD)
@@ -118,22 +124,22 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, double* As, double
 }
 
 template <bool BTRANS, bool V16>
-__global__ void __launch_bounds__(THREADS, 1) k_dgemm(GemmArgs g) {
+__global__ void __launch_bounds__(THREADS, 2) k_dgemm(GemmArgs g) {
     extern __shared__ __align__(16) double sm[];
     double* As = sm;
     double* Bs = sm + STAGES * A_STAGE;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 2, wn = warp & 3;  // 2 × 4 warps
+    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
     const int gq = lane >> 2, tq = lane & 3;
     const long long m0 = (long long)blockIdx.y * BM, n0 = (long long)blockIdx.x * BN;
     if (g.sym && n0 + BN <= m0) return;  // strictly below the diagonal: mirrored later
     const long long KT = (g.K + BK - 1) / BK;
 
-    double acc[8][4][2];
+    double acc[FM][FN][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -150,22 +156,22 @@ __global__ void __launch_bounds__(THREADS, 1) k_dgemm(GemmArgs g) {
         }
         cp_commit();
         const int cs = (int)(kt % STAGES);
-        const double* a_s = As + cs * A_STAGE + (wm * 64 + gq) * A_LD + tq;
+        const double* a_s = As + cs * A_STAGE + (wm * FM * 8 + gq) * A_LD + tq;
         const double* b_s = Bs + cs * B_STAGE;
 #pragma unroll
         for (int kk = 0; kk < BK / 4; ++kk) {
-            double af[8], bf[4];
+            double af[FM], bf[FN];
 #pragma unroll
-            for (int mi = 0; mi < 8; ++mi) af[mi] = a_s[mi * 8 * A_LD + kk * 4];
+            for (int mi = 0; mi < FM; ++mi) af[mi] = a_s[mi * 8 * A_LD + kk * 4];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int col = wn * 32 + ni * 8 + gq;
+            for (int ni = 0; ni < FN; ++ni) {
+                const int col = wn * FN * 8 + ni * 8 + gq;
                 bf[ni] = BTRANS ? b_s[col * BT_LD + kk * 4 + tq] : b_s[(kk * 4 + tq) * BN_LD + col];
             }
 #pragma unroll
-            for (int mi = 0; mi < 8; ++mi)
+            for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                for (int ni = 0; ni < FN; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
     }
     cp_wait<0>();
@@ -174,12 +180,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_dgemm(GemmArgs g) {
     double sq = 0.0, df = 0.0;
     const bool v2 = ((g.ldd | g.ldc | g.ldr) & 1) == 0;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
-        const long long r = m0 + wm * 64 + mi * 8 + gq;
+    for (int mi = 0; mi < FM; ++mi) {
+        const long long r = m0 + wm * FM * 8 + mi * 8 + gq;
         if (r >= g.M) continue;
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            const long long c = n0 + wn * 32 + ni * 8 + 2 * tq;
+        for (int ni = 0; ni < FN; ++ni) {
+            const long long c = n0 + wn * FN * 8 + ni * 8 + 2 * tq;
             if (c >= g.N) continue;
             const bool two = c + 1 < g.N;
             double o0 = acc[mi][ni][0], o1 = acc[mi][ni][1];

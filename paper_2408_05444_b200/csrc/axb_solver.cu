@@ -25,6 +25,7 @@
 #include <condition_variable>
 #include <mutex>
 #include <set>
+#include <thread>
 
 #include "../../include/axb_b200.h"
 #include "axb_device.cuh"
@@ -310,6 +311,64 @@ int env_int(const char* name, int dflt) {
 bool opt_r_tma() {
     const char* e = std::getenv("AXB_R_KERNEL");
     return !(e && std::strcmp(e, "simple") == 0);
+}
+
+// Device → host copy-out for the accessors (get_X / get_R / …).  A plain
+// cudaMemcpy into a freshly allocated pageable buffer (numpy.empty) measured
+// ~4 GB/s on the box — the driver faults the destination pages in serially — so
+// X at config 5 (0.54 GB) took 131 ms.  Large pageable copies therefore run
+// through two pinned 32 MB staging chunks: the DMA of chunk c+1 overlaps a
+// multi-threaded memcpy of chunk c into the destination.  Pinned or registered
+// destinations, and small copies, go straight through cudaMemcpy.
+void d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    cudaPointerAttributes pa{};
+    const bool pinned =
+        cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // an unregistered pointer may leave a sticky-free error code
+    constexpr size_t kChunk = size_t(32) << 20;
+    if (pinned || bytes < 2 * kChunk) {
+        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "copy out");
+        ck(cudaStreamSynchronize(s), "copy out");
+        return;
+    }
+    static std::mutex mu;
+    static char* stage[2] = {nullptr, nullptr};
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& b : stage)
+        if (!b) ck(cudaMallocHost(reinterpret_cast<void**>(&b), kChunk), "pinned staging");
+    cudaEvent_t ev[2];
+    for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            cudaEventDestroy(e[0]);
+            cudaEventDestroy(e[1]);
+        }
+    } eg{ev};
+    const size_t nch = (bytes + kChunk - 1) / kChunk;
+    auto enqueue = [&](size_t c) {
+        const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+        ck(cudaMemcpyAsync(stage[c & 1], static_cast<const char*>(src) + off, len,
+                           cudaMemcpyDeviceToHost, s), "copy out");
+        ck(cudaEventRecord(ev[c & 1], s), "event");
+    };
+    const unsigned nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    enqueue(0);
+    for (size_t c = 0; c < nch; ++c) {
+        if (c + 1 < nch) enqueue(c + 1);  // its staging chunk was drained at step c-1
+        ck(cudaEventSynchronize(ev[c & 1]), "copy out");
+        const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+        const size_t per = (len / nthr + 63) & ~size_t(63);
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nthr; ++t) {
+            const size_t a = std::min(len, t * per), b = std::min(len, a + per);
+            if (a < b)
+                th.emplace_back([=] {
+                    std::memcpy(static_cast<char*>(dst) + off + a, stage[c & 1] + a, b - a);
+                });
+        }
+        for (auto& t : th) t.join();
+    }
 }
 
 template <class T>
@@ -1407,9 +1466,8 @@ struct axb_solver {
         rep->trace_len = c.ntrace;
         if (c.x_out) {
             gather_X();
-            ck(cudaMemcpyAsync(c.x_out, X.p, sizeof(double) * p * q, cudaMemcpyDeviceToHost, stream),
-               "X out");
-            sync("X out");
+            sync("X gather");
+            d2h_copy(c.x_out, X.p, sizeof(double) * p * q, stream);
         }
     }
     void run(axb_report* rep, uint64_t* trace_k, double* trace_rrn, double* trace_rel,
@@ -1881,7 +1939,7 @@ int axb_solver_residual_fro_sq(axb_solver* s, double* out) {
 }
 static int copy_out(axb_solver* s, double* dst, const double* src, size_t count) {
     return guarded(s, [&] {
-        ck(cudaMemcpy(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost), "copy out");
+        d2h_copy(dst, src, sizeof(double) * count, s->stream);
     });
 }
 int axb_solver_get_X(axb_solver* s, double* out) {
