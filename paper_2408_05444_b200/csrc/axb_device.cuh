@@ -125,6 +125,7 @@ struct Params {
     int method, stop_kind, tie_guard, vec2;
     // launch geometry
     int r_grid, r_rows_per_cta, r_chunk, r_tma, r_stages, r_zstage;
+    int r_grab;  // K2 producer: rows taken per atomic grab (1..32)
     int persist, persist_grid;   // small systems: one cooperative kernel per batch
     int persist_lat;             // latency body (threads per CTA, 0 = off): selection state in
                                  // shared memory, 2 barriers per iteration (m ≤ kPersistLatRows)

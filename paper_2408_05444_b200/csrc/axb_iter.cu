@@ -1302,7 +1302,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
         sel = P.pack ? (long long)P.pack[P.n + P.p] : st->sel;
     }
     if (warp == kTmaConsumerWarps) {
-        // ---- producer warp: grab 32 rows at a time, read their Gram coefficients
+        // ---- producer warp: grab r_grab (≤ 32) rows at a time, read their Gram coefficients
         // coalesced, stream only rows with g ≠ 0 (an exactly-zero coefficient
         // leaves R_l and ‖R_l‖² unchanged — the reference's sparse G iterates
         // stored entries only, solver.hpp:294-295); unchanged rows still enter
@@ -1311,11 +1311,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
         unsigned round = 0;
         for (;;) {
             long long base = 0;
-            if (lane == 0) base = (long long)atomicAdd(&st->r_next, 32ull);
+            if (lane == 0) base = (long long)atomicAdd(&st->r_next, (unsigned long long)P.r_grab);
             base = __shfl_sync(0xffffffffu, base, 0);
             if (base >= m) break;
             const long long row = base + lane;
-            const bool valid = row < m;
+            const bool valid = lane < P.r_grab && row < m;
             double gl = 0.0;
             bool work = valid;
             if (UPDATE && valid) {

@@ -782,6 +782,13 @@ struct axb_solver {
             P.r_chunk = (int)std::min<uint64_t>(n, (uint64_t)tile);
             P.r_stages = std::max(2, std::min(stages, 16));
             P.r_zstage = env_int("AXB_R_ZSTAGE", 1);
+            // rows per dynamic grab (tools/sweep_grab.sh): one row at a time.  With
+            // 32-row grabs config 3's 8192 rows were 256 grabs over 296 CTAs (one
+            // or two per SM, so some SMs streamed twice the rows of others), and
+            // at config 5 the CTAs' concurrent rows sat 2 MB apart.  K2 time per
+            // grab of 32 / 8 / 1 rows: config 3 0.189 / 0.193 / 0.183 ms, config 5
+            // 5.37 / 5.25 / 5.16 ms.
+            P.r_grab = std::max(1, std::min(32, env_int("AXB_R_GRAB", 1)));
         } else {
             int rgrid = (int)std::min<uint64_t>((uint64_t)target, std::max<uint64_t>(1, (m + 7) / 8));
             P.r_rows_per_cta = (int)((m + rgrid - 1) / rgrid);
