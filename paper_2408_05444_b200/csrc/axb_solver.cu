@@ -929,6 +929,15 @@ struct axb_solver {
         *hs = s0;
         ck(cudaMemcpyAsync(st.p, hs, sizeof(DevState), cudaMemcpyHostToDevice, stream), "state");
         adopt_norms();
+        if (sharded) {
+            // every collective of the iteration once, eagerly: NCCL sets up its
+            // connections lazily at a collective's first call, which must not
+            // happen inside a graph capture (a first steps(k ≥ graph_iters) call
+            // captures at once).  y and z are recomputed before any use.
+            allreduce(y.p, y.p, q);
+            allgather_inplace(z.p, n_loc);
+            allreduce(pack_send.p, pack.p, n + p + 2);
+        }
         sync("init");
         pull_state();
     }
@@ -1532,8 +1541,26 @@ struct axb_solver {
 // C-ABI
 namespace {
 
+// Entry points on a created handle run on the handle's device and restore the
+// caller's current device afterwards, so handles on several devices can be
+// driven from one host thread (streams, events and launches are per device).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(const axb_solver* s) {
+        if (!s || !s->stream) return;  // not created yet: create() selects the device
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != s->opt.device &&
+            cudaSetDevice(s->opt.device) == cudaSuccess)
+            prev = cur;
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 template <class F>
 int guarded(axb_solver* s, F&& f) {
+    DeviceScope scope(s);
     try {
         f();
         return AXB_OK;
@@ -1705,7 +1732,10 @@ int axb_solver_create_ex(const axb_matrix* A, const axb_matrix* B, const double*
                              opt, out);
 }
 
-void axb_solver_destroy(axb_solver* s) { delete s; }
+void axb_solver_destroy(axb_solver* s) {
+    DeviceScope scope(s);
+    delete s;
+}
 const char* axb_solver_last_error(const axb_solver* s) { return s->err.c_str(); }
 
 int axb_solver_step(axb_solver* s, uint64_t* row) {
