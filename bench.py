@@ -325,9 +325,14 @@ def k2_bytes(cfg):
     return 16 * m * n + 8 * (2 * m + n)
 
 
-def iteration_bytes(cfg, gram_cached=True):
+def iteration_bytes(cfg, gram_cached=True, track_ref=True):
+    """Whole-iteration algorithmic bytes: K2, two passes over B (y, z), X read and
+    written, X_ref read for the solution_rrn error (the reference's err_sq update
+    in update_row, solver.hpp:272-289; the bench's stop rule), and the G column
+    (or A once more for g = A·A_iᵀ when G is not cached)."""
     m, p, q, n = cfg["m"], cfg["p"], cfg["q"], cfg["n"]
-    return k2_bytes(cfg) + 16 * q * n + 16 * p * q + (8 * m if gram_cached else 8 * m * p)
+    return (k2_bytes(cfg) + 16 * q * n + 16 * p * q + (8 * p * q if track_ref else 0)
+            + (8 * m if gram_cached else 8 * m * p))
 
 
 # --------------------------------------------------------------------- CPU legs
