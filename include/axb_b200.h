@@ -14,7 +14,9 @@
  *
  * Threading: a handle is single-owner and not thread-safe, like axb::Solver
  * (rng.hpp:15-17); different handles may run concurrently on
- * different devices/streams.
+ * different devices/streams.  Every call on a handle runs on the handle's device
+ * (axb_options.device) whatever the calling thread's current device is, and
+ * leaves the caller's current device unchanged.
  *
  * There is no CPU fallback: creating a solver without a usable sm_100 device
  * fails with AXB_CUDA_ERROR.
