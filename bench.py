@@ -518,9 +518,15 @@ def main():
     ap.add_argument("--shard", action="store_true",
                     help="use the row-sharded path even on one GPU (1-rank NCCL communicator)")
     ap.add_argument("--watchdog-s", type=float, default=1500.0)
+    ap.add_argument("--half-band", type=int, default=None,
+                    help="config 4: blur half-band (default 7; BASELINE's 'bandwidth 15' read "
+                         "as half-band 7, half-band 15 the other reading, SURVEY §8 D4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.half_band is not None and "half_band" in cfg:
+        cfg["desc"] = cfg["desc"].replace(f"half-band {cfg['half_band']}", f"half-band {args.half_band}")
+        cfg["half_band"] = args.half_band
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

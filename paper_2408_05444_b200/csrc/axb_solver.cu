@@ -1657,13 +1657,19 @@ int axb_solver_create(const double* A, uint64_t m, uint64_t p, const double* B, 
     s->cfg = *cfg;
     if (opt) s->opt = *opt;
     else axb_options_default(&s->opt);
+    int prev_dev = -1;
+    if (cudaGetDevice(&prev_dev) != cudaSuccess) prev_dev = -1;
+    cudaGetLastError();
     int st = guarded(s.get(), [&] { s->create(A, B, C, X0); });
     if (st != AXB_OK) {
         g_create_err = s->err;
-        return st;
+        s.reset();  // released on its own device
+    } else {
+        g_create_err.clear();
+        *out = s.release();
     }
-    g_create_err.clear();
-    *out = s.release();
+    if (prev_dev >= 0) cudaSetDevice(prev_dev);  // the caller's current device is left as it was
+    if (st != AXB_OK) return st;
     return AXB_OK;
 }
 
