@@ -72,6 +72,8 @@ struct alignas(16) DevState {
     unsigned long long r_next;   // dynamic row counter of the TMA residual kernel
     int32_t replay;              // 1: select from Params::forced_rows (index-stream replay)
     int32_t packed;              // sharded: this rank's pack_send holds the last row
+    int32_t pack_prev;           // sharded: ... held the row before (k_pack clears it)
+    unsigned int cnt_sel1;       // k_sel1 last-block counter
     unsigned long long dbg[8];   // phase timestamps of the last greedy selection (ns)
 };
 
@@ -132,6 +134,7 @@ struct Params {
     const double* BtB;           // n×n BᵀB (solver.hpp:172) for z = BᵀB·R_iᵀ in one phase, or null
     int yg_grid, yg_rbq, yg_rbm;  // K4 grid; B rows / A rows per CTA
     int z_nslab, z_nj, z_jrows, x_ctas;
+    int sel1_grid, pack_grid;  // sharded selection: membership CTAs, row-pack CTAs
     int sel_split, sel_grid;     // greedy pre-selection across sel_grid CTAs (k_sel_greedy)
 };
 

@@ -1469,23 +1469,56 @@ size_t tma_smem_bytes(const Params& P) {
 // Sharded selection, part 1 (after the record allgather): global ‖R‖², max
 // ratio / argmax and ‖X−X_ref‖² in rank order (identical on every rank), the
 // stop / divergence logic, and for GRBK this shard's member mass (group sums
-// over the local rows, kept in P.gsum for part 2).
+// over the local rows, kept in P.gsum for part 2).  The O(m_local) membership
+// pass is spread over sel1_grid CTAs, each combining the (world-sized) records
+// itself; the last CTA to finish commits the state and takes the ordered prefix
+// — the same group sums and prefix as one CTA would form (a group's sum does not
+// depend on which CTA forms it).  One CTA had taken 14 µs per iteration at the
+// world-8 shard of config 5 (m_local = 8192) and ~100 µs at m_local = 65536.
 __global__ void __launch_bounds__(kThreads) k_sel1(Params P, int update) {
     __shared__ SelShared sh;
+    __shared__ bool last;
     pdl_wait();
     DevState* st = P.st;
     if (update && halted(st)) return;
     const int tid = threadIdx.x;
     const int mode = update ? st->fin_mode : FIN_NORMS;
+    double s = 0.0, err = 0.0, mx = -INFINITY;
+    long long ax = LLONG_MAX;
+    for (int r = 0; r < P.world; ++r) {
+        const double* rec = P.recs + 4 * r;
+        s += rec[0];
+        maxidx_merge(mx, ax, rec[1], (long long)rec[2]);
+        err += rec[3];
+    }
+    const bool diverged = mode != FIN_NORMS && !isfinite(s);  // solver.hpp:306-307
+    const bool masses = (P.method == 2 || P.method == 3) && !st->replay && s > 0.0 &&
+                        !diverged && st->status != ST_ERROR;
+    const long long ng = (P.m + 31) / 32;
+    if (masses) {
+        Member mem;
+        mem.a_sq = P.a_sq;
+        mem.r_sq = P.r_sq;
+        mem.smem = 0;
+        mem.row0 = P.row0;
+        mem.argmax = ax;
+        mem.r_fro = s;
+        mem.zeta = __dadd_rn(__dmul_rn(P.theta, __ddiv_rn(mx, s)),
+                             __ddiv_rn(__dsub_rn(1.0, P.theta), P.a_fro_sq));  // as make_member
+        const long long per = (ng + gridDim.x - 1) / gridDim.x;
+        const long long gb = (long long)blockIdx.x * per;
+        grbk_group_sums(mem, P.m, P.gsum, min(ng, gb), min(ng, gb + per));
+    }
+    __threadfence();  // this CTA's group sums before its arrival
+    __syncthreads();
     if (tid == 0) {
-        double s = 0.0, err = 0.0, mx = -INFINITY;
-        long long ax = LLONG_MAX;
-        for (int r = 0; r < P.world; ++r) {
-            const double* rec = P.recs + 4 * r;
-            s += rec[0];
-            maxidx_merge(mx, ax, rec[1], (long long)rec[2]);
-            err += rec[3];
-        }
+        last = gridDim.x == 1 || atomicAdd(&st->cnt_sel1, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid == 0) {
+        st->cnt_sel1 = 0u;
         st->err_sq = err;
         st->r_fro_sq = s;
         st->max_ratio = mx;
@@ -1493,7 +1526,7 @@ __global__ void __launch_bounds__(kThreads) k_sel1(Params P, int update) {
         st->sel_valid = 0;
         const double cf = P.c_fro > 0.0 ? P.c_fro : 1.0;
         const double rel = sqrt(s > 0.0 ? s : 0.0) / cf;
-        if (mode != FIN_NORMS && !isfinite(s)) {  // solver.hpp:306-307
+        if (diverged) {
             st->status = ST_ERROR;
             st->err_code = 4;
             st->err_k = st->k;
@@ -1515,14 +1548,10 @@ __global__ void __launch_bounds__(kThreads) k_sel1(Params P, int update) {
             st->metric = P.stop_kind == 0 ? err / P.ref_sq : rel;
         }
     }
-    __syncthreads();
-    if ((P.method == 2 || P.method == 3) && !st->replay && st->r_fro_sq > 0.0 &&
-        st->status != ST_ERROR) {
-        const Member mem = make_member(P, st, P.theta);
-        grbk_group_sums(mem, P.m, P.gsum);
+    if (masses) {
         long long g0, g1;
         double excl;
-        const double tot = grbk_prefix(P.gsum, (P.m + 31) / 32, sh, g0, g1, excl);
+        const double tot = grbk_prefix(P.gsum, ng, sh, g0, g1, excl);
         if (tid == 0) P.masses[P.rank] = tot;
     }
 }
@@ -1538,7 +1567,6 @@ __global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
     pdl_wait();
     DevState* st = P.st;
     const int tid = threadIdx.x;
-    const long long n = P.n, p = P.p;
     const long long mg = P.m_global;
     if (st->status != ST_RUN || st->k >= st->k_limit) return;
     if (tid == 0) {
@@ -1651,27 +1679,43 @@ __global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
         s_owner = (int)(s_sel / mloc);  // equal shards
     }
     __syncthreads();
-    // pack: the owner writes its row; the previous owner clears its stale one
-    const bool mine = s_owner == P.rank;
-    const bool was = st->packed != 0;  // this rank packed last time
-    if (mine) {
-        const long long il = s_sel - P.row0;
-        const double* Rr = P.R + il * n;
-        const double* Ar = P.A + il * p;
-        for (long long k = tid; k < n; k += blockDim.x) P.pack_send[k] = Rr[k];
-        for (long long k = tid; k < p; k += blockDim.x) P.pack_send[n + k] = Ar[k];
-        if (tid == 0) {
-            P.pack_send[n + p] = (double)s_sel;
-            P.pack_send[n + p + 1] = __ddiv_rn(P.alpha, P.a_sq[il]);
-        }
-    } else if (was) {
-        for (long long k = tid; k < n + p + 2; k += blockDim.x) P.pack_send[k] = 0.0;
-    }
-    __syncthreads();
+    // the pack itself is k_pack's (many CTAs): the owner copies its row, the
+    // previous owner clears its stale one
     if (tid == 0) {
         st->sel = s_sel;  // −1 on non-owners for GRBK; the pack carries the row
         st->sel_valid = 1;
-        st->packed = mine ? 1 : 0;
+        st->pack_prev = st->packed;
+        st->packed = s_owner == P.rank ? 1 : 0;
+    }
+}
+
+// Sharded selection, part 3: R_i | A_i | i | coef into pack_send on the owning
+// rank (zeros where this rank packed the previous row), across pack_grid CTAs.
+// The copy had run in k_sel2's single CTA as one dependent load→store chain per
+// thread: ~80 µs per iteration on the owner at the world-8 shard of config 5.
+__global__ void __launch_bounds__(kThreads) k_pack(Params P) {
+    pdl_wait();
+    pdl_trigger();
+    const DevState* st = P.st;
+    if (st->status != ST_RUN || st->k >= st->k_limit) return;  // k_sel2 did not select
+    const bool mine = st->packed != 0, was = st->pack_prev != 0;
+    if (!mine && !was) return;
+    const long long n = P.n, p = P.p;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double* __restrict__ out = P.pack_send;
+    if (mine) {
+        const long long il = st->sel - P.row0;
+        const double* __restrict__ Rr = P.R + il * n;
+        const double* __restrict__ Ar = P.A + il * p;
+        for (long long k = t0; k < n; k += stride) out[k] = __ldcg(Rr + k);
+        for (long long k = t0; k < p; k += stride) out[n + k] = __ldg(Ar + k);
+        if (t0 == 0) {
+            out[n + p] = (double)st->sel;
+            out[n + p + 1] = __ddiv_rn(P.alpha, P.a_sq[il]);
+        }
+    } else {
+        for (long long k = t0; k < n + p + 2; k += stride) out[k] = 0.0;
     }
 }
 
@@ -2963,10 +3007,14 @@ void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* tot
 }
 
 void launch_sel1(const Params& P, cudaStream_t s, bool update) {
-    k_sel1<<<1, kThreads, 0, s>>>(P, update ? 1 : 0);
+    k_sel1<<<std::max(1, P.sel1_grid), kThreads, 0, s>>>(P, update ? 1 : 0);
 }
 
-void launch_sel2(const Params& P, cudaStream_t s) { k_sel2<<<1, kThreads, 0, s>>>(P); }
+// k_sel2 (one CTA: draw, owning shard, in-shard search) then k_pack (the row copy)
+void launch_sel2(const Params& P, cudaStream_t s) {
+    k_sel2<<<1, kThreads, 0, s>>>(P);
+    launch_pdl(k_pack, std::max(1, P.pack_grid), kThreads, 0, s, P);
+}
 
 void launch_power_step2(double* v, const double* w, long long dim, double* ps, double tol,
                         double max_iter, cudaStream_t s) {

@@ -714,6 +714,9 @@ struct axb_solver {
         gram_cached = opt.cache_gram == 1 ||
                       (opt.cache_gram < 0 && gbytes < 0.45 * (double)free_b &&
                        gbytes <= 48e9 && repays);
+        // one decision for all ranks: forming G gathers A (a collective), and a
+        // rank whose free memory differed must not take the other branch
+        if (sharded) gram_cached = global_sum(gram_cached ? 1.0 : 0.0) == (double)world;
         T.alloc(m * q, "T");
         const int gparts = gemm_num_ctas((long long)m, (long long)std::max(n, m));
         gemm_sq.alloc(gparts, "gemm parts");
@@ -864,6 +867,10 @@ struct axb_solver {
             const bool greedy = cfg.method == AXB_GRBK || cfg.method == AXB_RGRBK;
             P.sel_split = (!sharded && greedy && env_int("AXB_SEL_SPLIT", ng >= 64 ? 1 : 0)) ? 1 : 0;
             P.sel_grid = (int)std::max<long long>(1, std::min<long long>(sms, (ng + 3) / 4));
+            // sharded: k_sel1's membership pass and k_pack's row copy across the SMs
+            P.sel1_grid = greedy ? P.sel_grid : 1;
+            P.pack_grid = (int)std::max<long long>(
+                1, std::min<long long>(sms, (long long)(n + p + 2 + 1023) / 1024));
         }
         // small systems (per-iteration working set L2-resident): one persistent
         // cooperative kernel per batch instead of a graph of 3 kernels/iteration
@@ -1082,9 +1089,9 @@ struct axb_solver {
 
     void ensure_selection() {
         if (!sel_valid && sharded) {
-            launch_sel2(P, stream);
+            launch_sel2(P, stream);  // k_sel2 + k_pack
             allreduce(pack_send.p, pack.p, n + p + 2);
-            kernel_launches += 1;
+            kernel_launches += 2;
             sel_valid = true;
         } else if (!sel_valid) {
             launch_select(P, stream, cfg.method, P.theta, 0);
@@ -1116,7 +1123,7 @@ struct axb_solver {
             allreduce(pack_send.p, pack.p, n + p + 2);
         }
     }
-    int launches_per_iteration() const { return sharded ? 5 : (P.sel_split ? 4 : 3); }
+    int launches_per_iteration() const { return sharded ? 6 : (P.sel_split ? 4 : 3); }
     void launch_iteration() {
         enqueue_iteration();
         kernel_launches += launches_per_iteration();
