@@ -220,6 +220,32 @@ def test_sharded_mode_one_rank(axb, orc, tag, theta):
         shard.nccl_comm_destroy(comm)
 
 
+@pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.RGRBK, 0.7), (O.MWRBK, None)])
+def test_sharded_one_rank_tall(axb, orc, tag, theta):
+    """Sharded path on a tall system whose 282 member groups spread k_sel1 over 71
+    CTAs with a short last slice, and whose pack spans several k_pack CTAs: the
+    oracle's rows and X."""
+    from paper_2408_05444_b200 import shard
+
+    A, B, X, Cm = O.generate(orc, 11, 9000, 64, 32, 2300)
+    comm = shard.nccl_comm_create(1, shard.nccl_unique_id(), 0, 0)
+    try:
+        cfg_o = O.make_config(method=tag, theta=theta, seed=42, stop_kind=O.SOLUTION_RRN, tol=0.0,
+                              reference=X, refresh_interval=0)
+        so = O.Solver(orc, A, B, Cm, None, cfg_o)
+        cfg = axb.SolveConfig(method=axb_method(axb, tag, theta),
+                              stop=axb.StopRule.solution_rrn(0.0, X), seed=42, refresh_interval=0)
+        sg = shard.sharded_solver(A, B, Cm, None, cfg, comm, 1, 0)
+        ro = so.steps(400)
+        rg = sg.steps(400)
+        mism = np.nonzero(ro != rg)[0]
+        assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+        assert rel(sg.X(), so.X()) <= RTOL_X
+        del sg
+    finally:
+        shard.nccl_comm_destroy(comm)
+
+
 def test_sharded_run_to_tolerance_one_rank(axb, orc):
     from paper_2408_05444_b200 import shard
 
