@@ -408,3 +408,30 @@ def test_degenerate_shapes(axb, orc, shape, steps, tag, path):
     mism = np.nonzero(ro != rg)[0]
     assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
     assert rel(sg.X(), so.X()) <= RTOL_X
+
+
+def test_large_copy_out_is_exact(axb):
+    """Accessor copy-out of buffers ≥ 64 MB into fresh pageable arrays goes through
+    the pinned staging chunks (32 MB each, threaded memcpy): R₀ = C − (A·0)·B is C
+    exactly, so R() must return C bit for bit — 4096×4097 doubles (134 MB) end in
+    a partial chunk whose length is not a multiple of the thread split; X() and
+    run()'s X take the same route."""
+    rng = np.random.default_rng(3)
+    m, p, q, n = 4096, 8, 8, 4097
+    A = rng.standard_normal((m, p))
+    B = rng.standard_normal((q, n))
+    Cm = rng.standard_normal((m, n))
+    cfg = axb.SolveConfig(method=axb.Method.mwrbk(), stop=axb.StopRule.residual_rel(0.0),
+                          refresh_interval=0)
+    s = axb.Solver(A, B, Cm, None, cfg)
+    R = s.R()
+    assert R.shape == Cm.shape
+    assert np.array_equal(R, Cm)
+    # a large X through the same path: X0 returned unchanged before any step
+    p2, q2 = 3000, 2900  # 69.6 MB
+    A2 = rng.standard_normal((64, p2))
+    B2 = rng.standard_normal((q2, 64))
+    X0 = rng.standard_normal((p2, q2))
+    C2 = rng.standard_normal((64, 64))
+    s2 = axb.Solver(A2, B2, C2, X0, cfg)
+    assert np.array_equal(s2.X(), X0)
