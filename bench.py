@@ -40,6 +40,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
+    2: dict(m=2000, p=500, q=400, n=2000, x0="zero", scale_a=1.0, scale_b=1.0, cpu_div=1,
+            kind="svd", method="mwrbk",
+            desc="config2: deterministic ME-MWRBK fp64, A 2000x500 = U.diag(s).V^T and B 400x2000 "
+                 "likewise (random orthonormal U, V; s log-spaced 1..1e-2), X* N(0,1), X0=0, "
+                 "C=A.X*.B"),
     1: dict(m=500, p=100, q=80, n=400, x0="zero", scale_a=1.0, scale_b=1.0, cpu_div=1,
             desc="config1: ME-GRBK fp64 A 500x100, B 80x400 iid N(0,1), X0=0"),
     3: dict(m=8192, p=2048, q=2048, n=8192, x0="randn", scale_a=1.0, scale_b=1.0, cpu_div=1,
@@ -136,6 +141,29 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- workload
+def make_svd_system(cfg, seed):
+    """Config 2 (numpy, seeded): A = U·diag(σ)·Vᵀ and B likewise with Haar
+    orthonormal factors (QR of Gaussian matrices, sign-fixed) and σ log-spaced
+    1..1e-2, so κ(A) = κ(B) = 100; X* N(0,1); C = A·X*·B."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+
+    def orth(r, c):
+        qf, rf = np.linalg.qr(rng.standard_normal((r, c)))
+        return qf * np.sign(np.diag(rf))
+
+    def built(r, c):
+        k = min(r, c)
+        U, V = orth(r, k), orth(c, k)
+        return (U * np.logspace(0.0, -2.0, k)) @ V.T
+
+    A = built(cfg["m"], cfg["p"])
+    B = built(cfg["q"], cfg["n"])
+    Xs = rng.standard_normal((cfg["p"], cfg["q"]))
+    return A, B, Xs, (A @ Xs) @ B
+
+
 def make_inputs_device(cfg, seed, device, world=1, rank=0, blocks=8):
     """This rank's rows of A and C (A drawn in `blocks` fixed row blocks so the
     global system does not depend on the world size) plus full B, X*, X0."""
@@ -143,6 +171,14 @@ def make_inputs_device(cfg, seed, device, world=1, rank=0, blocks=8):
 
     dev = f"cuda:{device}"
     kw = dict(dtype=torch.float64, device=dev)
+    if cfg.get("kind") == "svd":
+        A, B, Xs, C = make_svd_system(cfg, seed)
+        mr = cfg["m"] // world
+        t = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+        out = (t(A[rank * mr:(rank + 1) * mr].copy()), t(B), t(C[rank * mr:(rank + 1) * mr].copy()),
+               None, t(Xs))
+        torch.cuda.synchronize(device)
+        return out
     mb = cfg["m"] // blocks
     per = blocks // world
     parts = []
@@ -312,8 +348,9 @@ def channels_arm(args, cfg, rank, world, local):
         dist.destroy_process_group()
 
 
-def solver_config(axb, Xs, max_iter):
-    return axb.SolveConfig(method=axb.Method.grbk(), alpha_rule=axb.AlphaRule.Safe,
+def solver_config(axb, Xs, max_iter, method="grbk"):
+    meth = axb.Method.mwrbk() if method == "mwrbk" else axb.Method.grbk()
+    return axb.SolveConfig(method=meth, alpha_rule=axb.AlphaRule.Safe,
                            stop=axb.StopRule.solution_rrn(1e-12, Xs), max_iter=max_iter,
                            seed=42, refresh_interval=1000)
 
@@ -362,11 +399,14 @@ def cpu_prepared_state(cfg, seed):
         return dict(A=A, B=B, C=C, X0=X0, Xs=Xs, R0=C.copy(), G=A @ A.T, BtB=B.T @ B, alpha=alpha)
     rng = np.random.default_rng(seed)
     m, p, q, n = cfg["m"], cfg["p"], cfg["q"], cfg["n"]
-    A = rng.standard_normal((m, p)) * cfg["scale_a"]
-    B = rng.standard_normal((q, n)) * cfg["scale_b"]
-    Xs = rng.standard_normal((p, q))
+    if cfg.get("kind") == "svd":
+        A, B, Xs, C = make_svd_system(cfg, seed)
+    else:
+        A = rng.standard_normal((m, p)) * cfg["scale_a"]
+        B = rng.standard_normal((q, n)) * cfg["scale_b"]
+        Xs = rng.standard_normal((p, q))
+        C = (A @ Xs) @ B
     X0 = rng.standard_normal((p, q)) if cfg["x0"] == "randn" else np.zeros((p, q))
-    C = (A @ Xs) @ B
     R0 = C - (A @ X0) @ B
     G = A @ A.T
     BtB = B.T @ B
@@ -375,8 +415,8 @@ def cpu_prepared_state(cfg, seed):
     return dict(A=A, B=B, C=C, X0=X0, Xs=Xs, R0=R0, G=G, BtB=BtB, alpha=alpha)
 
 
-def cpu_solver(O, orc, state, seed):
-    cfg_o = O.make_config(method=O.GRBK, stop_kind=O.SOLUTION_RRN, tol=1e-12,
+def cpu_solver(O, orc, state, seed, method="grbk"):
+    cfg_o = O.make_config(method=O.MWRBK if method == "mwrbk" else O.GRBK, stop_kind=O.SOLUTION_RRN, tol=1e-12,
                           reference=state["Xs"], seed=seed, refresh_interval=0)
     return O.PreparedSolver(orc, state["A"], state["B"], state["C"], state["X0"], state["R0"],
                             state["G"], state["BtB"], state["alpha"], cfg_o), cfg_o
@@ -390,7 +430,7 @@ def cpu_baseline(cfg, budget_s=15.0):
     orc = O.oracle()
     scfg, factor = cpu_sample_cfg(cfg)
     state = cpu_prepared_state(scfg, 7)
-    s, _keep = cpu_solver(O, orc, state, 42)
+    s, _keep = cpu_solver(O, orc, state, 42, cfg.get("method", "grbk"))
     s.steps(1)  # warm
     t0 = time.perf_counter()
     done = 0
@@ -404,7 +444,7 @@ def cpu_baseline(cfg, budget_s=15.0):
     extra = (f"; extrapolated x{factor} to {cfg['m']}x{cfg['p']}.{cfg['q']}x{cfg['n']} "
              f"(every per-iteration term scales by {factor})" if factor > 1 else "")
     return {"value": done / dt / factor, "unit": "iter/s", "cores": 1, "kind": "port",
-            "sample": f"{done} ME-GRBK iterations of one {shape} solve (oracle C port of "
+            "sample": f"{done} ME-{cfg.get('method', 'grbk').upper()} iterations of one {shape} solve (oracle C port of "
                       f"solver.hpp step(); constructor caches precomputed with numpy), "
                       f"{dt:.1f}s on 1 core{extra}"}
 
@@ -437,14 +477,15 @@ def reference_arm(args, cfg):
         X0 = None if not np.any(state["X0"]) else state["X0"]
 
         def build(t):
-            cfg_o = O.make_config(method=O.GRBK, stop_kind=O.SOLUTION_RRN, tol=1e-12,
+            cfg_o = O.make_config(method=O.MWRBK if cfg.get("method") == "mwrbk" else O.GRBK,
+                                  stop_kind=O.SOLUTION_RRN, tol=1e-12,
                                   reference=state["Xs"], seed=42 + t, refresh_interval=0)
             solvers[t] = O.Solver(lib, state["A"], state["B"], state["C"], X0, cfg_o)
     else:
         orc = O.oracle()
 
         def build(t):
-            solvers[t] = cpu_solver(O, orc, state, 42 + t)[0]
+            solvers[t] = cpu_solver(O, orc, state, 42 + t, cfg.get("method", "grbk"))[0]
     t0 = time.perf_counter()
     th = [threading.Thread(target=build, args=(t,)) for t in range(T)]
     for x in th:
@@ -492,7 +533,8 @@ def reference_arm(args, cfg):
         "data": ("synthetic (numpy seeded blur operator, smooth field, noise)" if "channels" in cfg
                  else "synthetic (numpy seeded N(0,1))"),
         "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
-                   "n": cfg["n"], "method": "grbk", "parallelism": f"{T} independent solves"},
+                   "n": cfg["n"], "method": cfg.get("method", "grbk"),
+                   "parallelism": f"{T} independent solves"},
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": T, "kind": kind,
                          "sample": f"{T} concurrent solves x {per} iterations (reference "
                                    f"benchmark-pool pattern), {engine}, {dt:.1f}s wall{extra}"},
@@ -590,11 +632,13 @@ def main():
     A, B, C, X0, Xs = make_inputs_device(cfg, seed, local, world, rank)
     sopts = dict(spectral_max_iter=200000)
 
+    meth = cfg.get("method", "grbk")
+
     def make_solver(A_, B_, C_, X0_, Xs_, budget=max_iter):
         if sharded:
-            return shard.sharded_solver(A_, B_, C_, X0_, solver_config(axb, Xs_, budget), comm,
+            return shard.sharded_solver(A_, B_, C_, X0_, solver_config(axb, Xs_, budget, meth), comm,
                                         world, rank, device=local, **sopts)
-        return axb.Solver(A_, B_, C_, X0_, solver_config(axb, Xs_, budget),
+        return axb.Solver(A_, B_, C_, X0_, solver_config(axb, Xs_, budget, meth),
                           axb.Options(device=local, **sopts))
 
     t0 = time.perf_counter()
@@ -717,10 +761,13 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded torch N(0,1) on device)",
             "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
-                       "n": cfg["n"], "method": "grbk", "refresh_interval": 1000,
+                       "n": cfg["n"], "method": meth, "refresh_interval": 1000,
                        "parallelism": (f"row-sharded over {world} GPUs (NCCL)" if sharded
                                        else "single GPU"),
-                       "l2": "R is 8*m*n bytes > 126 MB L2: inputs larger than L2, no flush"},
+                       "l2": ("R is 8*m*n bytes > 126 MB L2: inputs larger than L2, no flush"
+                              if 8 * cfg["m"] * cfg["n"] > 126e6 else
+                              "working set L2-resident by design (one persistent kernel per batch; "
+                              "each iteration's writes are the next one's inputs): no flush")},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
