@@ -462,7 +462,8 @@ def reference_arm(args, cfg):
     import numpy as np
     import oracle_lib as O
 
-    T = max(1, min(os.cpu_count() or 1, args.ref_threads))
+    avail = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    T = max(1, min(avail, args.ref_threads) if args.ref_threads > 0 else avail)
     # config 4: the reference constructor's spectral_norm(B) (cap 5000, tol 1e-10,
     # decomp.hpp:207-239) throws ConvergenceError for the 1024-wide blur,
     # so only the bitwise-equal port can run it
@@ -555,7 +556,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tol", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=50)
-    ap.add_argument("--ref-threads", type=int, default=16)
+    ap.add_argument("--ref-threads", type=int, default=0,
+                    help="reference arm solver threads (0: every host thread this process may use)")
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
     ap.add_argument("--shard", action="store_true",
                     help="use the row-sharded path even on one GPU (1-rank NCCL communicator)")
