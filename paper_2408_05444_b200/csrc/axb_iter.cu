@@ -263,11 +263,9 @@ __device__ void warp_dot_pair_u(const double* __restrict__ row0, const double* _
 constexpr int kYgThreads = 256;
 constexpr int kYgWarps = kYgThreads / 32;
 constexpr int kYgSeg = 2048;
-// rows per CTA: enough CTAs to cover the chip (≈148×8), as many rows as possible
-// per staged segment of the shared vector
-__host__ __device__ inline int yg_rows_per_cta(long long rows) {
-    return rows >= 8 * 1184 ? 8 : rows >= 4 * 1184 ? 4 : rows >= 2 * 1184 ? 2 : 1;
-}
+// rows per CTA (1, 2, 4 or 8: Params::yg_rbq / yg_rbm) are chosen on the host
+// (axb_solver.cu): enough CTAs to cover the chip, as many rows as possible per
+// staged segment of the shared vector
 __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
     __shared__ __align__(16) double vs[kYgSeg];
     __shared__ double part[kYgWarps];
