@@ -810,14 +810,22 @@ struct axb_solver {
             const uint64_t blocks = (q + rbq - 1) / rbq + (gram_cached ? 0 : (m + P.yg_rbm - 1) / P.yg_rbm);
             P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, blocks));
         }
+        // small systems run one persistent kernel per batch (decided below; the
+        // z row chunks depend on it)
+        const double persist_ws = 8.0 * ((double)m * n + (double)q * n + 2.0 * p * q + (double)m * p);
+        const int persist_force = env_int("AXB_PERSIST", -1);
+        const bool persist_path =
+            !sharded && (persist_force == 1 || (persist_force < 0 && persist_ws <= 64e6));
         {
             // K4b+K5 in small units over several waves, so the tail evens out:
             // X one row per warp (8 rows per CTA), z slabs of 512 columns ×
-            // chunks of AXB_Z_JROWS (128) rows of the B slice
+            // chunks of AXB_Z_JROWS rows of the B slice: 128 for the graph path
+            // (k_zx), 32 in the persistent general body, whose z items are few and
+            // each a chain of dependent L2 round trips (config 2: 29.2k → 35.6k it/s)
             const long long xrows = P.x1r - P.x0r;
             P.x_ctas = (int)std::max<long long>(1, (xrows + kZxWarps - 1) / kZxWarps);
             P.z_nslab = (int)std::max<long long>(1, (P.c1 - P.c0 + 511) / 512);
-            const long long jr = std::max(1, env_int("AXB_Z_JROWS", 128));
+            const long long jr = std::max(1, env_int("AXB_Z_JROWS", persist_path ? 32 : 128));
             P.z_jrows = (int)std::min<long long>((long long)q, jr);
             P.z_nj = (int)((q + P.z_jrows - 1) / P.z_jrows);
         }
@@ -875,11 +883,9 @@ struct axb_solver {
         // small systems (per-iteration working set L2-resident): one persistent
         // cooperative kernel per batch instead of a graph of 3 kernels/iteration
         {
-            const double ws = 8.0 * ((double)m * n + (double)q * n + 2.0 * p * q + (double)m * p);
-            const int force = env_int("AXB_PERSIST", -1);
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
-            P.persist = !sharded && (force == 1 || (force < 0 && ws <= 64e6));
+            P.persist = persist_path;
             // grid: enough SMs for the L2 bandwidth of R, few enough for cheap grid syncs
             const int want = (int)std::min<double>(sms, std::max(64.0, (double)m * n / 16384.0));
             P.persist_grid = env_int("AXB_PERSIST_GRID", want);
