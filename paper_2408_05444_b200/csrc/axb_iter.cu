@@ -2569,6 +2569,7 @@ int persist_grid(const Params& P) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = sizeof(double) * (size_t)((P.m + 31) / 32);
+    cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_persist, kPersistThreads, smem);
     return std::max(1, sms * std::min(per, 1));
 }
@@ -3033,8 +3034,8 @@ void launch_sel_greedy(const Params& P, cudaStream_t s) {
 // body's per-CTA refresh of every r_sq buys nothing there — measured slower)
 int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStream_t s) {
     const size_t smem = sizeof(double) * (size_t)((max_m + 31) / 32);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_persist_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // static shared memory counts against the 48 KB default too: always opt in
+    cudaFuncSetAttribute(k_persist_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_persist_batch<<<count, kBatchThreads, smem, s>>>(dPs);
     return (int)cudaGetLastError();
 }
@@ -3044,8 +3045,10 @@ int launch_persist(const Params& P, cudaStream_t s) {
         const int threads = P.persist_lat == 128 ? 128 : 256;
         const void* fn = threads == 128 ? (const void*)k_persist_lat<128> : (const void*)k_persist_lat<256>;
         const size_t smem = sizeof(double) * persist_lat_smem_doubles(P.m, threads);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // always opt in: the kernel's static shared memory (state copy, scan
+        // scratch) counts against the same 48 KB default — m = 2000 (48.5 KB
+        // dynamic + ~3 KB static) failed the cooperative launch without it
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -3058,6 +3061,7 @@ int launch_persist(const Params& P, cudaStream_t s) {
     }
     const int grid = std::min(P.persist_grid, persist_grid(P));
     const size_t smem = sizeof(double) * (size_t)((P.m + 31) / 32);
+    cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     Params Pc = P;
     void* args[] = {&Pc};
     return (int)cudaLaunchCooperativeKernel((const void*)k_persist, dim3((unsigned)grid),

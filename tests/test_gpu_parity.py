@@ -435,3 +435,22 @@ def test_large_copy_out_is_exact(axb):
     C2 = rng.standard_normal((64, 64))
     s2 = axb.Solver(A2, B2, C2, X0, cfg)
     assert np.array_equal(s2.X(), X0)
+
+
+@pytest.mark.parametrize("shape", [(2000, 100, 80, 1000), (2040, 48, 24, 1200), (1536, 64, 32, 900)])
+def test_latency_body_near_shared_memory_limit(axb, orc, shape):
+    """Latency-body systems whose selection state (3m + m/32 doubles) sits just under
+    48 KB of dynamic shared memory: with the kernel's static shared memory the
+    launch needs the opt-in (m = 2000 once failed the cooperative launch)."""
+    m, p, q, n = shape
+    A, B, X, Cm = O.generate(orc, 5, m, p, q, n)
+    cfg_o = O.make_config(method=O.GRBK, seed=42, stop_kind=O.SOLUTION_RRN, tol=0.0, reference=X,
+                          refresh_interval=0)
+    so = O.Solver(orc, A, B, Cm, None, cfg_o)
+    cfg = axb.SolveConfig(method=axb.Method.grbk(), stop=axb.StopRule.solution_rrn(0.0, X), seed=42,
+                          refresh_interval=0)
+    sg = axb.Solver(A, B, Cm, None, cfg)
+    ro, rg = so.steps(300), sg.steps(300)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
