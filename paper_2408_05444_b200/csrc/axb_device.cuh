@@ -133,6 +133,9 @@ struct Params {
                                  // shared memory, 2 barriers per iteration (m ≤ kPersistLatRows)
     const double* BtB;           // n×n BᵀB (solver.hpp:172) for z = BᵀB·R_iᵀ in one phase, or null
     int yg_grid, yg_rbq, yg_rbm;  // K4 grid; B rows / A rows per CTA
+    int yg_pf;                   // K4: bytes of its first B rows a CTA prefetches into L2
+                                 // before the selection it depends on has finished (0 = off)
+    int sel_early;               // K3 lets K4 launch (and prefetch) before K2 has drained
     int z_nslab, z_nj, z_jrows, x_ctas;
     int sel1_grid, pack_grid;  // sharded selection: membership CTAs, row-pack CTAs
     int sel_split, sel_grid;     // greedy pre-selection across sel_grid CTAs (k_sel_greedy)

@@ -269,6 +269,24 @@ constexpr int kYgSeg = 2048;
 __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
     __shared__ __align__(16) double vs[kYgSeg];
     __shared__ double part[kYgWarps];
+    if (P.yg_pf && (long long)blockIdx.x * P.yg_rbq < P.q) {
+        // B does not depend on the selected row: while the selection this launch
+        // waits on finishes (HBM otherwise idle), pull the head of this CTA's
+        // first B rows — the part its first segment reads — into L2
+        const int rb = P.yg_rbq;
+        const long long len8 = 8 * (P.c1 - P.c0);
+        const long long per = min(len8, (long long)(P.yg_pf / rb)) & ~4095LL;
+        const int cpr = (int)(per >> 12);  // 4 KB pieces per row
+        if (cpr > 0 && ((8 * (P.n | P.c0)) & 15) == 0) {
+            for (int t = threadIdx.x; t < rb * cpr; t += kYgThreads) {
+                const long long it = (long long)blockIdx.x * rb + t / cpr;
+                if (it >= P.q) break;
+                const char* src = reinterpret_cast<const char*>(P.B + it * P.n + P.c0) +
+                                  (long long)(t % cpr) * 4096;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], 4096;" ::"l"(src) : "memory");
+            }
+        }
+    }
     pdl_wait();
     pdl_trigger();
     const DevState* st = P.st;
@@ -1735,6 +1753,9 @@ __global__ void __launch_bounds__(kThreads) k_pack(Params P) {
 __global__ void __launch_bounds__(kThreads) k_sel_greedy(Params P) {
     __shared__ SelShared sh;
     __shared__ bool last;
+    // K4 (next in the stream) waits for this grid, which waits for K2, so letting
+    // it launch early is safe; it then prefetches B while K2 drains
+    if (P.sel_early) pdl_trigger();
     pdl_wait();
     pdl_trigger();
     DevState* st = P.st;

@@ -809,6 +809,9 @@ struct axb_solver {
             P.yg_rbm = rpc(m);
             const uint64_t blocks = (q + rbq - 1) / rbq + (gram_cached ? 0 : (m + P.yg_rbm - 1) / P.yg_rbm);
             P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, blocks));
+            if (const int e = env_int("AXB_YG_GRID", 0); e > 0) P.yg_grid = std::min(P.yg_grid, e);
+            P.yg_pf = std::max(0, env_int("AXB_YG_PF", 0));
+            P.sel_early = env_int("AXB_SEL_EARLY", 0);
         }
         // small systems run one persistent kernel per batch (decided below; the
         // z row chunks depend on it)
