@@ -149,6 +149,24 @@ def test_tall_system_mwrbk_sequence(axb, orc, path):
     assert rel(sg.X(), so.X()) <= RTOL_X
 
 
+@pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.RGRBK, 0.25), (O.MWRBK, None)])
+def test_k4_head_start_knobs(axb, orc, monkeypatch, tag, theta):
+    """Graph path with K4's L2 prefetch of B before its PDL wait, K3's early
+    trigger and a capped, grid-strided K4 (AXB_YG_PF / AXB_SEL_EARLY /
+    AXB_YG_GRID; off by default): B rows of 8 KB so the prefetch really issues,
+    m = 4096 so the greedy draw runs in k_sel_greedy.  Rows identical, X 1e-10."""
+    for k, v in (("AXB_PERSIST", "0"), ("AXB_YG_PF", "65536"), ("AXB_SEL_EARLY", "1"),
+                 ("AXB_YG_GRID", "7")):
+        monkeypatch.setenv(k, v)
+    A, B, X, Cm = O.generate(orc, 23, 4096, 48, 24, 1024)
+    so, sg = pair(axb, orc, A, B, Cm, None, tag, theta, seed=5, Xref=X)
+    ro = so.steps(600)
+    rg = sg.steps(600)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
+
+
 @pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.RGRBK, 0.8), (O.RBK, None),
                                        (O.BK, None)])
 def test_tall_system_replay(axb, orc, tag, theta, path):
