@@ -419,6 +419,14 @@ class PreparedSolver:
             raise OracleError(code, self.lib.last_error(self.h).decode())
         return rows[:k]
 
+    def X(self):
+        p, q = self._keep[0].shape[1], self._keep[1].shape[0]
+        out = np.empty((p, q)); self.lib.get_X(self.h, _ptr(out)); return out
+
+    def R(self):
+        m, n = self._keep[0].shape[0], self._keep[1].shape[1]
+        out = np.empty((m, n)); self.lib.get_R(self.h, _ptr(out)); return out
+
     def __del__(self):
         if getattr(self, "h", None):
             self.lib.destroy(self.h)
