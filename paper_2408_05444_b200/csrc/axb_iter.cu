@@ -2204,12 +2204,15 @@ __global__ void __launch_bounds__(kPersistThreads) k_persist(Params P) {
 // One CTA per system: Ps[blockIdx.x] describes an independent solve (its own
 // buffers and DevState).  Grid barriers become CTA barriers.
 // 512 threads: one CTA must carry a whole system's memory parallelism
+// (AXB_BATCH_THREADS=256 / 1024 select the 256-thread, two-per-SM or the
+// 1024-thread variant for sweeps)
 constexpr int kBatchThreads = 512;
-__global__ void __launch_bounds__(kBatchThreads, 1) k_persist_batch(const Params* __restrict__ Ps) {
+template <int kT>
+__global__ void __launch_bounds__(kT, kT <= 256 ? 2 : 1) k_persist_batch(const Params* __restrict__ Ps) {
     __shared__ Params sp;
     if (threadIdx.x == 0) sp = Ps[blockIdx.x];
     __syncthreads();
-    persist_body<SoloGroup, kBatchThreads>(sp, SoloGroup{});
+    persist_body<SoloGroup, kT>(sp, SoloGroup{});
 }
 
 // ------------------------------------------------------------------------
@@ -3056,8 +3059,28 @@ void launch_sel_greedy(const Params& P, cudaStream_t s) {
 int launch_persist_batch(const Params* dPs, int count, long long max_m, cudaStream_t s) {
     const size_t smem = sizeof(double) * (size_t)((max_m + 31) / 32);
     // static shared memory counts against the 48 KB default too: always opt in
-    cudaFuncSetAttribute(k_persist_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_persist_batch<<<count, kBatchThreads, smem, s>>>(dPs);
+    // two 256-thread systems per SM once there are at least two per SM: one CTA's
+    // serial phases (selection, reductions) then overlap the other's streaming.
+    // Config-1 systems, 2000 steps (tools/prof_batch.py): 296 / 592 systems
+    // 845k → 869k / 847k → 874k it/s; 148 systems stay on 512 threads (615k on 256)
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* e = getenv("AXB_BATCH_THREADS");
+    const int forced = e ? atoi(e) : 0;
+    const int threads = (forced == 256 || forced == 512 || forced == 1024) ? forced
+                        : (count >= 2 * sms ? 256 : kBatchThreads);
+    if (threads == 256) {
+        cudaFuncSetAttribute(k_persist_batch<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_persist_batch<256><<<count, 256, smem, s>>>(dPs);
+    } else if (threads == 1024) {
+        cudaFuncSetAttribute(k_persist_batch<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_persist_batch<1024><<<count, 1024, smem, s>>>(dPs);
+    } else {
+        cudaFuncSetAttribute(k_persist_batch<kBatchThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        k_persist_batch<kBatchThreads><<<count, kBatchThreads, smem, s>>>(dPs);
+    }
     return (int)cudaGetLastError();
 }
 
