@@ -714,6 +714,14 @@ def main():
         del Ad, Bd, Cd, X0d, Xsd
         torch.cuda.empty_cache()
         h2d = sum(v.nbytes for v in host.values() if v is not None)
+        # one untimed warm-up pass of the same calls (create, W steps, X()), as the
+        # device-timed value has its W warm-up steps: the first create of a given
+        # size in a process pays the driver's first mapping of its ~41 GB (config 5:
+        # 0.9-1.2 s instead of ~0.5 s, tools/e2e_breakdown.py)
+        w = make_solver(host["A"], host["B"], host["C"], host["X0"], host["Xs"], budget=args.steps)
+        w.steps(args.warmup, mirror_refresh=True)
+        w.X()
+        del w
         barrier()
         t0 = time.perf_counter()
         # the user's budget is the K iterations it asks for (max_iter = K): the
@@ -731,7 +739,8 @@ def main():
                "gram_cached": gram,
                "what": "Solver(host A,B,C,X0,X*, max_iter=K) -> steps(K) -> X() through the "
                        "C-ABI; includes H2D of the system, device ||B||_2, R0 (DMMA), G=A.A^T "
-                       "when K repays forming it (else g=A.A_i^T per step), D2H of X"}
+                       "when K repays forming it (else g=A.A_i^T per step), D2H of X; after one "
+                       "untimed warm-up pass of the same calls with W steps"}
         del s2
         host = None
 

@@ -589,15 +589,11 @@ struct axb_solver {
 
         const cudaMemcpyKind kind =
             opt.inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        A.alloc(m * p, "A");
-        B.alloc(q * n, "B");
-        C.alloc(m * n, "C");
-        R.alloc(m * n, "R");
-        X.alloc(p_loc * world * q, "X");
-        if (p_loc * world > p)
-            ck(cudaMemsetAsync(X.p, 0, sizeof(double) * p_loc * world * q, stream), "X pad");
         // inputs arrive on a copy stream in the order they are needed; the
-        // compute stream waits per input, so ‖B‖₂ (and G) overlap the C copy
+        // compute stream waits per input, so ‖B‖₂ (and G) overlap the C copy.
+        // Each buffer is allocated just before its copy is queued, so mapping the
+        // later ones (C, X, R: 35 GB at config 5) overlaps the earlier copies
+        A.alloc(m * p, "A");
         cudaStream_t cs = nullptr;
         ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
         cudaEvent_t evA, evB, evRest;
@@ -615,13 +611,16 @@ struct axb_solver {
                 cudaStreamDestroy(s);
             }
         } guard{cs, evA, evB, evRest};
-        ck(cudaEventRecord(ev0, stream), "event");  // X pad before the X0 copy
-        ck(cudaStreamWaitEvent(cs, ev0, 0), "wait");
         ck(cudaMemcpyAsync(A.p, A_in, sizeof(double) * m * p, kind, cs), "copy A");
         ck(cudaEventRecord(evA, cs), "event");
+        B.alloc(q * n, "B");
         ck(cudaMemcpyAsync(B.p, B_in, sizeof(double) * q * n, kind, cs), "copy B");
         ck(cudaEventRecord(evB, cs), "event");
+        C.alloc(m * n, "C");
         ck(cudaMemcpyAsync(C.p, C_in, sizeof(double) * m * n, kind, cs), "copy C");
+        X.alloc(p_loc * world * q, "X");
+        if (p_loc * world > p)  // X pad, before the X0 copy on the same stream
+            ck(cudaMemsetAsync(X.p, 0, sizeof(double) * p_loc * world * q, cs), "X pad");
         if (X0_in)
             ck(cudaMemcpyAsync(X.p, X0_in, sizeof(double) * p * q, kind, cs), "copy X0");
         else
@@ -632,6 +631,7 @@ struct axb_solver {
                "copy reference");
         }
         ck(cudaEventRecord(evRest, cs), "event");
+        R.alloc(m * n, "R");
         ck(cudaStreamWaitEvent(stream, evA, 0), "wait A");
         a_sq.alloc(m, "a_sq");
         rbk_cum.alloc(m_g, "rbk_cum");
