@@ -109,6 +109,11 @@ typedef struct {
     int32_t rank;
     uint64_t m_global;
     uint64_t row_offset;
+    /* SMs this handle's persistent kernel (small systems) may occupy, 0 = all: set
+     * it to share one GPU between handles that run concurrently on their own host
+     * threads (e.g. config 4's colour channels: three handles at SMs/3 each). */
+    int32_t sm_share;
+    int32_t _pad0;
 } axb_options;
 
 typedef struct axb_solver axb_solver;

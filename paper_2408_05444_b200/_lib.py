@@ -72,6 +72,8 @@ class AxbOptions(C.Structure):
         ("rank", C.c_int32),
         ("m_global", C.c_uint64),
         ("row_offset", C.c_uint64),
+        ("sm_share", C.c_int32),
+        ("_pad0", C.c_int32),
     ]
 
 

@@ -888,6 +888,7 @@ struct axb_solver {
         {
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
+            if (opt.sm_share > 0) sms = std::min(sms, (int)opt.sm_share);
             P.persist = persist_path;
             // grid: enough SMs for the L2 bandwidth of R, few enough for cheap grid syncs
             const int want = (int)std::min<double>(sms, std::max(64.0, (double)m * n / 16384.0));

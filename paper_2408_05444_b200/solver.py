@@ -178,6 +178,9 @@ class Options:
     rank: int = 0
     m_global: int = 0
     row_offset: int = 0
+    # SMs the persistent kernel of this handle may occupy (0 = all): handles that
+    # run concurrently from their own host threads share one GPU
+    sm_share: int = 0
 
 
 def _device_ptr(a):
@@ -277,6 +280,7 @@ class Solver:
         o.rank = opts.rank
         o.m_global = opts.m_global
         o.row_offset = opts.row_offset
+        o.sm_share = opts.sm_share
         h = C.c_void_p()
         if _is_csr(A) or _is_csr(B):
             if on_dev:

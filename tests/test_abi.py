@@ -52,6 +52,7 @@ def test_options_defaults_and_struct_layouts():
     _lib.load().axb_options_default(C.byref(o))
     assert (o.cache_gram, o.spectral_on_device, o.tie_guard, o.world_size) == (-1, -1, 1, 1)
     assert C.sizeof(_lib.AxbConfig) == 80 and C.sizeof(_lib.AxbReport) == 88
+    assert C.sizeof(_lib.AxbOptions) == 80 and o.sm_share == 0
 
 
 def test_no_device_fails_loudly():

@@ -325,6 +325,39 @@ def test_config4_blur_channel_fixed_budget(axb, orc):
     assert rel(sg.R(), so.R()) <= 1e-9
 
 
+def test_concurrent_handles_on_sm_shares(axb, orc):
+    """Three config-4-style channels (n = 256) on one GPU at once, each handle's
+    persistent kernel on a third of the SMs (Options.sm_share) and driven from its
+    own host thread: every channel gives the oracle's rows and X (bench.py's
+    schedule for several channels per GPU)."""
+    import threading
+
+    import configs
+
+    chans = [configs.config4_channel(seed=10 + c, nn=256, half_band=7) for c in range(3)]
+    share = 148 // 3
+    ref, dev = [None] * 3, [None] * 3
+    for c, (A, B, Xs, Cm) in enumerate(chans):
+        so, _ = pair(axb, orc, A, B, Cm, None, O.GRBK, seed=42 + c, Xref=Xs)
+        ref[c] = (so.steps(1500), so.X())
+    handles = [pair(axb, orc, A, B, Cm, None, O.GRBK, seed=42 + c, Xref=Xs,
+                    options=axb.Options(sm_share=share))[1]
+               for c, (A, B, Xs, Cm) in enumerate(chans)]
+
+    def run(c):
+        dev[c] = (handles[c].steps(1500), handles[c].X())
+
+    th = [threading.Thread(target=run, args=(c,)) for c in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for c in range(3):
+        mism = np.nonzero(ref[c][0] != dev[c][0])[0]
+        assert mism.size == 0, f"channel {c}: first row mismatch at step {mism[:5]}"
+        assert rel(dev[c][1], ref[c][1]) <= RTOL_X
+
+
 @pytest.mark.parametrize("tag", [O.MWRBK, O.GRBK])
 def test_csr_operands_match_dense_and_oracle(axb, orc, tag):
     """solve(const Matrix&…) with CSR A and B (test_solver.cpp:546-561): the CSR
