@@ -1,3 +1,5 @@
+"""Config 4 e2e phases (3 channels, 200 steps): create, concurrent steps and X()
+per share of the SMs, and each channel's whole round trip on its own thread."""
 import sys, time, threading
 sys.path.insert(0, ".")
 import torch
