@@ -325,6 +325,27 @@ def test_config4_blur_channel_fixed_budget(axb, orc):
     assert rel(sg.R(), so.R()) <= 1e-9
 
 
+@pytest.mark.parametrize("on_device", [0, 1])
+def test_spectral_cap_raises_convergence_error_like_the_reference(axb, orc, on_device):
+    """The reference constructor's spectral_norm(B) (tol 1e-10, cap 5000,
+    decomp.hpp:207-239) throws ConvergenceError for config 4's 1024-wide blur
+    (SURVEY §8(c)(i)); the oracle and the device path (‖B‖₂ on the host or on the
+    device) raise it too, and a raised cap lets all of them through."""
+    import configs
+
+    A, B, Xs, Cm = configs.config4_channel(seed=4, nn=1024, half_band=7)
+    cfg_o = O.make_config(method=O.GRBK, stop_kind=O.RESIDUAL_REL, tol=0.0)
+    with pytest.raises(O.OracleError) as ei:
+        O.Solver(orc, A, B, Cm, None, cfg_o)
+    assert ei.value.code == 6  # ORC_CONVERGENCE_ERROR
+    cfg = axb.SolveConfig(method=axb.Method.grbk(), stop=axb.StopRule.residual_rel(0.0))
+    with pytest.raises(axb.ConvergenceError):
+        axb.Solver(A, B, Cm, None, cfg, axb.Options(spectral_on_device=on_device))
+    s = axb.Solver(A, B, Cm, None, cfg,
+                   axb.Options(spectral_on_device=on_device, spectral_max_iter=200000))
+    assert 0.9999 < s.spectral_norm_b() < 1.0
+
+
 def test_concurrent_handles_on_sm_shares(axb, orc):
     """Three config-4-style channels (n = 256) on one GPU at once, each handle's
     persistent kernel on a third of the SMs (Options.sm_share) and driven from its
