@@ -778,8 +778,16 @@ struct axb_solver {
         if (P.r_tma) {
             // TMA ring: 2 CTAs per SM, rows split evenly, tiles of ≤2048 columns
             // (tunable for sweeps: AXB_R_CPS, AXB_R_STAGES, AXB_R_TILE)
-            const int cps = env_int("AXB_R_CPS", 2), stages = env_int("AXB_R_STAGES", 4);
-            const int tile = env_int("AXB_R_TILE", 1024);
+            const int cps = env_int("AXB_R_CPS", 2);
+            // few rows per CTA on wide rows (config 3: 28 rows of 8192 per CTA): two
+            // 2048-column stages, same ring bytes, half the per-tile handshakes
+            // (config 3 K2 0.1829 → 0.1818 ms, 3,785 → 3,824 it/s); many rows per CTA
+            // (config 5: 221) keep four 1024-column stages (161.3 vs 160.9 it/s), and
+            // so do rows longer than 16384 (config 5's world-8 shard, measured at the
+            // copy roofline with 1024 × 4)
+            const bool wide = m <= (uint64_t)64 * 148 * cps && n >= 4096 && n <= 16384;
+            const int stages = env_int("AXB_R_STAGES", wide ? 2 : 4);
+            const int tile = env_int("AXB_R_TILE", wide ? 2048 : 1024);
             P.r_grid = (int)std::min<uint64_t>((uint64_t)148 * cps, m);
             P.r_rows_per_cta = (int)((m + P.r_grid - 1) / P.r_grid);
             P.r_chunk = (int)std::min<uint64_t>(n, (uint64_t)tile);

@@ -167,6 +167,21 @@ def test_k4_head_start_knobs(axb, orc, monkeypatch, tag, theta):
     assert rel(sg.X(), so.X()) <= RTOL_X
 
 
+@pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.MWRBK, None)])
+def test_graph_path_wide_rows(axb, orc, monkeypatch, tag, theta):
+    """Graph path with few rows per K2 CTA on wide rows (m = 4096, n = 4096: the
+    two-stage 2048-column ring): rows identical to the oracle, X within 1e-10."""
+    monkeypatch.setenv("AXB_PERSIST", "0")
+    A, B, X, Cm = O.generate(orc, 29, 4096, 40, 20, 4096)
+    so, sg = pair(axb, orc, A, B, Cm, None, tag, theta, seed=8, Xref=X)
+    ro = so.steps(400)
+    rg = sg.steps(400)
+    mism = np.nonzero(ro != rg)[0]
+    assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+    assert rel(sg.X(), so.X()) <= RTOL_X
+    assert rel(sg.R(), so.R()) <= 1e-9
+
+
 @pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.RGRBK, 0.8), (O.RBK, None),
                                        (O.BK, None)])
 def test_tall_system_replay(axb, orc, tag, theta, path):
