@@ -19,10 +19,23 @@ iterations / max-over-ranks device time.  A is generated in 8 fixed row blocks,
 so the global system is bit-identical at N = 1, 2, 4, 8.  --shard forces the
 sharded code path on one GPU (1-rank communicator).
 
+--gpus N without torchrun: bench.py re-launches itself under
+torch.distributed.run with N ranks (it refuses when fewer than N GPUs are
+visible); under torchrun, WORLD_SIZE must equal --gpus.
+
+The default N=1 run (config 5) also measures configs 1-4 in the same process
+and carries them under "configs" (each with its own steps, roofline,
+cpu_baseline and e2e), so every BASELINE config is in the driver's BENCH line.
+
 --impl reference: the reference's own engine on the host cores — the unmodified
 axb::Solver compiled from /root/reference into oracle/_ref (kind "reference"; the
 bitwise-equal C port only where _ref is absent) — one solver per core as the
-reference's benchmark pool runs trials (analysis.hpp:295-313).
+reference's benchmark pool runs trials (analysis.hpp:295-313).  Config 5 does not
+fit the reference's constructor on a host (G = A·Aᵀ alone is 34 GB and ~10¹⁴
+FLOP), so it runs on the 1/8-per-dimension instance: "steps" / "ms_per_step"
+are what actually ran there, and "value" is the config-5-equivalent rate (every
+per-iteration term of the reference shrinks by exactly 64; the rule is checked
+at the literal size by tools/config5_cpu_literal.py).
 """
 from __future__ import annotations
 
@@ -232,24 +245,44 @@ def psnr(ref_planes, test_planes):
     return float("inf") if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
 
 
-def channels_arm(args, cfg, rank, world, local):
+class Ctx:
+    """Process-level run context: ranks, device, collective plumbing."""
+
+    def __init__(self, rank, world, local):
+        self.rank, self.world, self.local = rank, world, local
+
+    def allmax(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.synchronize(self.local)
+        if self.world > 1:
+            dist.barrier()
+
+
+def channels_arm(args, cfg, ctx, steps, warmup, with_cpu=True, cpu_budget_s=15.0):
     """Config 4: independent colour channels, channel c on rank c mod N (no
-    collective: the channels share nothing).  Each rank runs its channels one
-    after another on its GPU; value = all channel-iterations ÷ the slowest rank's
-    device time."""
-    import numpy as np
+    collective: the channels share nothing).  A rank's channels run concurrently,
+    each handle's persistent kernel on its share of the SMs; value = all
+    channel-iterations ÷ the slowest rank's device time."""
+    import threading
+
     import torch
     import torch.distributed as dist
 
     import paper_2408_05444_b200 as axb
 
-    def allmax(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
+    rank, world, local = ctx.rank, ctx.world, ctx.local
     mine = [c for c in range(cfg["channels"]) if c % world == rank]
     data = {c: make_channel(cfg, 4, c) for c in mine}
     mk = lambda: axb.SolveConfig(method=axb.Method.grbk(), stop=axb.StopRule.residual_rel(0.0),  # noqa: E731
@@ -257,8 +290,6 @@ def channels_arm(args, cfg, rank, world, local):
     # ‖B‖₂ on the device: the blur's top singular gap is tiny (the reference's own
     # power iteration needs >5000 steps and throws), and no oracle needs
     # the host-order α bit for bit at n = 1024
-    # a rank with several channels runs them concurrently, each handle's persistent
-    # kernel on its share of the SMs and driven from its own host thread
     # (tools/config4_concurrent.py: 3 channels on one B200, 49.9k it/s one after
     # another on the whole chip, 114.8k concurrently on 49 SMs each)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
@@ -266,15 +297,11 @@ def channels_arm(args, cfg, rank, world, local):
     opts = axb.Options(device=local, spectral_max_iter=200000, spectral_on_device=1, sm_share=share)
     solvers = {c: axb.Solver(d[0], d[1], d[2], None, mk(), opts) for c, d in data.items()}
     for s in solvers.values():
-        s.steps(args.warmup)
-    torch.cuda.synchronize(local)
-    if world > 1:
-        dist.barrier()
+        s.steps(warmup)
+    ctx.barrier()
     clocks = ClockSampler(local)
     clocks.start()
-    import threading
-
-    th = [threading.Thread(target=s.steps, args=(args.steps,)) for s in solvers.values()]
+    th = [threading.Thread(target=s.steps, args=(steps,)) for s in solvers.values()]
     torch.cuda.synchronize(local)
     t0 = time.perf_counter()
     for t in th:
@@ -288,8 +315,8 @@ def channels_arm(args, cfg, rank, world, local):
     dev_ms = max([wall_ms] + [s.last_timing()["loop_ms"] for s in solvers.values()])
     launches = sum(s.last_timing()["kernel_launches"] for s in solvers.values())
     ck = clocks.stop()
-    ms = allmax(dev_ms)
-    units = args.steps * cfg["channels"]
+    ms = ctx.allmax(dev_ms)
+    units = steps * cfg["channels"]
     value = units / (ms / 1000.0)
     # quality after the budget: PSNR against X* (imaging.hpp:202-215), ‖R‖/‖C‖
     planes = {c: (solvers[c].X(), data[c][3], solvers[c].current_residual_rel()) for c in mine}
@@ -300,7 +327,7 @@ def channels_arm(args, cfg, rank, world, local):
     order = sorted(planes)
     quality = {"psnr_db": round(psnr([planes[c][1] for c in order], [planes[c][0] for c in order]), 3),
                "residual_rel": [round(planes[c][2], 6) for c in order],
-               "iterations_per_channel": args.warmup + args.steps}
+               "iterations_per_channel": warmup + steps}
     # latency-bound L2-resident working set: algorithmic bytes per iteration (touched
     # R rows, B twice, X rows of the band) over the device time, against HBM peak
     peak, peak_kind = peaks()
@@ -308,67 +335,60 @@ def channels_arm(args, cfg, rank, world, local):
     nn = cfg["n"]
     touched = min(nn, 4 * hb + 1)
     it_bytes = 16 * touched * nn + 16 * nn * nn + 16 * (2 * hb + 1) * nn + 8 * (2 * nn)
-    per_it_s = dev_ms / 1000.0 / (args.steps * max(1, len(mine)))
+    per_it_s = dev_ms / 1000.0 / (steps * max(1, len(mine)))
     achieved = it_bytes / per_it_s / 1e9
     # e2e: the public API from host buffers — create every channel's solver
     # (H2D, ‖B‖₂, G, R0), K steps, X back — slowest rank, wall clock
     e2e = None
     if not args.no_e2e:
         solvers = None  # release the timed handles first
-        torch.cuda.synchronize(local)
-        if world > 1:
-            dist.barrier()
+        ctx.barrier()
         # the handles are created one after another (a create's device ‖B‖₂ would
         # otherwise run on the SMs the other channels' persistent kernels leave
         # free), then iterate concurrently, then X() comes back per channel
         t0 = time.perf_counter()
         hs = [axb.Solver(d[0], d[1], d[2], None, mk(), opts) for d in data.values()]
-        th = [threading.Thread(target=h.steps, args=(args.steps,)) for h in hs]
+        th = [threading.Thread(target=h.steps, args=(steps,)) for h in hs]
         for t in th:
             t.start()
         for t in th:
             t.join()
         outs = [h.X() for h in hs]
         torch.cuda.synchronize(local)
-        e2e_s = allmax(time.perf_counter() - t0)
+        e2e_s = ctx.allmax(time.perf_counter() - t0)
         h2d = sum(d[0].nbytes + d[1].nbytes + d[2].nbytes for d in data.values())
         d2h = sum(o.nbytes for o in outs)
         e2e = {"value": units / e2e_s, "unit": "iter/s",
-               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
                "seconds": round(e2e_s, 4),
-"what": "Solver(host A,B,C) per channel, then steps(K) of every channel "
+               "what": "Solver(host A,B,C) per channel, then steps(K) of every channel "
                        "concurrently, then X() per channel, through the C-ABI"}
         del hs
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
-    if rank == 0:
-        line = {
-            "metric": "kaczmarz_iterations_per_sec", "value": round(value, 2), "unit": "iter/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (numpy seeded blur operator, smooth field, Gaussian noise)",
-            "config": {"workload": cfg["desc"], "m": nn, "p": nn, "q": nn, "n": nn,
-                       "channels": cfg["channels"], "method": "grbk", "refresh_interval": 1000,
-                       "parallelism": f"channel c on GPU c mod {world} (independent solves, no collective; "
-                                      f"a GPU's channels run concurrently on equal SM shares)",
-                       "l2": "per-channel working set (40 MB) is L2-resident: latency-bound"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "persistent iteration kernel (y, z, X, banded R update, select)",
-                         "algorithmic_bytes_per_iteration": it_bytes,
-                         "note": "L2-resident and latency-bound; HBM fraction shown for scale only"},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": ck,
-            "quality": quality,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    if rank == 0 and with_cpu:
+        cpu = cpu_baseline(cfg, cpu_budget_s)
+    return {
+        "metric": "kaczmarz_iterations_per_sec", "value": round(value, 2), "unit": "iter/s",
+        "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": round(ms / steps, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (numpy seeded blur operator, smooth field, Gaussian noise)",
+        "config": {"workload": cfg["desc"], "m": nn, "p": nn, "q": nn, "n": nn,
+                   "channels": cfg["channels"], "method": "grbk", "refresh_interval": 1000,
+                   "parallelism": f"channel c on GPU c mod {world} (independent solves, no collective; "
+                                  f"a GPU's channels run concurrently on equal SM shares)",
+                   "l2": "per-channel working set (40 MB) is L2-resident: latency-bound"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "k_persist (persistent iteration kernel: y, z, X, banded R update, select)",
+                     "algorithmic_bytes_per_iteration": it_bytes,
+                     "note": "L2-resident and latency-bound; HBM fraction shown for scale only"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": ck,
+        "quality": quality,
+    }
 
 
 def solver_config(axb, Xs, max_iter, method="grbk"):
@@ -378,20 +398,23 @@ def solver_config(axb, Xs, max_iter, method="grbk"):
                            seed=42, refresh_interval=1000)
 
 
-def k2_bytes(cfg):
-    """Algorithmic bytes of one fused residual-update launch:
-    read+write R (16·m·n), read the G column and z, write ‖R_l‖² (8·(2m+n))."""
-    m, n = cfg["m"], cfg["n"]
+def k2_bytes(cfg, world=1):
+    """Algorithmic bytes of one fused residual-update launch on one
+    rank: read+write its R rows (16·m_loc·n), read the G column and z, write
+    ‖R_l‖² (8·(2·m_loc + n)); m_loc = m / world."""
+    m, n = cfg["m"] // world, cfg["n"]
     return 16 * m * n + 8 * (2 * m + n)
 
 
-def iteration_bytes(cfg, gram_cached=True, track_ref=True):
-    """Whole-iteration algorithmic bytes: K2, two passes over B (y, z), X read and
-    written, X_ref read for the solution_rrn error (the reference's err_sq update
-    in update_row, solver.hpp:272-289; the bench's stop rule), and the G column
-    (or A once more for g = A·A_iᵀ when G is not cached)."""
-    m, p, q, n = cfg["m"], cfg["p"], cfg["q"], cfg["n"]
-    return (k2_bytes(cfg) + 16 * q * n + 16 * p * q + (8 * p * q if track_ref else 0)
+def iteration_bytes(cfg, gram_cached=True, track_ref=True, world=1):
+    """Whole-iteration algorithmic bytes on one rank: K2, two passes over its
+    column slice of B (y, z), its rows of X read and written, X_ref read for the
+    solution_rrn error (the reference's err_sq update in update_row,
+    solver.hpp:272-289; the bench's stop rule), and the G column (or its rows of A
+    once more for g = A·A_iᵀ when G is not cached)."""
+    m, p, q, n = cfg["m"] // world, cfg["p"], cfg["q"], cfg["n"]
+    nl, pl = -(-n // world), -(-p // world)
+    return (k2_bytes(cfg, world) + 16 * q * nl + 16 * pl * q + (8 * pl * q if track_ref else 0)
             + (8 * m if gram_cached else 8 * m * p))
 
 
@@ -516,7 +539,8 @@ def reference_arm(args, cfg):
         x.start()
     for x in th:
         x.join()
-    log(f"[reference] {T} constructors in {time.perf_counter() - t0:.1f}s")
+    ctor_s = time.perf_counter() - t0
+    log(f"[reference] {T} constructors in {ctor_s:.1f}s")
     # warmup (W iterations spread over the pool)
     wper = max(1, math.ceil(args.warmup / T))
     for s in solvers:
@@ -542,121 +566,66 @@ def reference_arm(args, cfg):
         x.join()
     dt = time.perf_counter() - t0
     total = sum(counts)
-    value = total / dt / factor
+    sample_rate = total / dt  # iterations/s actually run, on the instance actually run
+    value = sample_rate / factor  # config-equivalent rate (== sample_rate when factor is 1)
     shape = f"{scfg['m']}x{scfg['p']}.{scfg['q']}x{scfg['n']}"
-    extra = (f"; instance {shape} (every dimension /{cfg['cpu_div']}), time extrapolated "
-             f"x{factor}" if factor > 1 else "")
+    extra = (f"; instance {shape} (every dimension /{cfg['cpu_div']}), config-{cfg['m']}x{cfg['p']}."
+             f"{cfg['q']}x{cfg['n']}-equivalent rate = sample rate / {factor}" if factor > 1 else "")
     engine = ("unmodified reference axb::Solver::step() (oracle/_ref, -O3 -DNDEBUG)"
               if kind == "reference" else "oracle C port of solver.hpp step()")
     line = {
         "impl": "reference",
         "metric": "kaczmarz_iterations_per_sec", "value": value, "unit": "iter/s",
-        "n_gpus": args.gpus, "steps": total, "warmup": wper * T,
-        "ms_per_step": 1000.0 * dt * factor / total,
+        "n_gpus": args.gpus,
+        # what actually ran: `steps` iterations over the pool in steps × ms_per_step
+        "steps": total, "warmup": wper * T,
+        "ms_per_step": 1000.0 * dt / total,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": ("synthetic (numpy seeded blur operator, smooth field, noise)" if "channels" in cfg
                  else "synthetic (numpy seeded N(0,1))"),
         "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
                    "n": cfg["n"], "method": cfg.get("method", "grbk"),
                    "parallelism": f"{T} independent solves"},
+        "sample": {"instance": shape, "solvers": T, "iterations": total, "seconds": round(dt, 3),
+                   "iter_per_s": sample_rate, "constructors_s": round(ctor_s, 1)},
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": T, "kind": kind,
                          "sample": f"{T} concurrent solves x {per} iterations (reference "
                                    f"benchmark-pool pattern), {engine}, {dt:.1f}s wall{extra}"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if factor > 1:
+        line["extrapolation"] = {
+            "factor": factor, "value_is": "sample iter_per_s / factor",
+            "rule": ("each per-iteration term of the reference (R update m*n, z = B^T B R_i^T n^2, "
+                     "y q*n, X p*q) shrinks by exactly cpu_div^2 on the instance with every "
+                     "dimension divided by cpu_div"),
+            "literal_size_check": "tools/config5_cpu_literal.py (profiles/r2_config5_cpu_literal.json)"}
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------- GPU arm
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-tol", action="store_true")
-    ap.add_argument("--profile-steps", type=int, default=50)
-    ap.add_argument("--ref-threads", type=int, default=0,
-                    help="reference arm solver threads (0: every host thread this process may use)")
-    ap.add_argument("--ref-budget-s", type=float, default=60.0)
-    ap.add_argument("--shard", action="store_true",
-                    help="use the row-sharded path even on one GPU (1-rank NCCL communicator)")
-    ap.add_argument("--watchdog-s", type=float, default=1500.0)
-    ap.add_argument("--half-band", type=int, default=None,
-                    help="config 4: blur half-band (default 7; BASELINE's 'bandwidth 15' read "
-                         "as half-band 7, half-band 15 the other reading, SURVEY §8 D4)")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    cfg = dict(CONFIGS[args.config])
-    if args.half_band is not None and "half_band" in cfg:
-        cfg["desc"] = cfg["desc"].replace(f"half-band {cfg['half_band']}", f"half-band {args.half_band}")
-        cfg["half_band"] = args.half_band
+# Sub-configurations measured in the default N=1 run, each with the number of
+# timed iterations that keeps its timed region ≳ 0.1 s: config 1 (13 µs/iteration),
+# config 2 (its BASELINE budget, 10⁴ MWRBK steps), config 3 (short of the first
+# refresh), config 4 (3 channels concurrently).
+SUB_STEPS = {1: 20000, 2: 10000, 3: 600, 4: 20000}
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
 
-    if args.impl == "reference":
-        if rank == 0:
-            reference_arm(args, cfg)
-        return
-    if "channels" in cfg:
-        import faulthandler
-
-        faulthandler.dump_traceback_later(args.watchdog_s, exit=True)
-        import torch
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        if world > 1:
-            dist.init_process_group("gloo")
-        channels_arm(args, cfg, rank, world, local)
-        return
-
-    import faulthandler
-
-    faulthandler.dump_traceback_later(args.watchdog_s, exit=True)  # never hang the box
-
+def system_arm(args, cfg, cfg_id, ctx, steps, warmup, sharded=False, comm=0,
+               with_cpu=True, cpu_budget_s=15.0, with_tol=False):
+    """One system (single GPU, or row-sharded over the ranks); returns the line."""
     import torch
-    import torch.distributed as dist
 
     import paper_2408_05444_b200 as axb
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("gloo")
-
-    def barrier():
-        torch.cuda.synchronize(local)
-        if world > 1:
-            dist.barrier()
-
-    def allmax(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
+    rank, world, local = ctx.rank, ctx.world, ctx.local
     seed = 1000
     max_iter = 10 ** 9
-    sharded = world > 1 or args.shard
-    comm = 0
     if sharded:
         from paper_2408_05444_b200 import shard
-
-        with stdout_to_stderr():
-            if world == 1:
-                comm = shard.nccl_comm_create(1, shard.nccl_unique_id(), 0, local)
-            else:
-                comm, _, _ = shard.init_comm(local)
     log(f"[rank {rank}] generating {cfg['desc']} (rows {rank}/{world})")
     A, B, C, X0, Xs = make_inputs_device(cfg, seed, local, world, rank)
     sopts = dict(spectral_max_iter=200000)
-
     meth = cfg.get("method", "grbk")
 
     def make_solver(A_, B_, C_, X0_, Xs_, budget=max_iter):
@@ -671,53 +640,72 @@ def main():
     setup_s = time.perf_counter() - t0
     del A, B, C, X0
     torch.cuda.empty_cache()
-    log(f"[rank {rank}] solver ready in {setup_s:.2f}s, alpha={s.alpha():.6e}")
+    log(f"[rank {rank}] config {cfg_id}: solver ready in {setup_s:.2f}s, alpha={s.alpha():.6e}")
 
     # warmup, then exactly K timed steps (device events on the solver stream)
-    s.steps(args.warmup, mirror_refresh=True)
+    s.steps(warmup, mirror_refresh=True)
     clocks = ClockSampler(local)
-    barrier()
+    ctx.barrier()
     clocks.start()
-    barrier()
-    s.steps(args.steps, mirror_refresh=True)
-    barrier()
+    ctx.barrier()
+    s.steps(steps, mirror_refresh=True)
+    ctx.barrier()
     ck = clocks.stop()
     tm = s.last_timing()
-    ms = allmax(tm["loop_ms"])
+    ms = ctx.allmax(tm["loop_ms"])
     launches = tm["kernel_launches"]
-    value = args.steps / (ms / 1000.0)  # K global iterations of one system
-    log(f"[rank {rank}] {args.steps} iterations in {tm['loop_ms']:.2f} ms -> "
-        f"{args.steps / (tm['loop_ms'] / 1000):.1f} it/s")
-
-    # dominant kernel K2 (fused residual update): CUDA events around each launch
-    s.set_profiling(True)
-    s.steps(args.profile_steps, mirror_refresh=False)
-    pt = s.last_timing()
-    kt = s.kernel_times()
-    s.set_profiling(False)
-    k2_ms = pt["k2_ms"] / max(pt["k2_launches"], 1)
+    persistent = launches < steps  # one persistent kernel runs a whole batch
+    value = steps / (ms / 1000.0)  # K global iterations of one system
+    log(f"[rank {rank}] config {cfg_id}: {steps} iterations in {tm['loop_ms']:.2f} ms -> "
+        f"{steps / (tm['loop_ms'] / 1000):.1f} it/s")
+    per_iter_ms = ms / steps
     peak, peak_kind = peaks()
-    kb = k2_bytes(cfg)
-    achieved = kb / (k2_ms / 1000.0) / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", f"k2_traffic_config{args.config}.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    per_iter_ms = ms / args.steps
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_r_tma<true> (fused R update + row norms, TMA ring) timed together with "
-                          "k_sel_greedy (next-row greedy select across the SMs)",
-                "algorithmic_bytes_per_launch": kb, "k2_ms": round(k2_ms, 5),
-                "peak_kind": peak_kind,
-                "k2_share_of_step": round(k2_ms / per_iter_ms, 4),
-                "in_pipeline_ms": {"k_yg": round(kt["yg_ms"], 5), "k_zx": round(kt["zx_ms"], 5),
-                                   "k_r_tma": round(kt["k2_ms"], 5)},
-                "iteration_bytes": iteration_bytes(cfg),
-                "iteration_achieved_gbs": round(iteration_bytes(cfg) / (per_iter_ms / 1000) / 1e9, 1)}
+    gram = bool(s.gram_cached())
+    it_bytes = iteration_bytes(cfg, gram, world=world)
+    coll = None
+    if persistent:
+        # the dominant (only) kernel is the persistent iteration kernel: its
+        # algorithmic bytes per launch over its launch time = per iteration
+        achieved = it_bytes / (per_iter_ms / 1000.0) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                    "kernel": "k_persist (one persistent cooperative kernel per batch: select, y, z/X, "
+                              "fused R update + norms)",
+                    "algorithmic_bytes_per_iteration": it_bytes,
+                    "note": "working set L2-resident: latency-bound (grid barriers, dependent L2 "
+                            "round trips); the HBM fraction is shown for scale only"}
+    else:
+        # dominant kernel K2 (fused residual update): CUDA events around each launch
+        s.set_profiling(True)
+        s.steps(args.profile_steps, mirror_refresh=False)
+        pt = s.last_timing()
+        kt = s.kernel_times()
+        if sharded:
+            coll = {k: round(v, 5) for k, v in s.collective_times().items()}
+        s.set_profiling(False)
+        k2_ms = pt["k2_ms"] / max(pt["k2_launches"], 1)
+        kb = k2_bytes(cfg, world)
+        achieved = kb / (k2_ms / 1000.0) / 1e9
+        traffic, tsrc = None, None
+        tf = os.path.join(ROOT, "profiles", f"k2_traffic_config{cfg_id}.json")
+        if os.path.exists(tf) and world == 1:
+            try:
+                tj = json.load(open(tf))
+                traffic, tsrc = tj.get("dram_bytes_per_launch"), tj.get("source")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "traffic_source": tsrc or ("not measured for this shard" if world > 1 else None),
+                    "kernel": "k_r_tma<true> (fused R update + row norms, TMA ring) timed together with "
+                              "k_sel_greedy (next-row greedy select across the SMs)",
+                    "algorithmic_bytes_per_launch": kb, "k2_ms": round(k2_ms, 5),
+                    "peak_kind": peak_kind,
+                    "k2_share_of_step": round(k2_ms / per_iter_ms, 4),
+                    "in_pipeline_ms": {"k_yg": round(kt["yg_ms"], 5), "k_zx": round(kt["zx_ms"], 5),
+                                       "k_r_tma": round(kt["k2_ms"], 5)}}
+    roofline["iteration_bytes"] = it_bytes
+    roofline["iteration_achieved_gbs"] = round(it_bytes / (per_iter_ms / 1000) / 1e9, 1)
     del s
     torch.cuda.empty_cache()
 
@@ -741,25 +729,25 @@ def main():
         # device-timed value has its W warm-up steps: the first create of a given
         # size in a process pays the driver's first mapping of its ~41 GB (config 5:
         # 0.9-1.2 s instead of ~0.5 s, tools/e2e_breakdown.py)
-        w = make_solver(host["A"], host["B"], host["C"], host["X0"], host["Xs"], budget=args.steps)
-        w.steps(args.warmup, mirror_refresh=True)
+        w = make_solver(host["A"], host["B"], host["C"], host["X0"], host["Xs"], budget=steps)
+        w.steps(warmup, mirror_refresh=True)
         w.X()
         del w
-        barrier()
+        ctx.barrier()
         t0 = time.perf_counter()
         # the user's budget is the K iterations it asks for (max_iter = K): the
         # solver then caches G = A·Aᵀ only if K iterations repay forming it
-        s2 = make_solver(host["A"], host["B"], host["C"], host["X0"], host["Xs"], budget=args.steps)
-        gram = bool(s2.gram_cached()) if hasattr(s2, "gram_cached") else None
-        s2.steps(args.steps, mirror_refresh=True)
+        s2 = make_solver(host["A"], host["B"], host["C"], host["X0"], host["Xs"], budget=steps)
+        gram_e2e = bool(s2.gram_cached())
+        s2.steps(steps, mirror_refresh=True)
         Xout = s2.X()
         torch.cuda.synchronize(local)
-        e2e_s = allmax(time.perf_counter() - t0)
-        d2h = Xout.nbytes + 8 * args.steps
-        e2e = {"value": args.steps / e2e_s, "unit": "iter/s",
-               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+        e2e_s = ctx.allmax(time.perf_counter() - t0)
+        d2h = Xout.nbytes + 8 * steps
+        e2e = {"value": steps / e2e_s, "unit": "iter/s",
+               "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
                "seconds": round(e2e_s, 4),
-               "gram_cached": gram,
+               "gram_cached": gram_e2e,
                "what": "Solver(host A,B,C,X0,X*, max_iter=K) -> steps(K) -> X() through the "
                        "C-ABI; includes H2D of the system, device ||B||_2, R0 (DMMA), G=A.A^T "
                        "when K repays forming it (else g=A.A_i^T per step), D2H of X; after one "
@@ -769,50 +757,168 @@ def main():
 
     # time-to-tolerance on config 1 (the reference's CPU-runnable case)
     ttt = None
-    if rank == 0 and world == 1 and not args.no_tol:
-        c1 = CONFIGS[1]
-        A1, B1, C1, _, X1 = make_inputs_device(c1, 7, local, 1, 0, blocks=4)
-        s1 = axb.Solver(A1, B1, C1, None, solver_config(axb, X1, 10 ** 6), axb.Options(device=local))
-        s1.cfg.max_iter = 10 ** 6
-        t0 = time.perf_counter()
-        rep = s1.run()
-        ttt = {"config": "config1 (A 500x100, B 80x400, GRBK, ||X-X*||/||X*|| < 1e-6)",
-               "iterations": rep.iterations, "seconds": round(rep.wall_seconds, 4),
-               "device_loop_ms": round(s1.last_timing()["loop_ms"], 3),
-               "final_rel_error": math.sqrt(rep.final_rrn),
-               "terminated_by": rep.terminated_by.name}
-        del s1
+    if rank == 0 and with_tol:
+        ttt = time_to_tol(axb, local)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
+    if rank == 0 and with_cpu:
+        cpu = cpu_baseline(cfg, cpu_budget_s)
+    line = {
+        "metric": "kaczmarz_iterations_per_sec", "value": round(value, 2), "unit": "iter/s",
+        "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": round(ms / steps, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": ("synthetic (numpy seeded SVD-built A, B; N(0,1) X*)" if cfg.get("kind") == "svd"
+                 else "synthetic (seeded torch N(0,1) on device)"),
+        "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
+                   "n": cfg["n"], "method": meth, "refresh_interval": 1000,
+                   "gram_cached": gram,
+                   "parallelism": (f"row-sharded over {world} GPUs (NCCL)" if sharded
+                                   else "single GPU"),
+                   "l2": ("R is 8*m*n bytes > 126 MB L2: inputs larger than L2, no flush"
+                          if 8 * cfg["m"] * cfg["n"] / world > 126e6 else
+                          "working set L2-resident by design (one persistent kernel per batch; "
+                          "each iteration's writes are the next one's inputs): no flush")},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": ck,
+        "setup_s": round(setup_s, 3),
+    }
+    if ttt is not None:
+        line["time_to_tol"] = ttt
+    if coll is not None:
+        line["collectives_ms_per_iteration"] = coll
+    return line
 
+
+def time_to_tol(axb, local):
+    """Config 1 run() to ‖X−X*‖/‖X*‖ < 1e-6 (squared RRN 1e-12)."""
+    c1 = CONFIGS[1]
+    A1, B1, C1, _, X1 = make_inputs_device(c1, 7, local, 1, 0, blocks=4)
+    s1 = axb.Solver(A1, B1, C1, None, solver_config(axb, X1, 10 ** 6), axb.Options(device=local))
+    rep = s1.run()
+    out = {"config": "config1 (A 500x100, B 80x400, GRBK, ||X-X*||/||X*|| < 1e-6)",
+           "iterations": rep.iterations, "seconds": round(rep.wall_seconds, 4),
+           "device_loop_ms": round(s1.last_timing()["loop_ms"], 3),
+           "final_rel_error": math.sqrt(rep.final_rrn),
+           "terminated_by": rep.terminated_by.name}
+    del s1
+    return out
+
+
+def self_launch(args):
+    """--gpus N without a torchrun environment: re-run this command as N ranks."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible; refusing to "
+            f"measure fewer GPUs than asked")
+        sys.exit(2)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    log("[bench] " + " ".join(cmd))
+    sys.exit(subprocess.call(cmd))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tol", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="N=1 config 5: skip configs 1-4")
+    ap.add_argument("--profile-steps", type=int, default=50)
+    ap.add_argument("--ref-threads", type=int, default=0,
+                    help="reference arm solver threads (0: every host thread this process may use)")
+    ap.add_argument("--ref-budget-s", type=float, default=60.0)
+    ap.add_argument("--shard", action="store_true",
+                    help="use the row-sharded path even on one GPU (1-rank NCCL communicator)")
+    ap.add_argument("--watchdog-s", type=float, default=1500.0)
+    ap.add_argument("--half-band", type=int, default=None,
+                    help="config 4: blur half-band (default 7; BASELINE's 'bandwidth 15' read "
+                         "as half-band 7, half-band 15 the other reading, SURVEY §8 D4)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = dict(CONFIGS[args.config])
+    if args.half_band is not None and "half_band" in cfg:
+        cfg["desc"] = cfg["desc"].replace(f"half-band {cfg['half_band']}", f"half-band {args.half_band}")
+        cfg["half_band"] = args.half_band
+
+    in_torchrun = "WORLD_SIZE" in os.environ
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, cfg)
+        return
+    if not in_torchrun and args.gpus > 1:
+        self_launch(args)
+    if in_torchrun and world != args.gpus:
+        log(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        sys.exit(2)
+
+    import faulthandler
+
+    faulthandler.dump_traceback_later(args.watchdog_s, exit=True)  # never hang the box
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    ctx = Ctx(rank, world, local)
+
+    if "channels" in cfg:
+        line = channels_arm(args, cfg, ctx, args.steps, args.warmup,
+                            with_cpu=not args.no_cpu_baseline)
+    else:
+        sharded = world > 1 or args.shard
+        comm = 0
+        if sharded:
+            from paper_2408_05444_b200 import shard
+
+            with stdout_to_stderr():
+                if world == 1:
+                    comm = shard.nccl_comm_create(1, shard.nccl_unique_id(), 0, local)
+                else:
+                    comm, _, _ = shard.init_comm(local)
+        line = system_arm(args, cfg, args.config, ctx, args.steps, args.warmup, sharded, comm,
+                          with_cpu=not args.no_cpu_baseline, with_tol=not args.no_tol)
+        if sharded:
+            shard.nccl_comm_destroy(comm)
+    # the other BASELINE configs in the same process (N=1 default run): D1-D4
+    if world == 1 and args.config == 5 and not args.no_sub and not args.shard:
+        subs = {}
+        for c in (1, 2, 3, 4):
+            sc = dict(CONFIGS[c])
+            k = SUB_STEPS[c]
+            if "channels" in sc:
+                subs[str(c)] = channels_arm(args, sc, ctx, k, args.warmup,
+                                            with_cpu=not args.no_cpu_baseline, cpu_budget_s=10.0)
+            else:
+                subs[str(c)] = system_arm(args, sc, c, ctx, k, args.warmup,
+                                          with_cpu=not args.no_cpu_baseline, cpu_budget_s=10.0,
+                                          with_tol=(c == 1 and not args.no_tol))
+            torch.cuda.empty_cache()
+        line["configs"] = subs
     if rank == 0:
-        line = {
-            "metric": "kaczmarz_iterations_per_sec", "value": round(value, 2), "unit": "iter/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded torch N(0,1) on device)",
-            "config": {"workload": cfg["desc"], "m": cfg["m"], "p": cfg["p"], "q": cfg["q"],
-                       "n": cfg["n"], "method": meth, "refresh_interval": 1000,
-                       "parallelism": (f"row-sharded over {world} GPUs (NCCL)" if sharded
-                                       else "single GPU"),
-                       "l2": ("R is 8*m*n bytes > 126 MB L2: inputs larger than L2, no flush"
-                              if 8 * cfg["m"] * cfg["n"] > 126e6 else
-                              "working set L2-resident by design (one persistent kernel per batch; "
-                              "each iteration's writes are the next one's inputs): no flush")},
-            "roofline": roofline,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": ck,
-            "time_to_tol": ttt,
-            "setup_s": round(setup_s, 3),
-        }
         print(json.dumps(line), flush=True)
-    if sharded:
-        shard.nccl_comm_destroy(comm)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

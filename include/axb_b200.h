@@ -99,7 +99,8 @@ typedef struct {
                                   0 form g = A·A_iᵀ per step, 1 cache G = A·Aᵀ */
     int32_t spectral_on_device;/* -1 auto, 0 host (bitwise reference α), 1 device */
     int32_t graph_iters;       /* iterations captured per CUDA graph (0 = default) */
-    int32_t tie_guard;         /* 1 (default): exact sequential re-check of near-boundary draws */
+    int32_t tie_guard;         /* 1 (default): exact sequential re-check of near-boundary draws;
+                                  0 off; 2 every greedy draw takes the sequential walk (test hook) */
     uint64_t spectral_max_iter;/* power-iteration cap (0 = reference default 5000) */
     double alpha_override;     /* >0: use this α verbatim (e.g. the oracle's), skip ‖B‖₂ */
     /* row sharding (§8(e)): this handle owns rows [row_offset, row_offset+m) of an
@@ -253,6 +254,11 @@ int axb_solver_debug_state(axb_solver* s, uint64_t out[8]);
 /* Average per-launch device times (ms) of K4 (y), K4b+K5 (z, X) and K2 over the
  * last profiled steps()/run(), CUDA events between consecutive launches. */
 int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]);
+/* Row-sharded solvers: average per-iteration device times (ms) of the exchange
+ * steps over the last profiled steps()/run(): [0] y allreduce, [1] z allgather,
+ * [2] the grouped ‖R_l‖²-slice + record allgather, [3] the global selection
+ * kernels (k_sel1 + k_pack), [4] the selected-row allreduce.  Zeros on one GPU. */
+int axb_solver_collective_times(const axb_solver* s, double out_ms[5]);
 /* Enable per-kernel CUDA-event timing of K2 inside steps()/run() (adds events to
  * the captured graph; off by default). */
 int axb_solver_set_profiling(axb_solver* s, int32_t on);

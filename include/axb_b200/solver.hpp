@@ -28,6 +28,10 @@
 #include <axb/errors.hpp>
 #define AXB_B200_REFERENCE_ERRORS 1
 #endif
+#if __has_include(<axb/solver.hpp>) && !defined(AXB_B200_NO_REFERENCE_TYPES)
+#include <axb/solver.hpp>
+#define AXB_B200_REFERENCE_TYPES 1
+#endif
 #endif
 
 namespace axb_b200 {
@@ -41,6 +45,7 @@ using ConfigError = axb::ConfigError;
 using ConvergenceError = axb::ConvergenceError;
 using DivergenceError = axb::DivergenceError;
 using InvariantError = axb::InvariantError;
+using DecompositionError = axb::DecompositionError;
 #else
 // errors.hpp:10-72, restated
 struct Error : std::runtime_error {
@@ -63,6 +68,7 @@ struct DivergenceError : Error {
     double residual_norm;
 };
 struct InvariantError : Error { using Error::Error; };
+struct DecompositionError : Error { using Error::Error; };
 #endif
 /// Device/runtime failure (no reference analogue): no sm_100 device, CUDA error.
 struct CudaError : Error {
@@ -79,6 +85,7 @@ struct CudaError : Error {
         case AXB_INVARIANT_ERROR: throw InvariantError(msg);
         case AXB_CONVERGENCE_ERROR: throw ConvergenceError(msg, val);
         case AXB_CAPACITY_ERROR: throw CapacityError(msg);
+        case AXB_DECOMPOSITION_ERROR: throw DecompositionError(msg);
         default: throw CudaError(msg);
     }
 }
@@ -182,33 +189,40 @@ public:
            const Options& opt = Options())
         : cfg_(std::move(cfg)), m_(m), p_(p), q_(q), n_(n) {
         cfg_.method.validate();
-        axb_config c{};
-        c.method = static_cast<int32_t>(cfg_.method.tag);
-        c.has_theta = cfg_.method.theta ? 1 : 0;
-        c.theta = cfg_.method.theta.value_or(0.0);
-        c.alpha_rule = static_cast<int32_t>(cfg_.alpha_rule);
-        c.stop_kind = static_cast<int32_t>(cfg_.stop.kind);
-        c.alpha_value = cfg_.alpha_value;
-        c.tol = cfg_.stop.tol;
-        c.reference = cfg_.stop.reference.empty() ? nullptr : cfg_.stop.reference.data();
-        c.max_iter = cfg_.max_iter;
-        c.seed = cfg_.seed;
-        c.record_trace = cfg_.record_trace ? 1 : 0;
-        c.refresh_interval = cfg_.refresh_interval;
+        // solver.hpp:182-185, before any buffer is handed to the library
+        if (cfg_.stop.kind == StopRule::Kind::SolutionRrn && !cfg_.stop.reference.empty() &&
+            cfg_.stop.reference.size() != p_ * q_)
+            throw ShapeError("reference solution shape mismatch");
+        const axb_config c = flat(cfg_);
         axb_solver* h = nullptr;
         const int st = axb_solver_create(A, m, p, B, q, n, C, X0, &c, &opt, &h);
         if (st) throw_status(st, axb_last_create_error());
         h_.reset(h);
     }
+    /// Dense operands (any type with rows(), cols() and row-major data(), e.g.
+    /// axb::DenseMatrix).  Shapes are checked BEFORE any buffer is read, as the
+    /// reference's constructor does (solver.hpp:150-154): an undersized C or X0
+    /// throws ShapeError instead of being copied past its end.
     template <class M>
     Solver(const M& A, const M& B, const M& C, const M& X0, SolveConfig cfg,
            const Options& opt = Options())
-        : Solver(A.data().data(), A.rows(), A.cols(), B.data().data(), B.rows(), B.cols(),
-                 C.data().data(), X0.data().data(), std::move(cfg), opt) {
-        if (X0.rows() != p_ || X0.cols() != q_)
-            throw ShapeError("solve: X0 must be " + std::to_string(p_) + "x" + std::to_string(q_));
-        if (C.rows() != m_ || C.cols() != n_)
-            throw ShapeError("solve: C must be " + std::to_string(m_) + "x" + std::to_string(n_));
+        : Solver(checked(A, B, C, X0), A.data().data(), A.rows(), A.cols(), B.data().data(),
+                 B.rows(), B.cols(), C.data().data(), X0.data().data(), std::move(cfg), opt) {}
+
+    /// Storage-agnostic operands (the reference's axb::Matrix variant, matrix.hpp:178):
+    /// dense or CSR descriptors (axb_matrix), C m×n and X0 p×q dense (X0 may be null).
+    Solver(const axb_matrix& A, const axb_matrix& B, const double* C, const double* X0,
+           SolveConfig cfg, const Options& opt = Options())
+        : cfg_(std::move(cfg)), m_(A.rows), p_(A.cols), q_(B.rows), n_(B.cols) {
+        cfg_.method.validate();
+        if (cfg_.stop.kind == StopRule::Kind::SolutionRrn && !cfg_.stop.reference.empty() &&
+            cfg_.stop.reference.size() != p_ * q_)
+            throw ShapeError("reference solution shape mismatch");
+        const axb_config c = flat(cfg_);
+        axb_solver* h = nullptr;
+        const int st = axb_solver_create_ex(&A, &B, C, X0, &c, &opt, &h);
+        if (st) throw_status(st, axb_last_create_error());
+        h_.reset(h);
     }
 
     std::size_t step() {
@@ -300,6 +314,35 @@ public:
     std::vector<double> a_row_sq() { return vec(axb_solver_get_a_sq, m_); }
 
 private:
+    struct Checked {};
+    template <class M>
+    static Checked checked(const M& A, const M& B, const M& C, const M& X0) {
+        const std::size_t m = A.rows(), p = A.cols(), q = B.rows(), n = B.cols();
+        if (X0.rows() != p || X0.cols() != q)
+            throw ShapeError("solve: X0 must be " + std::to_string(p) + "x" + std::to_string(q));
+        if (C.rows() != m || C.cols() != n)
+            throw ShapeError("solve: C must be " + std::to_string(m) + "x" + std::to_string(n));
+        return {};
+    }
+    Solver(Checked, const double* A, std::size_t m, std::size_t p, const double* B, std::size_t q,
+           std::size_t n, const double* C, const double* X0, SolveConfig cfg, const Options& opt)
+        : Solver(A, m, p, B, q, n, C, X0, std::move(cfg), opt) {}
+    static axb_config flat(const SolveConfig& k) {
+        axb_config c{};
+        c.method = static_cast<int32_t>(k.method.tag);
+        c.has_theta = k.method.theta ? 1 : 0;
+        c.theta = k.method.theta.value_or(0.0);
+        c.alpha_rule = static_cast<int32_t>(k.alpha_rule);
+        c.stop_kind = static_cast<int32_t>(k.stop.kind);
+        c.alpha_value = k.alpha_value;
+        c.tol = k.stop.tol;
+        c.reference = k.stop.reference.empty() ? nullptr : k.stop.reference.data();
+        c.max_iter = k.max_iter;
+        c.seed = k.seed;
+        c.record_trace = k.record_trace ? 1 : 0;
+        c.refresh_interval = k.refresh_interval;
+        return c;
+    }
     struct Del {
         void operator()(axb_solver* s) const { axb_solver_destroy(s); }
     };
@@ -342,5 +385,104 @@ SolveReport solve(const M& A, const M& B, const M& C, const M& X0, const SolveCo
                   const Options& opt = Options()) {
     return Solver(A, B, C, X0, cfg, opt).run();
 }
+
+#ifdef AXB_B200_REFERENCE_TYPES
+// ---- the reference's own types in and out (reference headers on the include path) ----
+// A call site switches from   axb::solve(A, B, C, X0, cfg)
+//                        to   axb_b200::solve(A, B, C, X0, cfg)
+// with the same argument types (axb::Matrix or axb::DenseMatrix operands,
+// axb::SolveConfig) and the same result type (axb::SolveReport).
+
+/// axb::SolveConfig (solver.hpp:100-109) → axb_b200::SolveConfig.
+inline SolveConfig to_b200(const axb::SolveConfig& c) {
+    SolveConfig o;
+    o.method.tag = static_cast<MethodTag>(static_cast<int>(c.method.tag));
+    o.method.theta = c.method.theta;
+    o.alpha_rule = static_cast<AlphaRule>(static_cast<int>(c.alpha_rule));
+    o.alpha_value = c.alpha_value;
+    o.stop.kind = c.stop.kind == axb::StopRule::Kind::SolutionRrn ? StopRule::Kind::SolutionRrn
+                                                                  : StopRule::Kind::ResidualRel;
+    o.stop.tol = c.stop.tol;
+    if (c.stop.reference) {
+        if (o.stop.kind == StopRule::Kind::SolutionRrn &&
+            (c.stop.reference->rows() == 0 || c.stop.reference->cols() == 0))
+            throw ConfigError("solution_rrn stopping needs a reference solution");
+        const auto d = c.stop.reference->data();
+        o.stop.reference.assign(d.begin(), d.end());
+    }
+    o.max_iter = c.max_iter;
+    o.seed = c.seed;
+    o.record_trace = c.record_trace;
+    o.refresh_interval = c.refresh_interval;
+    return o;
+}
+
+/// axb_b200::SolveReport → axb::SolveReport (solver.hpp:120-133); X is p×q.
+inline axb::SolveReport to_axb(SolveReport&& r, std::size_t p, std::size_t q) {
+    axb::SolveReport o;
+    o.iterations = r.iterations;
+    o.wall_seconds = r.wall_seconds;
+    o.final_rrn = r.final_rrn;
+    o.final_residual_rel = r.final_residual_rel;
+    o.terminated_by = r.terminated_by == Terminated::Tolerance ? axb::Terminated::Tolerance
+                                                               : axb::Terminated::MaxIter;
+    o.trace.reserve(r.trace.size());
+    for (const auto& t : r.trace) o.trace.push_back({t.k, t.rrn, t.residual_rel, t.selected_row});
+    o.X = axb::DenseMatrix(p, q, std::move(r.X));
+    o.alpha = r.alpha;
+    o.seed = r.seed;
+    o.method_label = std::move(r.method_label);
+    o.alpha_outside_bound = r.alpha_outside_bound;
+    o.skipped_zero_rows = r.skipped_zero_rows;
+    return o;
+}
+
+/// axb::Matrix (matrix.hpp:178: DenseMatrix or CSR SparseMatrix) → a borrowed
+/// axb_matrix descriptor (valid while m lives).
+inline axb_matrix describe(const axb::Matrix& m) {
+    axb_matrix d{};
+    if (const auto* dm = std::get_if<axb::DenseMatrix>(&m)) {
+        d.kind = 0;
+        d.rows = dm->rows();
+        d.cols = dm->cols();
+        d.dense = dm->data().data();
+    } else {
+        const auto& sm = std::get<axb::SparseMatrix>(m);
+        d.kind = 1;
+        d.rows = sm.rows();
+        d.cols = sm.cols();
+        d.nnz = sm.nnz();
+        static_assert(sizeof(std::size_t) == sizeof(std::uint64_t), "CSR index width");
+        d.row_ptr = reinterpret_cast<const std::uint64_t*>(sm.row_ptr().data());
+        d.col_idx = sm.rows() ? reinterpret_cast<const std::uint64_t*>(sm.row_indices(0).data())
+                              : nullptr;
+        d.values = sm.rows() ? sm.row_values(0).data() : nullptr;
+    }
+    return d;
+}
+
+/// Drop-in for axb::solve(const Matrix&, const Matrix&, const DenseMatrix&,
+/// const DenseMatrix&, const SolveConfig&) (solver.hpp:518-526): same arguments,
+/// same axb::SolveReport, the reference's exception types.
+inline axb::SolveReport solve(const axb::Matrix& A, const axb::Matrix& B, const axb::DenseMatrix& C,
+                              const axb::DenseMatrix& X0, const axb::SolveConfig& cfg,
+                              const Options& opt = Options()) {
+    const axb_matrix a = describe(A), b = describe(B);
+    if (X0.rows() != a.cols || X0.cols() != b.rows)
+        throw ShapeError("solve: X0 must be " + std::to_string(a.cols) + "x" + std::to_string(b.rows));
+    if (C.rows() != a.rows || C.cols() != b.cols)
+        throw ShapeError("solve: C must be " + std::to_string(a.rows) + "x" + std::to_string(b.cols));
+    Solver s(a, b, C.data().data(), X0.data().data(), to_b200(cfg), opt);
+    return to_axb(s.run(), a.cols, b.rows);
+}
+
+/// Dense overload (solver.hpp:528-532).
+inline axb::SolveReport solve(const axb::DenseMatrix& A, const axb::DenseMatrix& B,
+                              const axb::DenseMatrix& C, const axb::DenseMatrix& X0,
+                              const axb::SolveConfig& cfg, const Options& opt = Options()) {
+    Solver s(A, B, C, X0, to_b200(cfg), opt);
+    return to_axb(s.run(), A.cols(), B.rows());
+}
+#endif  // AXB_B200_REFERENCE_TYPES
 
 }  // namespace axb_b200

@@ -148,6 +148,7 @@ SIGNATURES = [
     ("axb_solver_dims", C.c_int, [_H, _u64p]),
     ("axb_solver_last_timing", C.c_int, [_H, _dp, _dp, _u64p, _u64p]),
     ("axb_solver_kernel_times", C.c_int, [_H, _dp]),
+    ("axb_solver_collective_times", C.c_int, [_H, _dp]),
     ("axb_solver_debug_state", C.c_int, [_H, _u64p]),
     ("axb_solver_set_profiling", C.c_int, [_H, C.c_int32]),
     ("axb_solvers_run", C.c_int,

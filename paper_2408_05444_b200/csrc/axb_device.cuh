@@ -118,7 +118,7 @@ struct Params {
     double* pack;                // n + p + 2 (allreduced): R_i | A_i | sel | coef
     double* pack_send;           // this rank's contribution (zeros unless owner)
     double* recs;                // world × 4 (allgathered): Σ‖R_l‖², max ratio, argmax, err
-    double* masses;              // world (allgathered): greedy member mass per shard
+    double* r_sq_g;              // m_global ‖R_l‖² (allgathered; r_sq points at this rank's slice)
     const double* a_sq_g;        // m_global ‖A_i‖² (allgathered), for BK/RBK/replay
     long long c0, c1;            // this rank's column slice of B for y and z
     long long x0r, x1r;          // this rank's rows of X
@@ -172,9 +172,9 @@ int sumsq_parts(long long n);
 void launch_sumsq(const double* v, long long n, double* part, cudaStream_t s);
 void launch_row_sq_seq(const double* A, long long m, long long p, double* out, cudaStream_t s);
 void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* total, cudaStream_t s);
-// sharded selection (between the record / mass allgathers and the row allreduce)
-void launch_sel1(const Params& P, cudaStream_t s, bool update);
-void launch_sel2(const Params& P, cudaStream_t s);
+// sharded selection (between the r_sq / record allgather and the row allreduce):
+// mode 0 norms only, 1 iteration (+ select, + k_pack), 2 select only (+ k_pack)
+void launch_sel1(const Params& P, cudaStream_t s, int mode);
 // persistent cooperative batch kernel for small systems; returns a cudaError_t
 int launch_persist(const Params& P, cudaStream_t s);
 // many independent small systems, one CTA each (dPs: device array of Params)

@@ -729,7 +729,16 @@ __device__ long long grbk_search(const Member& mem, long long m, const double* g
 }
 
 __device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const double* gs,
-                         long long* out_row, SelShared& sh);
+                         long long m, long long row0, long long* out_row, SelShared& sh);
+
+// Distance from a member-mass boundary inside which the tree-ordered search may
+// round differently from the reference's sequential prefix: the draw then takes
+// the exact sequential walk.  tie_guard 0 = off, 1 = on (default), 2 = every
+// draw takes the walk (a test hook that exercises the near-tie path on every step).
+__device__ __forceinline__ double tie_slack(const Params& P, long long m, double total) {
+    if (P.tie_guard == 2) return INFINITY;
+    return P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
+}
 
 __device__ int select_rows(const Params& P, DevState* st, int method, double theta,
                            long long* out_row, SelShared& sh, double* scratch,
@@ -811,7 +820,7 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
 #ifdef AXB_TRACE_PERSIST
     if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh.t_groups));
 #endif
-    return grbk_pick(P, st, mem, gs, out_row, sh);
+    return grbk_pick(P, st, mem, gs, P.m, P.row0, out_row, sh);
 }
 
 // The greedy draw once the group sums gs are in place: ordered prefix, one
@@ -823,9 +832,8 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
 // of the group sums; the tie guard covers the rounding difference exactly as
 // it does between those and the reference's sequential walk.
 __device__ long long grbk_pick_warp(const Params& P, DevState* st, const Member& mem,
-                                    const double* gs, long long ng, SelShared& sh) {
+                                    const double* gs, long long m, long long ng, SelShared& sh) {
     const int tid = threadIdx.x, lane = tid & 31;
-    const long long m = P.m;
     if (tid < 32) {
         const long long gseg = (ng + 31) / 32;
         const long long g0 = min(ng, (long long)lane * gseg), g1 = min(ng, g0 + gseg);
@@ -849,7 +857,7 @@ __device__ long long grbk_pick_warp(const Params& P, DevState* st, const Member&
             if (lane == 0) u = rng_unit(st->rng);
             u = __shfl_sync(0xffffffffu, u, 0);
             const double target = __dmul_rn(u, total);
-            const double slack = P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
+            const double slack = tie_slack(P, m, total);
             long long my_g = -1;
             double my_before = 0.0, cum = excl;
             for (long long g = g0; g < g1; ++g) {
@@ -903,15 +911,16 @@ __device__ long long grbk_pick_warp(const Params& P, DevState* st, const Member&
     return r;
 }
 
+// m rows of mem / gs; the picked row is row0 + its index (K2's shard offset on
+// one GPU, 0 for the sharded path's global arrays)
 __device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const double* gs,
-                         long long* out_row, SelShared& sh) {
+                         long long m, long long row0, long long* out_row, SelShared& sh) {
     const int tid = threadIdx.x;
-    const long long m = P.m;
     const long long ng = (m + 31) / 32;
     if (tid == 0) AXB_STAMP(1);
     long long pick;
     if (ng <= 1024) {
-        pick = grbk_pick_warp(P, st, mem, gs, ng, sh);
+        pick = grbk_pick_warp(P, st, mem, gs, m, ng, sh);
         if (tid == 0) AXB_STAMP(2);
         if (pick == -2) return 2;
     } else {
@@ -925,7 +934,7 @@ __device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const
             sh.target = __dmul_rn(sh.u, total);
         }
         __syncthreads();
-        const double slack = P.tie_guard ? 8.0 * (double)m * DBL_EPSILON * total : -1.0;
+        const double slack = tie_slack(P, m, total);
         pick = grbk_search(mem, m, gs, g0, g1, excl, sh.target, slack, sh);
     }
     if (tid == 0) {
@@ -965,7 +974,7 @@ __device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const
         pick = sh.cand;
     }
     if (tid == 0) AXB_STAMP(4);
-    *out_row = P.row0 + pick;
+    *out_row = row0 + pick;
     return 0;
 }
 
@@ -1444,8 +1453,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
         // per thread (deep memory-level parallelism for the serial tail)
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const long long T = blockDim.x;
-        const long long h = m >> 1;
-        const double2* r2 = reinterpret_cast<const double2*>(P.r_sq);
+        // a shard's slice of the global r_sq starts at row0, which may be odd:
+        // the first row then goes scalar and the rest in aligned pairs
+        const int off = (reinterpret_cast<uintptr_t>(P.r_sq) & 15) ? 1 : 0;
+        const long long h = (m - off) >> 1;
+        const double2* r2 = reinterpret_cast<const double2*>(P.r_sq + off);
+        if (off && tid == 0) acc[1] += __ldcg(P.r_sq);
         long long k = tid;
         for (; k + 3 * T < h; k += 4 * T) {
 #pragma unroll
@@ -1460,7 +1473,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
             acc[0] += v.x;
             acc[1] += v.y;
         }
-        if ((m & 1) && tid == 0) acc[0] += __ldcg(P.r_sq + m - 1);
+        if (((m - off) & 1) && tid == 0) acc[0] += __ldcg(P.r_sq + m - 1);
         sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     }
     for (int k = tid; k < (int)gridDim.x; k += blockDim.x) {
@@ -1482,142 +1495,152 @@ size_t tma_smem_bytes(const Params& P) {
 }
 
 // ------------------------------------------------------------------------
-// Sharded selection, part 1 (after the record allgather): global ‖R‖², max
-// ratio / argmax and ‖X−X_ref‖² in rank order (identical on every rank), the
-// stop / divergence logic, and for GRBK this shard's member mass (group sums
-// over the local rows, kept in P.gsum for part 2).  The O(m_local) membership
-// pass is spread over sel1_grid CTAs, each combining the (world-sized) records
-// itself; the last CTA to finish commits the state and takes the ordered prefix
-// — the same group sums and prefix as one CTA would form (a group's sum does not
-// depend on which CTA forms it).  One CTA had taken 14 µs per iteration at the
-// world-8 shard of config 5 (m_local = 8192) and ~100 µs at m_local = 65536.
-__global__ void __launch_bounds__(kThreads) k_sel1(Params P, int update) {
+// Sharded selection (after ONE grouped allgather of every shard's ‖R_l‖² slice
+// into the global r_sq_g and of the per-shard records).  Every rank then holds
+// the global ‖R_l‖² and ‖A_l‖², so every rank runs the single-GPU selection over
+// the GLOBAL rows — membership, ordered member-mass prefix, one xoshiro draw, the
+// two-level search, the tie guard and the reference's sequential walk as the
+// exact fallback (solver.hpp:241-254, rng.hpp:84-99) — on identical inputs with
+// an identical RNG state, and all ranks agree on the row bit for bit with no
+// further exchange.  (The first version exchanged per-shard member masses and let
+// the owner search alone; it could not replay the reference's sequential walk
+// on a near-tie because no rank saw all rows.)
+//
+//   mode 0  norms pass: commit ‖R‖², max ratio / argmax, ‖X−X_ref‖², no selection
+//   mode 1  iteration: commit, trace, stop / divergence logic, select the next row
+//   mode 2  select only, from the committed state (ensure_selection)
+//
+// The O(m_global) membership pass is spread over sel1_grid CTAs (a group's sum does
+// not depend on which CTA forms it); the last CTA to arrive commits and selects.
+__global__ void __launch_bounds__(kThreads) k_sel1(Params P, int mode) {
     __shared__ SelShared sh;
     __shared__ bool last;
+    __shared__ long long s_sel;
+    __shared__ int s_err;
     pdl_wait();
     DevState* st = P.st;
-    if (update && halted(st)) return;
+    if (mode == 1 && halted(st)) return;
     const int tid = threadIdx.x;
-    const int mode = update ? st->fin_mode : FIN_NORMS;
+    const int fmode = mode == 1 ? st->fin_mode : FIN_NORMS;
+    const long long mg = P.m_global;
     double s = 0.0, err = 0.0, mx = -INFINITY;
     long long ax = LLONG_MAX;
-    for (int r = 0; r < P.world; ++r) {
-        const double* rec = P.recs + 4 * r;
-        s += rec[0];
-        maxidx_merge(mx, ax, rec[1], (long long)rec[2]);
-        err += rec[3];
+    if (mode == 2) {
+        s = st->r_fro_sq;
+        mx = st->max_ratio;
+        ax = st->argmax;
+    } else {
+        for (int r = 0; r < P.world; ++r) {
+            const double* rec = P.recs + 4 * r;
+            s += rec[0];
+            maxidx_merge(mx, ax, rec[1], (long long)rec[2]);
+            err += rec[3];
+        }
     }
-    const bool diverged = mode != FIN_NORMS && !isfinite(s);  // solver.hpp:306-307
-    const bool masses = (P.method == 2 || P.method == 3) && !st->replay && s > 0.0 &&
-                        !diverged && st->status != ST_ERROR;
-    const long long ng = (P.m + 31) / 32;
+    const bool diverged = fmode != FIN_NORMS && !isfinite(s);  // solver.hpp:306-307
+    const bool greedy = P.method == 2 || P.method == 3;
+    const bool masses = mode != 0 && greedy && !st->replay && s > 0.0 && !diverged &&
+                        st->status != ST_ERROR;
+    Member mem;
+    mem.a_sq = P.a_sq_g;
+    mem.r_sq = P.r_sq_g;
+    mem.smem = 0;
+    mem.row0 = 0;
+    mem.argmax = ax;
+    mem.r_fro = s;
+    mem.zeta = __dadd_rn(__dmul_rn(P.theta, __ddiv_rn(mx, s)),
+                         __ddiv_rn(__dsub_rn(1.0, P.theta), P.a_fro_sq));  // as make_member
     if (masses) {
-        Member mem;
-        mem.a_sq = P.a_sq;
-        mem.r_sq = P.r_sq;
-        mem.smem = 0;
-        mem.row0 = P.row0;
-        mem.argmax = ax;
-        mem.r_fro = s;
-        mem.zeta = __dadd_rn(__dmul_rn(P.theta, __ddiv_rn(mx, s)),
-                             __ddiv_rn(__dsub_rn(1.0, P.theta), P.a_fro_sq));  // as make_member
+        const long long ng = (mg + 31) / 32;
         const long long per = (ng + gridDim.x - 1) / gridDim.x;
         const long long gb = (long long)blockIdx.x * per;
-        grbk_group_sums(mem, P.m, P.gsum, min(ng, gb), min(ng, gb + per));
+        grbk_group_sums(mem, mg, P.gsum, min(ng, gb), min(ng, gb + per));
     }
     __threadfence();  // this CTA's group sums before its arrival
     __syncthreads();
-    if (tid == 0) {
-        last = gridDim.x == 1 || atomicAdd(&st->cnt_sel1, 1u) == gridDim.x - 1;
-    }
+    if (tid == 0) last = gridDim.x == 1 || atomicAdd(&st->cnt_sel1, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
     if (tid == 0) {
         st->cnt_sel1 = 0u;
-        st->err_sq = err;
-        st->r_fro_sq = s;
-        st->max_ratio = mx;
-        st->argmax = ax;
-        st->sel_valid = 0;
-        const double cf = P.c_fro > 0.0 ? P.c_fro : 1.0;
-        const double rel = sqrt(s > 0.0 ? s : 0.0) / cf;
-        if (diverged) {
-            st->status = ST_ERROR;
-            st->err_code = 4;
-            st->err_k = st->k;
-            st->err_val = sqrt(fabs(s));
-        } else if (mode == FIN_ITERATION) {
-            const unsigned long long k = st->k;
-            const double metric = P.stop_kind == 0 ? err / P.ref_sq : rel;
-            const unsigned long long slot = k - st->k0;
-            if (slot < P.trace_cap) {
-                P.trace_row[slot] = (long long)P.pack[P.n + P.p];
-                P.trace_metric[slot] = metric;
-                P.trace_rel[slot] = rel;
+        if (mode != 2) {
+            st->err_sq = err;
+            st->r_fro_sq = s;
+            st->max_ratio = mx;
+            st->argmax = ax;
+            st->sel_valid = 0;
+            const double cf = P.c_fro > 0.0 ? P.c_fro : 1.0;
+            const double rel = sqrt(s > 0.0 ? s : 0.0) / cf;
+            if (diverged) {
+                st->status = ST_ERROR;
+                st->err_code = 4;
+                st->err_k = st->k;
+                st->err_val = sqrt(fabs(s));
+            } else if (mode == 1 && fmode == FIN_ITERATION) {
+                const unsigned long long k = st->k;
+                const double metric = P.stop_kind == 0 ? err / P.ref_sq : rel;
+                const unsigned long long slot = k - st->k0;
+                if (slot < P.trace_cap) {
+                    P.trace_row[slot] = (long long)P.pack[P.n + P.p];
+                    P.trace_metric[slot] = metric;
+                    P.trace_rel[slot] = rel;
+                }
+                st->k = k + 1;
+                st->metric = metric;
+                if (st->run_mode && metric <= P.tol) st->status = ST_PAUSE;
+                else if (st->run_mode && !(s > 0.0)) st->status = ST_ZERO;
+            } else {
+                st->metric = P.stop_kind == 0 ? err / P.ref_sq : rel;
             }
-            st->k = k + 1;
-            st->metric = metric;
-            if (st->run_mode && metric <= P.tol) st->status = ST_PAUSE;
-            else if (st->run_mode && !(s > 0.0)) st->status = ST_ZERO;
-        } else {
-            st->metric = P.stop_kind == 0 ? err / P.ref_sq : rel;
         }
     }
-    if (masses) {
-        long long g0, g1;
-        double excl;
-        const double tot = grbk_prefix(P.gsum, ng, sh, g0, g1, excl);
-        if (tid == 0) P.masses[P.rank] = tot;
-    }
-}
-
-// Sharded selection, part 2 (after the mass allgather): every rank draws the
-// same uniform from its identical xoshiro state, finds the owning shard and
-// the row; the owner packs R_i | A_i | i | coef into pack_send (everyone else
-// contributes zeros), and the allreduce that follows hands the row to all.
-__global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
-    __shared__ SelShared sh;
-    __shared__ long long s_sel;
-    __shared__ int s_owner;
-    pdl_wait();
-    DevState* st = P.st;
-    const int tid = threadIdx.x;
-    const long long mg = P.m_global;
-    if (st->status != ST_RUN || st->k >= st->k_limit) return;
+    __syncthreads();
+    if (mode == 0) return;
+    if (st->status != ST_RUN || st->k >= st->k_limit) return;  // nothing to select
+    // ---- the selection, identical on every rank ----
+    sel_snapshot(st, sh);  // rollback point (an unused pre-selection is undone)
     if (tid == 0) {
-        for (int k = 0; k < 4; ++k) st->rng_snap[k] = st->rng[k];
-        st->cyclic_snap = st->cyclic_pos;
-        st->skipped_snap = st->skipped_zero_rows;
         s_sel = -1;
-        s_owner = -1;
-        sh.err = 0;
+        s_err = 0;
+    }
+    __syncthreads();
+    if (greedy && !st->replay) {
+        long long row = -1;
+        int e = 2;  // "greedy threshold: zero residual" (solver.hpp:213-214)
+        if (s > 0.0) e = grbk_pick(P, st, mem, P.gsum, mg, 0, &row, sh);
+        if (tid == 0) {
+            s_sel = row;
+            s_err = e;
+        }
+    } else if (tid == 0) {
         const int method = P.method;
         if (st->replay) {
             const long long row = P.forced_rows[st->k - st->k0];
-            if (row < 0 || row >= mg || !(P.a_sq_g[row] > 0.0)) sh.err = 2;
+            if (row < 0 || row >= mg || !(P.a_sq_g[row] > 0.0)) s_err = 2;
             else s_sel = row;
             if (method == 1 || method == 2 || method == 3) (void)rng_next(st->rng);
-            if (method == 0 && !sh.err) st->cyclic_pos = (unsigned long long)((row + 1) % mg);
-        } else if (method == 4) {  // MWRBK
-            s_sel = st->argmax;
-        } else if (method == 0) {  // BK over the global rows
-            sh.err = 2;
+            if (method == 0 && !s_err) st->cyclic_pos = (unsigned long long)((row + 1) % mg);
+        } else if (method == 4) {  // MWRBK: smallest global argmax (solver.hpp:258)
+            if (st->argmax == LLONG_MAX) s_err = 2;
+            else s_sel = st->argmax;
+        } else if (method == 0) {  // BK over the global rows (solver.hpp:197-206)
+            s_err = 2;
             for (long long tries = 0; tries < mg; ++tries) {
                 const long long i = (long long)st->cyclic_pos;
                 st->cyclic_pos = (st->cyclic_pos + 1) % (unsigned long long)mg;
                 if (P.a_sq_g[i] > 0.0) {
                     s_sel = i;
-                    sh.err = 0;
+                    s_err = 0;
                     break;
                 }
                 ++st->skipped_zero_rows;
             }
-        } else if (method == 1) {  // RBK on the global CDF
+        } else {  // RBK on the global CDF (solver.hpp:209, rng.hpp:84-99)
             const double* cum = P.rbk_cum;
             const double total = cum[mg - 1];
             if (!(total > 0.0)) {
-                sh.err = 2;
+                s_err = 2;
             } else {
                 const double target = __dmul_rn(rng_unit(st->rng), total);
                 long long lo = 0, hi = mg - 1;
@@ -1629,79 +1652,23 @@ __global__ void __launch_bounds__(kThreads) k_sel2(Params P) {
                 while (lo > 0 && cum[lo] == cum[lo - 1]) --lo;
                 s_sel = lo;
             }
-        } else {  // GRBK / RGRBK: shard masses in rank order, then the owner searches
-            if (!(st->r_fro_sq > 0.0)) {
-                sh.err = 2;
-            } else {
-                double total = 0.0;
-                for (int r = 0; r < P.world; ++r) total = __dadd_rn(total, P.masses[r]);
-                if (!(total > 0.0)) {
-                    sh.err = 2;
-                } else {
-                    sh.u = rng_unit(st->rng);
-                    sh.target = __dmul_rn(sh.u, total);
-                    double before = 0.0;
-                    int owner = -1, last_pos = -1;
-                    for (int r = 0; r < P.world; ++r) {
-                        if (P.masses[r] > 0.0) last_pos = r;
-                        const double nc = __dadd_rn(before, P.masses[r]);
-                        if (owner < 0 && nc > sh.target) owner = r;
-                        if (owner < 0) before = nc;
-                    }
-                    if (owner < 0) {  // target rounded past the last cum: last positive shard
-                        owner = last_pos;
-                        before = 0.0;
-                        for (int r = 0; r < owner; ++r) before = __dadd_rn(before, P.masses[r]);
-                        sh.target = __dadd_rn(before, 0.5 * P.masses[owner]);
-                    }
-                    s_owner = owner;
-                    sh.redv[1] = before;  // mass of the shards before the owner
-                }
-            }
         }
     }
     __syncthreads();
-    if (sh.err) {
-        if (tid == 0) {
-            st->status = ST_ERROR;
-            st->err_code = sh.err;
-            st->err_k = st->k;
-        }
-        return;
-    }
-    const long long mloc = P.m;
-    if ((P.method == 2 || P.method == 3) && !st->replay) {
-        if (s_owner == P.rank) {
-            const Member mem = make_member(P, st, P.theta);
-            long long g0, g1;
-            double excl;
-            (void)grbk_prefix(P.gsum, (mloc + 31) / 32, sh, g0, g1, excl);
-            const double base = sh.redv[1];
-            long long local = grbk_search(mem, mloc, P.gsum, g0, g1, __dadd_rn(base, excl),
-                                          sh.target, -1.0, sh);
-            if (local < 0) {  // rounding disagreement: last member of the shard with mass
-                if (tid == 0) {
-                    local = 0;
-                    for (long long r = 0; r < mloc; ++r)
-                        if (mem(r) > 0.0) local = r;
-                    sh.cand = local;
-                }
-                __syncthreads();
-                local = sh.cand;
-            }
-            if (tid == 0) s_sel = P.row0 + local;
-        }
-    } else if (tid == 0) {
-        s_owner = (int)(s_sel / mloc);  // equal shards
-    }
-    __syncthreads();
-    // the pack itself is k_pack's (many CTAs): the owner copies its row, the
-    // previous owner clears its stale one
     if (tid == 0) {
-        st->sel = s_sel;  // −1 on non-owners for GRBK; the pack carries the row
-        st->sel_valid = 1;
-        st->pack_prev = st->packed;
-        st->packed = s_owner == P.rank ? 1 : 0;
+        if (s_err) {
+            st->status = ST_ERROR;
+            st->err_code = s_err;
+            st->err_k = st->k;
+            st->sel_valid = 0;
+        } else {
+            // the pack itself is k_pack's (many CTAs): the owner copies its row,
+            // the previous owner clears its stale one
+            st->sel = s_sel;
+            st->sel_valid = 1;
+            st->pack_prev = st->packed;
+            st->packed = (s_sel / P.m) == P.rank ? 1 : 0;  // equal contiguous shards
+        }
     }
 }
 
@@ -1780,7 +1747,7 @@ __global__ void __launch_bounds__(kThreads) k_sel_greedy(Params P) {
     int err = 2;  // "greedy threshold: zero residual"
     if (live) {
         const Member mem = make_member(P, st, P.theta);
-        err = grbk_pick(P, st, mem, P.gsum, &row, sh);
+        err = grbk_pick(P, st, mem, P.gsum, P.m, P.row0, &row, sh);
     }
     __syncthreads();
     sel_commit(P, st, err, row);
@@ -3029,14 +2996,11 @@ void launch_cumsum_seq(const double* a_sq, long long m, double* cum, double* tot
     k_cumsum_seq<<<1, 1, 0, s>>>(a_sq, m, cum, total);
 }
 
-void launch_sel1(const Params& P, cudaStream_t s, bool update) {
-    k_sel1<<<std::max(1, P.sel1_grid), kThreads, 0, s>>>(P, update ? 1 : 0);
-}
-
-// k_sel2 (one CTA: draw, owning shard, in-shard search) then k_pack (the row copy)
-void launch_sel2(const Params& P, cudaStream_t s) {
-    k_sel2<<<1, kThreads, 0, s>>>(P);
-    launch_pdl(k_pack, std::max(1, P.pack_grid), kThreads, 0, s, P);
+// k_sel1 (global reductions, stop logic, selection) then, when it selects,
+// k_pack (the owner's row copy)
+void launch_sel1(const Params& P, cudaStream_t s, int mode) {
+    k_sel1<<<std::max(1, P.sel1_grid), kThreads, 0, s>>>(P, mode);
+    if (mode != 0) launch_pdl(k_pack, std::max(1, P.pack_grid), kThreads, 0, s, P);
 }
 
 void launch_power_step2(double* v, const double* w, long long dim, double* ps, double tol,

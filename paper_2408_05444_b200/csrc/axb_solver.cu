@@ -50,8 +50,10 @@ const Api* api(const char** why) {
             a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
             a.GetErrorString =
                 reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+            a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+            a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
             const bool ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce &&
-                            a.AllGather && a.GetErrorString;
+                            a.AllGather && a.GetErrorString && a.GroupStart && a.GroupEnd;
             state = ok ? 1 : -1;
             if (!ok) reason = "libnccl.so.2 lacks a required symbol";
         }
@@ -168,6 +170,10 @@ ncclResult_t emu_destroy(ncclComm_t comm) {
     return ncclSuccess;
 }
 
+// the emulated collectives complete synchronously, one after another: a group
+// needs no fusing
+ncclResult_t emu_group() { return ncclSuccess; }
+
 const char* emu_error(ncclResult_t r) {
     return r == ncclSuccess ? "ok" : "emulated collective failed";
 }
@@ -181,6 +187,8 @@ const Api* emulated_api() {
         e.AllGather = emu_allgather;
         e.CommDestroy = emu_destroy;
         e.GetErrorString = emu_error;
+        e.GroupStart = emu_group;
+        e.GroupEnd = emu_group;
         init = true;
     }
     return &e;
@@ -403,7 +411,7 @@ struct axb_solver {
     uint64_t m_g = 0, row0 = 0, p_loc = 0, n_loc = 0;
     ncclComm_t comm = nullptr;
     const axb_nccl::Api* nc = nullptr;
-    DevBuf<double> pack, pack_send, recs, masses, a_sq_g, scal_ag;
+    DevBuf<double> pack, pack_send, recs, a_sq_g, scal_ag;
     DevBuf<int> flags;
     DevBuf<DevState> st;
     DevState* hs = nullptr;  // pinned host mirror
@@ -426,7 +434,9 @@ struct axb_solver {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;
-    double loop_ms = 0.0, k2_ms = 0.0, yg_ms = 0.0, zx_ms = 0.0;
+    double loop_ms = 0.0, k2_ms = 0.0, yg_ms = 0.0, zx_ms = 0.0, sel_ms = 0.0;
+    double coll_ms[4] = {0.0, 0.0, 0.0, 0.0};  // y allreduce, z allgather, norms allgather, row allreduce
+    static constexpr int kProfEv = 9;
     uint64_t k2_launches = 0, kernel_launches = 0;
     uint64_t last_nb = 0;  // iterations armed by the last batch_launch
 
@@ -506,6 +516,15 @@ struct axb_solver {
     void allreduce(const double* send, double* recv, size_t count) {
         nccl_ck(nc->AllReduce(send, recv, count, ncclFloat64, ncclSum, comm, stream),
                 "ncclAllReduce");
+    }
+    // every shard's ‖R_l‖² slice into the global r_sq and every shard's record
+    // {Σ‖R_l‖², max ratio, argmax, ‖X−X_ref‖² part} into recs: one NCCL group, so
+    // one fused collective launch
+    void gather_norms() {
+        nccl_ck(nc->GroupStart(), "ncclGroupStart");
+        allgather_inplace(r_sq.p, m);
+        allgather_inplace(recs.p, 4);
+        nccl_ck(nc->GroupEnd(), "ncclGroupEnd");
     }
     // Σ over ranks in rank order of a host scalar (identical on every rank)
     double global_sum(double local) {
@@ -589,6 +608,11 @@ struct axb_solver {
 
         const cudaMemcpyKind kind =
             opt.inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        // device inputs may still be being written by the caller's work on any of
+        // its streams (e.g. C = A·X*·B just queued on torch's current stream); the
+        // copy stream below is non-blocking and would not wait for it, so order
+        // the copies after everything already queued on this device
+        if (opt.inputs_on_device) ck(cudaDeviceSynchronize(), "order after the caller's work");
         // inputs arrive on a copy stream in the order they are needed; the
         // compute stream waits per input, so ‖B‖₂ (and G) overlap the C copy.
         // Each buffer is allocated just before its copy is queued, so mapping the
@@ -635,7 +659,9 @@ struct axb_solver {
         ck(cudaStreamWaitEvent(stream, evA, 0), "wait A");
         a_sq.alloc(m, "a_sq");
         rbk_cum.alloc(m_g, "rbk_cum");
-        r_sq.alloc(m, "r_sq");
+        // sharded: the global ‖R_l‖² (allgathered each iteration); this rank's
+        // kernels write their rows in place at row0
+        r_sq.alloc(sharded ? m_g : m, "r_sq");
         scal.alloc(4, "scalars");
         if (sharded) {
             a_sq_g.alloc(m_g, "a_sq global");
@@ -644,8 +670,6 @@ struct axb_solver {
             pack_send.alloc(n + p + 2, "pack send");
             ck(cudaMemsetAsync(pack_send.p, 0, sizeof(double) * (n + p + 2), stream), "pack");
             recs.alloc(4 * (size_t)world, "records");
-            masses.alloc(world, "masses");
-            ck(cudaMemsetAsync(masses.p, 0, sizeof(double) * world, stream), "masses");
         }
         sq_part.alloc(sumsq_parts((long long)std::max({m * n, q * n, p * q, m * p})), "parts");
 
@@ -849,14 +873,16 @@ struct axb_solver {
         rrec.alloc(std::max<size_t>((size_t)P.r_grid, 1024), "rrec");
         tr_row.alloc(trace_cap, "trace");
         forced.alloc(trace_cap, "forced rows");
-        gsum.alloc((m + 31) / 32, "group sums");
+        gsum.alloc(((sharded ? m_g : m) + 31) / 32, "group sums");
         tr_metric.alloc(trace_cap, "trace");
         tr_rel.alloc(trace_cap, "trace");
         flags.alloc(m, "flags");
         st.alloc(1, "state");
 
         P.A = A.p; P.B = B.p; P.R = R.p; P.X = X.p; P.Xref = Xref.p;
-        P.a_sq = a_sq.p; P.rbk_cum = rbk_cum.p; P.r_sq = r_sq.p;
+        P.a_sq = a_sq.p; P.rbk_cum = rbk_cum.p;
+        P.r_sq = sharded ? r_sq.p + row0 : r_sq.p;
+        P.r_sq_g = sharded ? r_sq.p : nullptr;
         P.G = gram_cached ? G.p : nullptr;
         P.g = g.p; P.y = y.p; P.z = z.p; P.zpart = zpart.p; P.zcnt = zcnt.p; P.xpart = xpart.p;
         P.rrec = rrec.p; P.trace_row = tr_row.p; P.trace_metric = tr_metric.p;
@@ -866,7 +892,6 @@ struct axb_solver {
         P.pack = sharded ? pack.p : nullptr;
         P.pack_send = pack_send.p;
         P.recs = recs.p;
-        P.masses = masses.p;
         P.a_sq_g = sharded ? a_sq_g.p : a_sq.p;
         P.alpha = alpha;
         P.theta = cfg.method == AXB_RGRBK ? cfg.theta : 0.5;
@@ -876,7 +901,8 @@ struct axb_solver {
         P.c_fro = c_fro;
         P.method = cfg.method;
         P.stop_kind = cfg.stop_kind;
-        P.tie_guard = (opt.tie_guard && !sharded) ? 1 : 0;  // exact replay needs all rows
+        // sharded too: every rank sees all of r_sq; 2 = always walk (test hook)
+        P.tie_guard = opt.tie_guard == 2 ? 2 : (opt.tie_guard ? 1 : 0);
         {
             // greedy pre-selection spread over the SMs (k_sel_greedy) once the
             // O(m) membership pass outweighs one more PDL-chained launch
@@ -1089,9 +1115,8 @@ struct axb_solver {
             // local ‖X−X_ref‖² first: this shard's record carries it
             if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) launch_err_fresh(P, stream);
             launch_r(P, stream, false);
-            allgather_inplace(recs.p, 4);
-            launch_sel1(P, stream, false);
-            if (needs_masses()) allgather_inplace(masses.p, 1);
+            gather_norms();
+            launch_sel1(P, stream, 0);
         } else {
             launch_r(P, stream, false);
             if (cfg.stop_kind == AXB_STOP_SOLUTION_RRN) launch_err_fresh(P, stream);
@@ -1107,7 +1132,7 @@ struct axb_solver {
 
     void ensure_selection() {
         if (!sel_valid && sharded) {
-            launch_sel2(P, stream);  // k_sel2 + k_pack
+            launch_sel1(P, stream, 2);  // k_sel1 (select only) + k_pack
             allreduce(pack_send.p, pack.p, n + p + 2);
             kernel_launches += 2;
             sel_valid = true;
@@ -1120,11 +1145,9 @@ struct axb_solver {
 
     // ---------------------------------------------------------------- iteration
     // one iteration; sharded: y partial → allreduce, z slice → allgather, local R
-    // update → record allgather → global stop logic + shard masses → mass
-    // allgather → draw + owner pack → row allreduce
-    // greedy rules need the per-shard member masses; the others select from the
-    // allgathered records (MWRBK) or the replicated ‖A_i‖² (BK, RBK) alone
-    bool needs_masses() const { return cfg.method == AXB_GRBK || cfg.method == AXB_RGRBK; }
+    // update → ONE grouped allgather (‖R_l‖² slices + shard records) → global stop
+    // logic and the selection over the global rows, identical on every rank →
+    // owner pack → row allreduce: 4 collectives, 5 kernels
 
     void enqueue_iteration() {
         launch_yg(P, stream, !gram_cached);
@@ -1134,14 +1157,12 @@ struct axb_solver {
         launch_r(P, stream, true);
         if (P.sel_split) launch_sel_greedy(P, stream);
         if (sharded) {
-            allgather_inplace(recs.p, 4);
-            launch_sel1(P, stream, true);
-            if (needs_masses()) allgather_inplace(masses.p, 1);
-            launch_sel2(P, stream);
+            gather_norms();
+            launch_sel1(P, stream, 1);
             allreduce(pack_send.p, pack.p, n + p + 2);
         }
     }
-    int launches_per_iteration() const { return sharded ? 6 : (P.sel_split ? 4 : 3); }
+    int launches_per_iteration() const { return sharded ? 5 : (P.sel_split ? 4 : 3); }
     void launch_iteration() {
         enqueue_iteration();
         kernel_launches += launches_per_iteration();
@@ -1182,29 +1203,33 @@ struct axb_solver {
         if (P.persist && !profiling) {
             // nothing more to enqueue
         } else if (profiling) {
-            if (prof_ev.size() < 4 * nb) {
+            // 9 events per iteration around every op: [y][y allreduce][z, X][z allgather]
+            // [R update (+ K3)][r_sq/record allgather][selection + pack][row allreduce]
+            if (prof_ev.size() < kProfEv * nb) {
                 size_t have = prof_ev.size();
-                prof_ev.resize(4 * nb);
+                prof_ev.resize(kProfEv * nb);
                 for (size_t i = have; i < prof_ev.size(); ++i) ck(cudaEventCreate(&prof_ev[i]), "ev");
             }
             for (uint64_t i = 0; i < nb; ++i) {
-                ck(cudaEventRecord(prof_ev[4 * i], stream), "ev");
+                cudaEvent_t* e = &prof_ev[kProfEv * i];
+                ck(cudaEventRecord(e[0], stream), "ev");
                 launch_yg(P, stream, !gram_cached);
-                ck(cudaEventRecord(prof_ev[4 * i + 1], stream), "ev");
+                ck(cudaEventRecord(e[1], stream), "ev");
                 if (sharded) allreduce(y.p, y.p, q);
+                ck(cudaEventRecord(e[2], stream), "ev");
                 launch_zx(P, stream);
+                ck(cudaEventRecord(e[3], stream), "ev");
                 if (sharded) allgather_inplace(z.p, n_loc);
-                ck(cudaEventRecord(prof_ev[4 * i + 2], stream), "ev");
+                ck(cudaEventRecord(e[4], stream), "ev");
                 launch_r(P, stream, true);
                 if (P.sel_split) launch_sel_greedy(P, stream);  // timed with K2: its tail
-                ck(cudaEventRecord(prof_ev[4 * i + 3], stream), "ev");
-                if (sharded) {
-                    allgather_inplace(recs.p, 4);
-                    launch_sel1(P, stream, true);
-                    if (needs_masses()) allgather_inplace(masses.p, 1);
-                    launch_sel2(P, stream);
-                    allreduce(pack_send.p, pack.p, n + p + 2);
-                }
+                ck(cudaEventRecord(e[5], stream), "ev");
+                if (sharded) gather_norms();
+                ck(cudaEventRecord(e[6], stream), "ev");
+                if (sharded) launch_sel1(P, stream, 1);
+                ck(cudaEventRecord(e[7], stream), "ev");
+                if (sharded) allreduce(pack_send.p, pack.p, n + p + 2);
+                ck(cudaEventRecord(e[8], stream), "ev");
                 kernel_launches += launches_per_iteration();
             }
         } else if (nb < (uint64_t)graph_iters || emulated) {
@@ -1224,13 +1249,18 @@ struct axb_solver {
         if (profiling) {
             const uint64_t done = hs->k - k;
             for (uint64_t i = 0; i < done; ++i) {
-                float a = 0.f, b = 0.f, c = 0.f;
-                ck(cudaEventElapsedTime(&a, prof_ev[4 * i], prof_ev[4 * i + 1]), "elapsed");
-                ck(cudaEventElapsedTime(&b, prof_ev[4 * i + 1], prof_ev[4 * i + 2]), "elapsed");
-                ck(cudaEventElapsedTime(&c, prof_ev[4 * i + 2], prof_ev[4 * i + 3]), "elapsed");
-                yg_ms += a;
-                zx_ms += b;
-                k2_ms += c;
+                const cudaEvent_t* e = &prof_ev[kProfEv * i];
+                float t[kProfEv - 1];
+                for (int j = 0; j + 1 < kProfEv; ++j)
+                    ck(cudaEventElapsedTime(&t[j], e[j], e[j + 1]), "elapsed");
+                yg_ms += t[0];
+                coll_ms[0] += t[1];
+                zx_ms += t[2];
+                coll_ms[1] += t[3];
+                k2_ms += t[4];
+                coll_ms[2] += t[5];
+                sel_ms += t[6];
+                coll_ms[3] += t[7];
                 ++k2_launches;
             }
         }
@@ -1852,6 +1882,18 @@ int axb_solvers_run(axb_solver* const* hs, uint32_t count, axb_report* reps,
             statuses[i] = record_failure(hs[i], e);
         }
     }
+    // Batched wall-clock semantics: every handle's loop clock starts at one common
+    // instant, after all the run_begin() work (each handle's initial exact metric,
+    // solver.hpp:344, which the reference also runs before its clock starts), and
+    // ends when that handle's own loop ends.  Handles advance together through
+    // shared launches, so a handle's wall time covers the batch's progress up to
+    // its own end — it is the time-to-solution inside this batch, not the time the
+    // handle would take alone (use axb_solver_run for that).
+    {
+        const auto common = std::chrono::steady_clock::now();
+        for (uint32_t i = 0; i < count; ++i)
+            if (active[i]) ctx[i].t0 = common;
+    }
     auto fail_one = [&](uint32_t i, const AxbError& e) {
         hs[i]->run_fail(ctx[i], e);
         statuses[i] = record_failure(hs[i], e);
@@ -2018,7 +2060,9 @@ int axb_solver_get_X(axb_solver* s, double* out) {
     return st ? st : copy_out(s, out, s->X.p, s->p * s->q);
 }
 int axb_solver_get_R(axb_solver* s, double* out) { return copy_out(s, out, s->R.p, s->m * s->n); }
-int axb_solver_get_r_sq(axb_solver* s, double* out) { return copy_out(s, out, s->r_sq.p, s->m); }
+int axb_solver_get_r_sq(axb_solver* s, double* out) {
+    return copy_out(s, out, s->P.r_sq, s->m);  // sharded: this rank's slice of the global r_sq
+}
 int axb_solver_get_a_sq(axb_solver* s, double* out) { return copy_out(s, out, s->a_sq.p, s->m); }
 int axb_solver_dims(const axb_solver* s, uint64_t dims[4]) {
     dims[0] = s->m; dims[1] = s->p; dims[2] = s->q; dims[3] = s->n;
@@ -2050,11 +2094,22 @@ int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]) {
     out_ms[2] = s->k2_ms / nl;
     return AXB_OK;
 }
+int axb_solver_collective_times(const axb_solver* s, double out_ms[5]) {
+    const double nl = s->k2_launches ? (double)s->k2_launches : 1.0;
+    out_ms[0] = s->coll_ms[0] / nl;
+    out_ms[1] = s->coll_ms[1] / nl;
+    out_ms[2] = s->coll_ms[2] / nl;
+    out_ms[3] = s->sel_ms / nl;
+    out_ms[4] = s->coll_ms[3] / nl;
+    return AXB_OK;
+}
 int axb_solver_set_profiling(axb_solver* s, int32_t on) {
     s->profiling = on != 0;
     s->k2_ms = 0.0;
     s->yg_ms = 0.0;
     s->zx_ms = 0.0;
+    s->sel_ms = 0.0;
+    for (double& c : s->coll_ms) c = 0.0;
     s->k2_launches = 0;
     s->kernel_launches = 0;
     return AXB_OK;

@@ -57,8 +57,8 @@ class BenchmarkOptions:  # analysis.hpp BenchmarkOptions
     trials: int = 20
     alpha_rule: AlphaRule = AlphaRule.Safe
     alpha_value: float = 0.0
-    max_iter: int = 200000
-    seed: int = 0
+    max_iter: int = 1000000   # analysis.hpp:220
+    seed: int = 1             # analysis.hpp:221
     stop_kind: StopRule.Kind = StopRule.Kind.SolutionRrn
     tol: float = 1e-6
     jobs: int = 4

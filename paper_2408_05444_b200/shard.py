@@ -5,8 +5,12 @@ only the NCCL unique id at start-up; every data-path exchange of the iteration
 is an NCCL call the C-ABI library enqueues itself (inside its CUDA graphs):
 
     y partial  → allreduce (q doubles)      z slice   → allgather (n doubles)
-    records    → allgather (4 per rank)     masses    → allgather (1 per rank)
+    ‖R_l‖² slice + record → one grouped allgather (m_local + 4 doubles per rank)
     owner row  → allreduce (n + p + 2; only the owner contributes non-zeros)
+
+After the grouped allgather every rank holds the global ‖R_l‖², so every rank
+runs the single-GPU selection over the global rows (tie guard and the
+reference's sequential walk included) and all ranks agree on the row.
 
 Rows are split into equal contiguous shards (m_global = world·m_local).
 """

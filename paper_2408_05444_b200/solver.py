@@ -168,7 +168,7 @@ class Options:
     cache_gram: int = -1          # -1 auto, 0 GEMV g = A·A_iᵀ per step, 1 cache G = A·Aᵀ
     spectral_on_device: int = -1  # -1 auto, 0 host (bitwise reference α), 1 device
     graph_iters: int = 0          # iterations per captured CUDA graph (0 = default)
-    tie_guard: bool = True        # sequential re-check of near-boundary greedy draws
+    tie_guard: int = 1            # sequential re-check of near-boundary greedy draws (2: always)
     spectral_max_iter: int = 0    # 0 = reference default 5000
     alpha_override: float = 0.0   # >0: use verbatim (e.g. the oracle's α)
     # row sharding: this solver owns rows [row_offset, row_offset+m)
@@ -236,6 +236,11 @@ class Solver:
         if _shape(C_) != (m, n):
             from .errors import ShapeError
             raise ShapeError(f"solve: C must be {m}x{n}")
+        # checked before any buffer is handed to the library (solver.hpp:182-185)
+        if cfg.stop.kind == StopRule.Kind.SolutionRrn and cfg.stop.reference is not None:
+            if _shape(cfg.stop.reference) != (p, q):
+                from .errors import ShapeError
+                raise ShapeError("reference solution shape mismatch")
         self.m, self.p, self.q, self.n = m, p, q, n
         on_dev = _device_ptr(A) is not None
         keep = []
@@ -272,7 +277,7 @@ class Solver:
         o.cache_gram = opts.cache_gram
         o.spectral_on_device = opts.spectral_on_device
         o.graph_iters = opts.graph_iters
-        o.tie_guard = 1 if opts.tie_guard else 0
+        o.tie_guard = 2 if opts.tie_guard == 2 else (1 if opts.tie_guard else 0)
         o.spectral_max_iter = opts.spectral_max_iter
         o.alpha_override = opts.alpha_override
         o.nccl_comm = opts.nccl_comm or None
@@ -491,6 +496,22 @@ class Solver:
         out = (C.c_double * 3)()
         self._lib.axb_solver_kernel_times(self._h, out)
         return {"yg_ms": out[0], "zx_ms": out[1], "k2_ms": out[2]}
+
+    def collective_times(self):
+        """Row-sharded solvers, profiled runs: average ms per iteration of each
+        exchange step (zeros on one GPU)."""
+        out = (C.c_double * 5)()
+        self._lib.axb_solver_collective_times(self._h, out)
+        return {"y_allreduce_ms": out[0], "z_allgather_ms": out[1],
+                "norms_allgather_ms": out[2], "select_kernels_ms": out[3],
+                "row_allreduce_ms": out[4]}
+
+    def selection_stats(self):
+        """Greedy draws made on the device and how many of them took the exact
+        sequential walk of the reference (the tie guard's fallback)."""
+        d = (C.c_uint64 * 8)()
+        self._chk(self._lib.axb_solver_debug_state(self._h, d))
+        return {"greedy_selections": int(d[5]), "sequential_walks": int(d[6])}
 
     def last_timing(self):
         a = C.c_double(); b = C.c_double(); c = C.c_uint64(); d = C.c_uint64()

@@ -151,3 +151,23 @@ def test_csr_validation_errors_before_any_device_work():
     nanm.data[0] = np.nan
     with pytest.raises(axb.DomainError):
         axb.Solver(nanm, np.eye(3), np.eye(3), None, axb.SolveConfig())
+
+
+def test_reference_dropin_builds_against_reference_headers():
+    """tests/cpp/reference_dropin.cpp — the shim with the reference's own headers on
+    the include path (axb::Matrix / axb::SolveConfig in, axb::SolveReport out, the
+    reference's exception types) — compiles and links; without a device it exits 3
+    after its first create (no CPU fallback)."""
+    import subprocess
+
+    import __graft_entry__ as g
+    import paper_2408_05444_b200 as axb
+
+    if not os.path.isdir(os.path.join(g.REF_INC, "axb")):
+        pytest.skip("reference headers absent (GPU box): the prebuilt binary is used there")
+    g.build_reference_dropin()
+    assert os.path.exists(g.DROPIN_EXE)
+    if axb.device_available():
+        pytest.skip("device present: tests/test_gpu_dropin.py runs it")
+    out = subprocess.run([g.DROPIN_EXE], capture_output=True, text=True)
+    assert out.returncode == 3 and "device none" in out.stdout, out.stdout

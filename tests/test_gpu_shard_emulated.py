@@ -5,8 +5,9 @@ collectives run through the library's in-process emulation
 (axb_nccl_emulated_group: stream sync, host barrier, rank 0 combines, barrier),
 so no rank's kernel ever waits on another's (the profiling recipe's rule for
 fewer GPUs than ranks).  Everything else is the production sharded path:
-column-split y/z, row-split X, the shard records and masses, the rank-ordered
-prefix with the shared xoshiro draw, the owner's row pack, the sharded init
+column-split y/z, row-split X, the grouped allgather of the ‖R_l‖² slices and
+shard records, the selection over the global rows that every rank runs with the
+shared xoshiro draw (tie guard included), the owner's row pack, the sharded init
 (a_sq, G columns, ‖B‖₂, R0) and checkpoints.  Bar: the oracle's rows and X within
 1e-10, as for one GPU.
 """
@@ -174,3 +175,47 @@ def test_sharded_config5_shape_world8(axb, orc):
         mism = np.nonzero(rows != ro)[0]
         assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
         assert rel(Xr, so.X()) <= 1e-10
+
+
+@pytest.mark.parametrize("world", [1, 8])
+@pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.RGRBK, 0.3)])
+def test_sharded_forced_near_tie_walk(axb, orc, world, tag, theta):
+    """The near-tie path of the sharded selection.  tie_guard = 2 makes EVERY
+    greedy draw take the exact fallback — the reference's sequential member-mass
+    walk with upper_bound and the zero-weight walk-back (solver.hpp:243-253,
+    rng.hpp:84-99) over the global rows — which a real near-tie takes only when
+    the draw lands within 8·m·ε·total of a boundary.  Every rank must still pick
+    the oracle's row on every step, and count one walk per draw."""
+    from paper_2408_05444_b200 import shard
+
+    m, p, q, n = 1024, 64, 32, 160
+    A, B, X, Cm = O.generate(orc, 13, m, p, q, n)
+    A[5] = 0.0  # a zero row of A (and of C): never a member
+    Cm[5] = 0.0
+    k = 300
+    cfg_o = O.make_config(method=tag, theta=theta, seed=9, stop_kind=O.SOLUTION_RRN, tol=0.0,
+                          reference=X, refresh_interval=0)
+    so = O.Solver(orc, A, B, Cm, None, cfg_o)
+    ro = so.steps(k)
+    comms = shard.emulated_comms(world)
+    ml = m // world
+    try:
+        def rank(r):
+            sl = slice(r * ml, (r + 1) * ml)
+            cfg = axb.SolveConfig(method=method(axb, tag, theta),
+                                  stop=axb.StopRule.solution_rrn(0.0, X), seed=9,
+                                  refresh_interval=0)
+            s = shard.sharded_solver(np.ascontiguousarray(A[sl]), B, np.ascontiguousarray(Cm[sl]),
+                                     None, cfg, comms[r], world, r, tie_guard=2)
+            rows = s.steps(k)
+            return rows, s.X(), s.selection_stats()
+
+        res = run_ranks(world, rank)
+    finally:
+        for c in comms:
+            shard.nccl_comm_destroy(c)
+    for rows, Xr, stats in res:
+        mism = np.nonzero(rows != ro)[0]
+        assert mism.size == 0, f"first row mismatch at step {mism[:5]}"
+        assert rel(Xr, so.X()) <= 1e-10
+        assert stats["sequential_walks"] == stats["greedy_selections"] >= k
