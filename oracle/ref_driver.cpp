@@ -14,6 +14,7 @@
 
 #include "axb/analysis.hpp"
 #include "axb/decomp.hpp"
+#include "axb/imaging.hpp"
 #include "axb/rng.hpp"
 #include "axb/solver.hpp"
 
@@ -338,6 +339,74 @@ int ref_bk_limit(const double* A, size_t m, size_t p, const double* B, size_t q,
 
 int ref_rrn(const double* xk, const double* ref, size_t rows, size_t cols, double* out) {
     return guarded(&g_an, [&] { *out = rrn(mk(xk, rows, cols), mk(ref, rows, cols)); });
+}
+
+// ---- CSR operands and the §6 restoration shape -------------
+// imaging.hpp:93-136 build_blur_operator(gaussian_kernel(ksize, sigma)) for an
+// h×w image: returns nnz; fills rp (h·w+1), ci, v when non-NULL.
+uint64_t ref_blur_operator(size_t h, size_t w, size_t ksize, double sigma, uint64_t* rp,
+                           uint64_t* ci, double* v) {
+    const SparseMatrix A = build_blur_operator(h, w, gaussian_kernel(ksize, sigma));
+    if (rp) {
+        auto r = A.row_ptr();
+        for (size_t i = 0; i < r.size(); ++i) rp[i] = r[i];
+        for (size_t i = 0; i < A.rows(); ++i) {
+            auto idx = A.row_indices(i);
+            auto val = A.row_values(i);
+            for (size_t k = 0; k < idx.size(); ++k) {
+                ci[r[i] + k] = idx[k];
+                v[r[i] + k] = val[k];
+            }
+        }
+    }
+    return A.nnz();
+}
+
+// imaging.hpp:276-310 synthetic_test_image, column-stacked (stack_channels,
+// :42-51): X (h·w)×3 row-major; and the paper's cross-channel matrix A_c (:139-141)
+void ref_synthetic_stack(size_t h, size_t w, double* X, double* A_c) {
+    const ChannelStack s = stack_channels(synthetic_test_image(h, w));
+    const auto d = s.X.data();
+    std::copy(d.begin(), d.end(), X);
+    const DenseMatrix c = cross_channel_paper();
+    std::copy(c.data().begin(), c.data().end(), A_c);
+}
+
+// The reference's sparse engine: Solver<SparseMatrix, BMat> (BMat CSR when b_rp is
+// non-NULL, else dense), k step() calls; rows, X (p×q), r_sq (m), α out.
+int ref_sparse_steps(const uint64_t* a_rp, const uint64_t* a_ci, const double* a_v, size_t m,
+                     size_t p, const uint64_t* b_rp, const uint64_t* b_ci, const double* b_v,
+                     const double* b_dense, size_t q, size_t n, const double* C, const double* X0,
+                     const RefConfig* cfg, uint64_t k, uint64_t* rows, double* X_out,
+                     double* r_sq_out, double* alpha_out, char* err) {
+    Handle h;
+    auto csr = [](const uint64_t* rp, const uint64_t* ci, const double* v, size_t r, size_t c) {
+        std::vector<size_t> R(rp, rp + r + 1), I(ci, ci + rp[r]);
+        std::vector<double> V(v, v + rp[r]);
+        return SparseMatrix(r, c, std::move(R), std::move(I), std::move(V));
+    };
+    auto drive = [&](auto& s) {
+        for (uint64_t t = 0; t < k; ++t) rows[t] = s.step();
+        const auto x = s.X().data();
+        std::copy(x.begin(), x.end(), X_out);
+        const auto rs = s.residual_row_sq();
+        std::copy(rs.begin(), rs.end(), r_sq_out);
+        *alpha_out = s.alpha();
+    };
+    const int st = guarded(&h, [&] {
+        SparseMatrix A = csr(a_rp, a_ci, a_v, m, p);
+        if (b_rp) {
+            Solver<SparseMatrix, SparseMatrix> s(std::move(A), csr(b_rp, b_ci, b_v, q, n),
+                                                 mk(C, m, n), mk(X0, p, q), to_cfg(cfg, p, q));
+            drive(s);
+        } else {
+            Solver<SparseMatrix, DenseMatrix> s(std::move(A), mk(b_dense, q, n), mk(C, m, n),
+                                                mk(X0, p, q), to_cfg(cfg, p, q));
+            drive(s);
+        }
+    });
+    if (st && err) std::snprintf(err, 256, "%s", h.err.c_str());
+    return st;
 }
 
 }  // extern "C"

@@ -139,6 +139,15 @@ struct Params {
     int z_nslab, z_nj, z_jrows, x_ctas;
     int sel1_grid, pack_grid;  // sharded selection: membership CTAs, row-pack CTAs
     int sel_split, sel_grid;     // greedy pre-selection across sel_grid CTAs (k_sel_greedy)
+    // ---- CSR operands (null = dense).  The persistent general body
+    // iterates stored entries only, as the reference's Solver<SparseMatrix,…> does
+    // (solver.hpp:272-273, 294-295, 489-492): y = B·R_iᵀ over B's rows, z = yᵀ·B over
+    // Bᵀ's rows (B's columns), the X update over A_i's entries, the R update over
+    // the CSR Gram row G_i (scattered into g, zero elsewhere) ----
+    const long long* a_rp; const int* a_ci; const double* a_v;     // A  m×p
+    const long long* g_rp; const int* g_ci; const double* g_v;     // G = A·Aᵀ (m×m)
+    const long long* b_rp; const int* b_ci; const double* b_v;     // B  q×n
+    const long long* bt_rp; const int* bt_ci; const double* bt_v;  // Bᵀ n×q
 };
 
 // ---- launchers (axb_iter.cu) ----
@@ -151,6 +160,11 @@ void launch_select(const Params& P, cudaStream_t s, int method, double theta, in
 void launch_query(const Params& P, cudaStream_t s, double theta, int want_set);
 void launch_rollback(const Params& P, cudaStream_t s);
 void launch_err_fresh(const Params& P, cudaStream_t s);
+// T = S·X for a CSR S (rows × p) and dense X (p × q), row-major T (rows × q):
+// T_i = Σ_e S_v[e]·X[S_ci[e], :] over S_i's stored entries in order
+// (matrix.hpp sparse matmul), one warp per row
+void launch_spmm_csr(const long long* rp, const int* ci, const double* v, long long rows,
+                     const double* X, long long q, double* T, cudaStream_t s);
 // device power iteration helpers: y = M v (rows), w = Mᵀ y (cols)
 void launch_rowdot(const double* M, long long rows, long long cols, const double* v, double* out,
                    cudaStream_t s);

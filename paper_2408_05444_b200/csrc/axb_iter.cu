@@ -1815,13 +1815,15 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
     const long long m = P.m, n = P.n, p = P.p, q = P.q;
     const long long gw = (long long)grid.rank() * kW + warp;  // global warp
     const long long nw = (long long)grid.size() * kW;
+    long long g_prev = -1;  // CSR A: the Gram row scattered into g last (CTA 0)
     if (tid == 0) lst = *P.st;
     __syncthreads();
     for (;;) {
         if (lst.status != ST_RUN || lst.k >= lst.k_limit) break;
         PT_MARK(-1);
         PT_ITER();
-        if (!lst.sel_valid) {  // K3 (every CTA, identically)
+        // K3 (every CTA, identically); update_row(i) brings its own row (k_set_sel)
+        if (!lst.sel_valid && lst.fin_mode != FIN_UPDATE_ROW) {
             long long row = 0;
             if (tid == 0) sh.err = 0;
             __syncthreads();
@@ -1849,12 +1851,43 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         const double* Ai = P.A + sel * p;
         // ---- y = B·R_iᵀ (+ g = A·A_iᵀ) ----
         // two rows per warp pass sharing the vector loads (y rows, then g rows)
-        {
+        if (P.b_rp) {
+            // CSR B: y_j = Σ over B_j's stored entries of B_jk·R_ik (matvec_into,
+            // solver.hpp:489-492), a warp per row
+            const long long* const brp = P.b_rp;
+            const int* const bci = P.b_ci;
+            const double* const bv = P.b_v;
+            for (long long j = gw; j < q; j += nw) {
+                double a = 0.0;
+                for (long long e = brp[j] + lane; e < brp[j + 1]; e += 32)
+                    a += __ldg(bv + e) * __ldcg(Ri + __ldg(bci + e));
+                a = warp_sum(a);
+                if (lane == 0) P.y[j] = a;
+            }
+        }
+        if (P.g_rp) {
+            // CSR A: the Gram row G_i (CSR, formed once in the reference's order)
+            // scattered into the dense coefficient vector g, whose other entries stay
+            // exactly zero, so the R phase below touches only l ∈ nz(G_i)
+            // (solver.hpp:294-295).  CTA 0 clears the previous row's entries first;
+            // the grid barrier publishes g before the R phase reads it.
+            if (grid.rank() == 0) {
+                double* const go = P.g;
+                if (g_prev >= 0)
+                    for (long long e = P.g_rp[g_prev] + tid; e < P.g_rp[g_prev + 1]; e += kT)
+                        go[P.g_ci[e]] = 0.0;
+                __syncthreads();
+                for (long long e = P.g_rp[sel] + tid; e < P.g_rp[sel + 1]; e += kT)
+                    go[P.g_ci[e]] = P.g_v[e];
+                g_prev = sel;
+            }
+        }
+        if (!P.b_rp || (!P.G && !P.g_rp)) {
             double* const yo = P.y;
             double* const go = P.g;
             const double* const Bb = P.B;
             const double* const Ab = P.A;
-            for (long long it = gw; it < q; it += 2 * nw) {
+            for (long long it = gw; it < q && !P.b_rp; it += 2 * nw) {
                 const long long it1 = it + nw;
                 double a0, a1;
                 warp_dot_pair(Bb + it * n, it1 < q ? Bb + it1 * n : nullptr, Ri, n, lane,
@@ -1864,7 +1897,7 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
                     if (it1 < q) yo[it1] = a1;
                 }
             }
-            if (!P.G) {
+            if (!P.G && !P.g_rp) {
                 for (long long it = gw; it < m; it += 2 * nw) {
                     const long long it1 = it + nw;
                     double a0, a1;
@@ -1881,7 +1914,20 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         grid.sync();
         PT_MARK(6);
         // ---- z = yᵀ·B, stage 1: (column slab × row chunk) partials; X update ----
-        {
+        if (P.bt_rp) {
+            // CSR B: z_c = Σ over column c of B (the rows of Bᵀ, ascending j) of
+            // y_j·B_jc, a warp per column, written straight to z
+            const long long* const trp = P.bt_rp;
+            const int* const tci = P.bt_ci;
+            const double* const tv = P.bt_v;
+            for (long long c = gw; c < n; c += nw) {
+                double a = 0.0;
+                for (long long e = trp[c] + lane; e < trp[c + 1]; e += 32)
+                    a += __ldcg(P.y + __ldg(tci + e)) * __ldg(tv + e);
+                a = warp_sum(a);
+                if (lane == 0) P.z[c] = a;
+            }
+        } else {
             const int items = P.z_nslab * P.z_nj;
             const int sub = tid / kPersistThreads, stid = tid % kPersistThreads;
             for (int itm = grid.rank() * kSub + sub; itm < items; itm += grid.size() * kSub) {
@@ -1906,7 +1952,29 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         const double* const yb = P.y;
         double* const Xb = P.X;
         const double* const Xrefb = P.Xref;
-        for (long long t = gw; t < p; t += nw) {
+        if (P.a_rp) {
+            // CSR A: X_t += (coef·A_it)·y for t ∈ nz(A_i) only, and the reference's
+            // incremental ‖X−X_ref‖² tracker, Σ_j (d1² − d0²) per updated row
+            // (solver.hpp:272-289); a warp per stored entry
+            const long long e0 = P.a_rp[sel], e1 = P.a_rp[sel + 1];
+            for (long long e = e0 + gw; e < e1; e += nw) {
+                const long long t = P.a_ci[e];
+                const double f = __dmul_rn(coef, P.a_v[e]);
+                double* xr = Xb + t * q;
+                const double* rr = Xrefb ? Xrefb + t * q : nullptr;
+                for (long long k = lane; k < q; k += 32) {
+                    const double x0 = xr[k];
+                    const double x1 = __dadd_rn(x0, __dmul_rn(f, __ldcg(yb + k)));
+                    xr[k] = x1;
+                    if (rr) {
+                        const double rv = rr[k];
+                        const double d0 = __dsub_rn(x0, rv), d1 = __dsub_rn(x1, rv);
+                        xacc += __dsub_rn(__dmul_rn(d1, d1), __dmul_rn(d0, d0));
+                    }
+                }
+            }
+        }
+        for (long long t = gw; t < p && !P.a_rp; t += nw) {
             const double f = __dmul_rn(coef, Ai[t]);
             if (f == 0.0 && !Xrefb) continue;  // A_it = 0: X_t unchanged (solver.hpp:272-273)
             double* xr = Xb + t * q;
@@ -1942,7 +2010,7 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         grid.sync();
         PT_MARK(6);
         // ---- z stage 2: fixed-order combine of the row-chunk partials ----
-        for (long long c = (long long)grid.rank() * kT + tid; c < n;
+        for (long long c = (long long)grid.rank() * kT + tid; c < n && !P.bt_rp;
              c += (long long)grid.size() * kT) {
             double a = 0.0;
             for (int k = 0; k < P.z_nj; ++k) a += __ldcg(P.zpart + (long long)k * n + c);
@@ -2125,7 +2193,13 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             __syncthreads();
         }
         if (tid == 0) {
-            const double s = sh.scan[0], e = sh.scan[1], mx = sh.scan[2];
+            const double s = sh.scan[0], mx = sh.scan[2];
+            // CSR A: the incremental tracker (clamped at 0, solver.hpp:290); dense: fresh
+            double e = sh.scan[1];
+            if (P.a_rp) {
+                e = __dadd_rn(lst.err_sq, e);
+                if (e < 0.0) e = 0.0;
+            }
             const long long ax = sh.cand;
             lst.r_fro_sq = s;
             lst.max_ratio = mx;
@@ -2139,6 +2213,10 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
                 lst.err_code = 4;
                 lst.err_k = lst.k;
                 lst.err_val = sqrt(fabs(s));
+            } else if (lst.fin_mode == FIN_UPDATE_ROW) {
+                // public update_row(i): no k++, no trace, no stop check; one pass
+                lst.metric = P.stop_kind == 0 ? e / P.ref_sq : rel;
+                lst.k_limit = lst.k;
             } else {
                 const unsigned long long k = lst.k;
                 const double metric = P.stop_kind == 0 ? e / P.ref_sq : rel;
@@ -2159,6 +2237,9 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         // no barrier needed before the next y phase: it only reads R/B (last
         // written before the grid.sync above) and writes y, which nobody reads
         // until after the next grid.sync
+    }
+    if (P.g_rp && grid.rank() == 0 && g_prev >= 0) {  // leave g all-zero for the next launch
+        for (long long e = P.g_rp[g_prev] + tid; e < P.g_rp[g_prev + 1]; e += kT) P.g[P.g_ci[e]] = 0.0;
     }
     if (grid.rank() == 0 && tid == 0) *P.st = lst;
     PT_STORE();
@@ -3074,6 +3155,30 @@ int launch_persist(const Params& P, cudaStream_t s) {
     void* args[] = {&Pc};
     return (int)cudaLaunchCooperativeKernel((const void*)k_persist, dim3((unsigned)grid),
                                             dim3(kPersistThreads), args, smem, s);
+}
+
+__global__ void __launch_bounds__(256) k_spmm_csr(const long long* __restrict__ rp,
+                                                  const int* __restrict__ ci,
+                                                  const double* __restrict__ v, long long rows,
+                                                  const double* __restrict__ X, long long q,
+                                                  double* __restrict__ T) {
+    const int lane = threadIdx.x & 31;
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = w; i < rows; i += nw) {
+        const long long e0 = rp[i], e1 = rp[i + 1];
+        for (long long c = lane; c < q; c += 32) {
+            double a = 0.0;
+            for (long long e = e0; e < e1; ++e) a = __dadd_rn(a, __dmul_rn(v[e], X[(long long)ci[e] * q + c]));
+            T[i * q + c] = a;
+        }
+    }
+}
+
+void launch_spmm_csr(const long long* rp, const int* ci, const double* v, long long rows,
+                     const double* X, long long q, double* T, cudaStream_t s) {
+    const int grid = (int)std::max<long long>(1, std::min<long long>(148 * 8, (rows + 7) / 8));
+    k_spmm_csr<<<grid, 256, 0, s>>>(rp, ci, v, rows, X, q, T);
 }
 
 void launch_fill(double* p, long long n, double v, cudaStream_t s) {

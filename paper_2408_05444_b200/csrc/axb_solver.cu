@@ -392,6 +392,93 @@ struct DevBuf {
     }
 };
 
+// ---- host CSR helpers ----
+struct Csr {
+    uint64_t rows = 0, cols = 0;
+    std::vector<long long> rp;
+    std::vector<int> ci;
+    std::vector<double> v;
+};
+
+Csr csr_of(const axb_matrix* M) {  // validated by create_ex (SparseMatrix::validate)
+    Csr c;
+    c.rows = M->rows;
+    c.cols = M->cols;
+    c.rp.assign(M->row_ptr, M->row_ptr + M->rows + 1);
+    c.ci.resize(M->nnz);
+    for (uint64_t e = 0; e < M->nnz; ++e) c.ci[e] = (int)M->col_idx[e];
+    c.v.assign(M->values, M->values + M->nnz);
+    return c;
+}
+
+// transpose (matrix.hpp's CSR transpose): column-major counting sort, so each
+// row of the result lists its entries in ascending original-row order
+Csr csr_transpose(const Csr& a) {
+    Csr t;
+    t.rows = a.cols;
+    t.cols = a.rows;
+    t.rp.assign(a.cols + 1, 0);
+    for (int c : a.ci) ++t.rp[(size_t)c + 1];
+    for (uint64_t j = 0; j < a.cols; ++j) t.rp[j + 1] += t.rp[j];
+    t.ci.resize(a.ci.size());
+    t.v.resize(a.v.size());
+    std::vector<long long> pos(t.rp.begin(), t.rp.end() - 1);
+    for (uint64_t i = 0; i < a.rows; ++i)
+        for (long long e = a.rp[i]; e < a.rp[i + 1]; ++e) {
+            const long long d = pos[(size_t)a.ci[e]]++;
+            t.ci[d] = (int)i;
+            t.v[d] = a.v[e];
+        }
+    return t;
+}
+
+// gram_mmt(const SparseMatrix&) (matrix.hpp:496-535): Gustavson accumulation of
+// M·Mᵀ through Mᵀ's rows in the reference's order (acc[j] += m_ik·m_jk over k in
+// row i's stored order), exact-zero sums dropped — so G is the reference's G bit
+// for bit (host code, no FMA contraction)
+Csr gram_csr(const Csr& a) {
+    const Csr t = csr_transpose(a);
+    Csr g;
+    g.rows = g.cols = a.rows;
+    g.rp.assign(a.rows + 1, 0);
+    std::vector<double> acc(a.rows, 0.0);
+    std::vector<char> seen(a.rows, 0);
+    std::vector<int> touched;
+    for (uint64_t i = 0; i < a.rows; ++i) {
+        for (long long e = a.rp[i]; e < a.rp[i + 1]; ++e) {
+            const double v = a.v[e];
+            const int k = a.ci[e];
+            for (long long f = t.rp[k]; f < t.rp[k + 1]; ++f) {
+                const int j = t.ci[f];
+                if (!seen[j]) {
+                    seen[j] = 1;
+                    touched.push_back(j);
+                }
+                acc[j] += v * t.v[f];
+            }
+        }
+        std::sort(touched.begin(), touched.end());
+        for (int j : touched) {
+            if (acc[j] != 0.0) {
+                g.ci.push_back(j);
+                g.v.push_back(acc[j]);
+            }
+            acc[j] = 0.0;
+            seen[j] = 0;
+        }
+        touched.clear();
+        g.rp[i + 1] = (long long)g.ci.size();
+    }
+    return g;
+}
+
+template <class T>
+void upload(DevBuf<T>& d, const std::vector<T>& h, const char* what, cudaStream_t s) {
+    d.alloc(h.size(), what);
+    if (!h.empty()) ck(cudaMemcpyAsync(d.p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, s), what);
+    ck(cudaStreamSynchronize(s), what);  // h is a pageable temporary
+}
+
 }  // namespace
 
 struct axb_solver {
@@ -403,6 +490,16 @@ struct axb_solver {
         gemm_sq, gemm_diff, scal, tr_metric, tr_rel, sq_part, gsum, BtB;
     DevBuf<unsigned int> zcnt;
     DevBuf<RowRecord> rrec;
+    // CSR operands: A and its Gram G = A·Aᵀ kept sparse (A is never
+    // expanded), B as CSR plus Bᵀ for the per-iteration passes (its dense copy
+    // serves ‖B‖₂ and the residual GEMM only)
+    const axb_matrix* in_A = nullptr;
+    const axb_matrix* in_B = nullptr;
+    bool sp_a = false, sp_b = false;
+    DevBuf<long long> a_rp, g_rp, b_rp, bt_rp;
+    DevBuf<int> a_ci, g_ci, b_ci, bt_ci;
+    DevBuf<double> a_v, g_v, b_v, bt_v;
+    uint64_t nnz_a = 0, nnz_g = 0, nnz_b = 0;
     DevBuf<long long> tr_row, forced;
     // row sharding (§8(e))
     bool sharded = false;
@@ -617,7 +714,16 @@ struct axb_solver {
         // compute stream waits per input, so ‖B‖₂ (and G) overlap the C copy.
         // Each buffer is allocated just before its copy is queued, so mapping the
         // later ones (C, X, R: 35 GB at config 5) overlaps the earlier copies
-        A.alloc(m * p, "A");
+        sp_a = in_A && in_A->kind == 1;
+        sp_b = in_B && in_B->kind == 1;
+        if (sp_a || sp_b) {
+            if (sharded) fail(AXB_CONFIG_ERROR, "row sharding takes dense operands");
+            if (opt.inputs_on_device) fail(AXB_CONFIG_ERROR, "CSR operands are host arrays");
+            if ((sp_a && (in_A->cols > 0x7fffffffull || in_A->rows > 0x7fffffffull)) ||
+                (sp_b && (in_B->cols > 0x7fffffffull || in_B->rows > 0x7fffffffull)))
+                fail(AXB_CAPACITY_ERROR, "CSR dimensions above 2^31");
+        }
+        if (!sp_a) A.alloc(m * p, "A");
         cudaStream_t cs = nullptr;
         ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
         cudaEvent_t evA, evB, evRest;
@@ -635,7 +741,7 @@ struct axb_solver {
                 cudaStreamDestroy(s);
             }
         } guard{cs, evA, evB, evRest};
-        ck(cudaMemcpyAsync(A.p, A_in, sizeof(double) * m * p, kind, cs), "copy A");
+        if (!sp_a) ck(cudaMemcpyAsync(A.p, A_in, sizeof(double) * m * p, kind, cs), "copy A");
         ck(cudaEventRecord(evA, cs), "event");
         B.alloc(q * n, "B");
         ck(cudaMemcpyAsync(B.p, B_in, sizeof(double) * q * n, kind, cs), "copy B");
@@ -674,7 +780,41 @@ struct axb_solver {
         sq_part.alloc(sumsq_parts((long long)std::max({m * n, q * n, p * q, m * p})), "parts");
 
         // a_sq_ = row_sq_norms(A); a_fro_sq_; rbk_cumsum_ (solver.hpp:156-166), sequential
-        launch_row_sq_seq(A.p, (long long)m, (long long)p, a_sq.p, stream);
+        if (sp_a) {
+            // CSR A: RowView::sq_norm over the stored entries, in order (host), and
+            // the CSR arrays the iteration and the residual products read
+            const Csr ah = csr_of(in_A);
+            nnz_a = ah.v.size();
+            std::vector<double> as(m, 0.0);
+            for (uint64_t i = 0; i < m; ++i) {
+                double sacc = 0.0;
+                for (long long e = ah.rp[i]; e < ah.rp[i + 1]; ++e) sacc += ah.v[e] * ah.v[e];
+                as[i] = sacc;
+            }
+            ck(cudaMemcpyAsync(a_sq.p, as.data(), sizeof(double) * m, cudaMemcpyHostToDevice, stream),
+               "a_sq");
+            upload(a_rp, ah.rp, "A row_ptr", stream);
+            upload(a_ci, ah.ci, "A col_idx", stream);
+            upload(a_v, ah.v, "A values", stream);
+            const Csr gh = gram_csr(ah);  // gram_ = gram_mmt(A) (solver.hpp:171)
+            nnz_g = gh.v.size();
+            upload(g_rp, gh.rp, "G row_ptr", stream);
+            upload(g_ci, gh.ci, "G col_idx", stream);
+            upload(g_v, gh.v, "G values", stream);
+        } else {
+            launch_row_sq_seq(A.p, (long long)m, (long long)p, a_sq.p, stream);
+        }
+        if (sp_b) {
+            const Csr bh = csr_of(in_B);
+            nnz_b = bh.v.size();
+            const Csr bt = csr_transpose(bh);
+            upload(b_rp, bh.rp, "B row_ptr", stream);
+            upload(b_ci, bh.ci, "B col_idx", stream);
+            upload(b_v, bh.v, "B values", stream);
+            upload(bt_rp, bt.rp, "B^T row_ptr", stream);
+            upload(bt_ci, bt.ci, "B^T col_idx", stream);
+            upload(bt_v, bt.v, "B^T values", stream);
+        }
         const double* a_all = a_sq.p;
         if (sharded) {  // every rank holds all ‖A_i‖² (BK/RBK selection, ‖A‖²_F, CDF)
             ck(cudaMemcpyAsync(a_sq_g.p + row0, a_sq.p, sizeof(double) * m,
@@ -735,9 +875,9 @@ struct axb_solver {
         const double g_form_s = (double)m_g * (double)m * (double)p / (sharded ? 14.5e12 : 29e12);
         const double g_step_s = 8.0 * (double)m * (double)p / 6.4e12;
         const bool repays = (double)cfg.max_iter * g_step_s >= g_form_s;
-        gram_cached = opt.cache_gram == 1 ||
-                      (opt.cache_gram < 0 && gbytes < 0.45 * (double)free_b &&
-                       gbytes <= 48e9 && repays);
+        gram_cached = !sp_a && (opt.cache_gram == 1 ||
+                                (opt.cache_gram < 0 && gbytes < 0.45 * (double)free_b &&
+                                 gbytes <= 48e9 && repays));
         // one decision for all ranks: forming G gathers A (a collective), and a
         // rank whose free memory differed must not take the other branch
         if (sharded) gram_cached = global_sum(gram_cached ? 1.0 : 0.0) == (double)world;
@@ -769,6 +909,8 @@ struct axb_solver {
             sync("G");  // A_all released at scope end
         } else {
             g.alloc(m, "g");
+            // CSR A: g holds the scattered Gram row, exactly zero elsewhere
+            if (sp_a) ck(cudaMemsetAsync(g.p, 0, sizeof(double) * m, stream), "g");
         }
 
         // r_ = C − (A·X0)·B (solver.hpp:173)
@@ -849,8 +991,10 @@ struct axb_solver {
         // z row chunks depend on it)
         const double persist_ws = 8.0 * ((double)m * n + (double)q * n + 2.0 * p * q + (double)m * p);
         const int persist_force = env_int("AXB_PERSIST", -1);
+        // CSR operands always take the persistent general body (its phases iterate
+        // stored entries); their working set is the touched rows, not m·n
         const bool persist_path =
-            !sharded && (persist_force == 1 || (persist_force < 0 && persist_ws <= 64e6));
+            !sharded && (sp_a || sp_b || persist_force == 1 || (persist_force < 0 && persist_ws <= 64e6));
         {
             // K4b+K5 in small units over several waves, so the tail evens out:
             // X one row per warp (8 rows per CTA), z slabs of 512 columns ×
@@ -934,7 +1078,8 @@ struct axb_solver {
             const int lat_env = env_int("AXB_PERSIST_LAT", 256);
             const int bforce = env_int("AXB_PERSIST_BTB", -1);
             const bool btb_ok = bforce == 1 || (bforce < 0 && 8.0 * (double)n * (double)n <= 16e6);
-            P.persist_lat = (P.persist && (long long)m <= kPersistLatRows && lat_env != 0 && btb_ok)
+            P.persist_lat = (P.persist && !sp_a && !sp_b && (long long)m <= kPersistLatRows &&
+                             lat_env != 0 && btb_ok)
                                 ? (lat_env == 128 ? 128 : 256) : 0;
             // latency-bound: every SM's load parallelism, barrier cost barely grows
             if (P.persist_lat) P.persist_grid = env_int("AXB_PERSIST_GRID", sms);
@@ -962,6 +1107,10 @@ struct axb_solver {
             }
         }
         P.vec2 = (n % 2) == 0;
+        P.a_rp = sp_a ? a_rp.p : nullptr; P.a_ci = a_ci.p; P.a_v = a_v.p;
+        P.g_rp = sp_a ? g_rp.p : nullptr; P.g_ci = g_ci.p; P.g_v = g_v.p;
+        P.b_rp = sp_b ? b_rp.p : nullptr; P.b_ci = b_ci.p; P.b_v = b_v.p;
+        P.bt_rp = sp_b ? bt_rp.p : nullptr; P.bt_ci = bt_ci.p; P.bt_v = bt_v.p;
 
         // DevState: RngStream(cfg.seed) (rng.hpp:20-25), k = 0
         DevState s0{};
@@ -1089,13 +1238,17 @@ struct axb_solver {
 
     // D = C − (A·X)·B into out (store) with optional Σ D² and Σ (Rold − D)² partials
     void exact_residual_into(double* out, double* sq, const double* rold, bool store) {
-        GemmArgs t1{};
-        t1.M = m; t1.N = q; t1.K = p;
-        t1.A = A.p; t1.lda = p;
-        t1.B = X.p; t1.ldb = q;
-        t1.D = T.p; t1.ldd = q;
-        t1.store = 1;
-        launch_gemm(t1, stream);
+        if (sp_a) {  // T = A·X over A's stored entries (matrix.hpp sparse matmul)
+            launch_spmm_csr(a_rp.p, a_ci.p, a_v.p, (long long)m, X.p, (long long)q, T.p, stream);
+        } else {
+            GemmArgs t1{};
+            t1.M = m; t1.N = q; t1.K = p;
+            t1.A = A.p; t1.lda = p;
+            t1.B = X.p; t1.ldb = q;
+            t1.D = T.p; t1.ldd = q;
+            t1.store = 1;
+            launch_gemm(t1, stream);
+        }
         GemmArgs t2{};
         t2.M = m; t2.N = n; t2.K = q;
         t2.A = T.p; t2.lda = q;
@@ -1184,7 +1337,10 @@ struct axb_solver {
     }
     // a persistent-kernel handle whose kernel a multi-system launch runs
     // (axb_solvers_run): only the control block is armed here
-    bool batchable() const { return P.persist && !profiling; }
+    // CSR operands run only on the persistent body (per-kernel profiling is the
+    // dense graph path's measurement hook)
+    bool use_persist() const { return P.persist && (!profiling || sp_a || sp_b); }
+    bool batchable() const { return use_persist(); }
     void batch_launch(uint64_t nb, int run_mode, bool external) {
         launch_ctrl(st.p, k, k + nb, FIN_ITERATION, run_mode, 0, stream);
         ++kernel_launches;
@@ -1192,7 +1348,7 @@ struct axb_solver {
             ++kernel_launches;  // the shared k_persist_batch launch
             return;
         }
-        if (P.persist && !profiling) {
+        if (use_persist()) {
             // the kernel selects at the top of each iteration itself
             const int e = launch_persist(P, stream);
             if (e != 0) ck(static_cast<cudaError_t>(e), "persistent kernel launch");
@@ -1200,7 +1356,7 @@ struct axb_solver {
         } else {
             ensure_selection();
         }
-        if (P.persist && !profiling) {
+        if (use_persist()) {
             // nothing more to enqueue
         } else if (profiling) {
             // 9 events per iteration around every op: [y][y allreduce][z, X][z allgather]
@@ -1362,7 +1518,13 @@ struct axb_solver {
         rollback();
         launch_set_sel(st.p, (long long)i, alpha / a_sq_h[i], stream);
         launch_ctrl(st.p, k, k + 1, FIN_UPDATE_ROW, 0, 1, stream);
-        launch_iteration();
+        if (sp_a || sp_b) {  // one pass of the persistent body on the given row
+            const int e = launch_persist(P, stream);
+            if (e != 0) ck(static_cast<cudaError_t>(e), "persistent kernel launch");
+            ++kernel_launches;
+        } else {
+            launch_iteration();
+        }
         launch_ctrl(st.p, k, k, FIN_ITERATION, 0, 0, stream);
         pull_state();
         sel_valid = false;
@@ -1729,8 +1891,13 @@ int axb_solver_create(const double* A, uint64_t m, uint64_t p, const double* B, 
 }
 
 namespace {
+int expand(const axb_matrix* M, std::vector<double>& out, const char* name, bool fill = true);
+int check_csr(const axb_matrix* M, const char* name) {
+    std::vector<double> none;
+    return expand(M, none, name, false);
+}
 // SparseMatrix::validate (matrix.hpp:94-175) + expansion to row-major dense
-int expand(const axb_matrix* M, std::vector<double>& out, const char* name) {
+int expand(const axb_matrix* M, std::vector<double>& out, const char* name, bool fill) {
     if (M->kind == 0) return AXB_OK;
     if (M->kind != 1) {
         g_create_err = std::string(name) + ": unknown matrix kind";
@@ -1742,7 +1909,7 @@ int expand(const axb_matrix* M, std::vector<double>& out, const char* name) {
         g_create_err = std::string(name) + ": malformed CSR row pointer";
         return AXB_SHAPE_ERROR;
     }
-    out.assign(r * c, 0.0);
+    if (fill) out.assign(r * c, 0.0);
     for (uint64_t i = 0; i < r; ++i) {
         if (M->row_ptr[i + 1] < M->row_ptr[i]) {
             g_create_err = std::string(name) + ": CSR row pointer decreases";
@@ -1759,7 +1926,7 @@ int expand(const axb_matrix* M, std::vector<double>& out, const char* name) {
                 g_create_err = std::string(name) + ": CSR values must be finite and nonzero";
                 return AXB_DOMAIN_ERROR;
             }
-            out[i * c + j] = v;
+            if (fill) out[i * c + j] = v;
         }
     }
     return AXB_OK;
@@ -1784,13 +1951,41 @@ int axb_solver_create_ex(const axb_matrix* A, const axb_matrix* B, const double*
         return AXB_CONFIG_ERROR;
     }
     std::vector<double> Ad, Bd;
-    int st = expand(A, Ad, "A");
+    int st = A->kind == 1 ? check_csr(A, "A") : expand(A, Ad, "A");
     if (st) return st;
-    st = expand(B, Bd, "B");
+    st = expand(B, Bd, "B");  // B's dense copy serves ‖B‖₂ and the residual GEMM
     if (st) return st;
-    return axb_solver_create(A->kind == 1 ? Ad.data() : A->dense, A->rows, A->cols,
-                             B->kind == 1 ? Bd.data() : B->dense, B->rows, B->cols, C, X0, cfg,
-                             opt, out);
+    if (opt && opt->nccl_comm && A->kind == 1) {  // row sharding takes dense operands
+        st = expand(A, Ad, "A");
+        if (st) return st;
+    }
+    const bool sparse = (A->kind == 1 || B->kind == 1) && !(opt && opt->nccl_comm);
+    *out = nullptr;
+    auto s = std::make_unique<axb_solver>();
+    s->m = A->rows; s->p = A->cols; s->q = B->rows; s->n = B->cols;
+    s->cfg = *cfg;
+    if (opt) s->opt = *opt;
+    else axb_options_default(&s->opt);
+    if (sparse) {
+        s->in_A = A;
+        s->in_B = B;
+    }
+    int prev_dev = -1;
+    if (cudaGetDevice(&prev_dev) != cudaSuccess) prev_dev = -1;
+    cudaGetLastError();
+    const double* a_dense = A->kind == 1 ? (Ad.empty() ? nullptr : Ad.data()) : A->dense;
+    const double* b_dense = B->kind == 1 ? Bd.data() : B->dense;
+    st = guarded(s.get(), [&] { s->create(a_dense, b_dense, C, X0); });
+    s->in_A = s->in_B = nullptr;  // borrowed for create() only
+    if (st != AXB_OK) {
+        g_create_err = s->err;
+        s.reset();
+    } else {
+        g_create_err.clear();
+        *out = s.release();
+    }
+    if (prev_dev >= 0) cudaSetDevice(prev_dev);
+    return st;
 }
 
 void axb_solver_destroy(axb_solver* s) {

@@ -225,6 +225,62 @@ class RefLib(_Lib):
         self.get_R = self._f("solver_get_R", None, [C.c_void_p, _dp])
         self.get_r_sq = self._f("solver_get_r_sq", None, [C.c_void_p, _dp])
         self.get_a_sq = self._f("solver_get_a_sq", None, [C.c_void_p, _dp])
+        self.blur_operator = self._f("blur_operator", C.c_uint64,
+                                     [S, S, S, C.c_double, _u64p, _u64p, _dp])
+        self.synthetic_stack = self._f("synthetic_stack", None, [S, S, _dp, _dp])
+        self.sparse_steps_c = self._f(
+            "sparse_steps", C.c_int,
+            [_u64p, _u64p, _dp, S, S, _u64p, _u64p, _dp, _dp, S, S, _dp, _dp,
+             C.POINTER(Config), C.c_uint64, _u64p, _dp, _dp, _dp, C.c_char_p])
+
+    def blur_model(self, h, w, ksize, sigma):
+        """imaging.hpp:93-136 + :276-310: (A as scipy CSR h·w × h·w, X* stack
+        (h·w)×3, A_c 3×3)."""
+        import scipy.sparse as sp
+
+        nnz = self.blur_operator(h, w, ksize, sigma, None, None, None)
+        rp = np.empty(h * w + 1, dtype=np.uint64)
+        ci = np.empty(nnz, dtype=np.uint64)
+        v = np.empty(nnz)
+        self.blur_operator(h, w, ksize, sigma, rp.ctypes.data_as(_u64p), ci.ctypes.data_as(_u64p),
+                           _ptr(v))
+        A = sp.csr_matrix((v, ci.astype(np.int64), rp.astype(np.int64)), shape=(h * w, h * w))
+        X = np.empty((h * w, 3))
+        Ac = np.empty((3, 3))
+        self.synthetic_stack(h, w, _ptr(X), _ptr(Ac))
+        return A, X, Ac
+
+    def sparse_steps(self, A, B, Cm, X0, cfg, k):
+        """Solver<SparseMatrix, BMat> (B CSR or dense), k step() calls:
+        rows, X, r_sq, α."""
+        def parts(M):
+            M = M.tocsr()
+            M.sort_indices()
+            return (np.ascontiguousarray(M.indptr, dtype=np.uint64),
+                    np.ascontiguousarray(M.indices, dtype=np.uint64),
+                    np.ascontiguousarray(M.data, dtype=np.float64))
+
+        a = parts(A)
+        m, p = A.shape
+        q, n = B.shape
+        bcsr = hasattr(B, "indptr")
+        b = parts(B) if bcsr else None
+        Bd = None if bcsr else np.ascontiguousarray(B, dtype=np.float64)
+        Cm = np.ascontiguousarray(Cm, dtype=np.float64)
+        X0 = np.zeros((p, q)) if X0 is None else np.ascontiguousarray(X0, dtype=np.float64)
+        rows = np.empty(max(k, 1), dtype=np.uint64)
+        X = np.empty((p, q))
+        rs = np.empty(m)
+        al = C.c_double()
+        err = C.create_string_buffer(256)
+        u = lambda t: t.ctypes.data_as(_u64p)  # noqa: E731
+        code = self.sparse_steps_c(u(a[0]), u(a[1]), _ptr(a[2]), m, p,
+                                   u(b[0]) if b else None, u(b[1]) if b else None,
+                                   _ptr(b[2]) if b else None, _ptr(Bd), q, n, _ptr(Cm), _ptr(X0),
+                                   C.byref(cfg), k, u(rows), _ptr(X), _ptr(rs), C.byref(al), err)
+        if code:
+            raise OracleError(code, err.value.decode())
+        return rows[:k], X, rs, al.value
 
 
 _oracle = None
