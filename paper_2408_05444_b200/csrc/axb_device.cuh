@@ -148,6 +148,7 @@ struct Params {
     const long long* g_rp; const int* g_ci; const double* g_v;     // G = A·Aᵀ (m×m)
     const long long* b_rp; const int* b_ci; const double* b_v;     // B  q×n
     const long long* bt_rp; const int* bt_ci; const double* bt_v;  // Bᵀ n×q
+    const long long* btb_rp; const int* btb_ci; const double* btb_v;  // BᵀB n×n (latency body)
 };
 
 // ---- launchers (axb_iter.cu) ----

@@ -2329,8 +2329,32 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
     // X_t += (coef·A_it)·y (solver.hpp:272-289), warp per row, rows taken from the
     // LAST warps (the R rows start at the first), so a warp rarely does both;
     // each warp's Σ (X − X_ref)² goes to xpart[gw] (fixed slots, fixed order)
-    auto x_update = [&](const double* Ai, double coef) {
+    auto x_update = [&](const double* Ai, double coef, long long sel) {
         double xacc = 0.0;
+        if (P.a_rp) {
+            // CSR A: rows t ∈ nz(A_i) only, incremental Σ_j (d1² − d0²) per row
+            // (solver.hpp:272-289); the warp's slot holds its delta
+            const long long w = nw - 1 - gw;
+            for (long long e = P.a_rp[sel] + w; e < P.a_rp[sel + 1]; e += nw) {
+                const long long t = P.a_ci[e];
+                const double f = __dmul_rn(coef, P.a_v[e]);
+                double* xr = Xb + t * q;
+                const double* rr = Xrefb ? Xrefb + t * q : nullptr;
+                for (long long k = lane; k < q; k += 32) {
+                    const double x0 = xr[k];
+                    const double x1 = __dadd_rn(x0, __dmul_rn(f, __ldcg(yo + k)));
+                    xr[k] = x1;
+                    if (rr) {
+                        const double rv = rr[k];
+                        const double d0 = __dsub_rn(x0, rv), d1 = __dsub_rn(x1, rv);
+                        xacc += __dsub_rn(__dmul_rn(d1, d1), __dmul_rn(d0, d0));
+                    }
+                }
+            }
+            xacc = warp_sum(xacc);
+            if (lane == 0 && w < p) xpart[w] = xacc;
+            return;
+        }
         for (long long t = nw - 1 - gw; t < p; t += nw) {
             const double f = __dmul_rn(coef, Ai[t]);
             if (f == 0.0 && !Xrefb) continue;  // A_it = 0: X_t unchanged (solver.hpp:272-273)
@@ -2366,11 +2390,13 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
         if (lane == 0 && nw - 1 - gw < p) xpart[nw - 1 - gw] = xacc;
     };
 
+    long long g_prev = -1;  // CSR A: the Gram row scattered into g last (CTA 0)
     for (;;) {
         if (lst.status != ST_RUN || lst.k >= lst.k_limit) break;
         PT_MARK(-1);
         PT_ITER();
-        if (!lst.sel_valid) {  // K3 from shared memory (every CTA, identically)
+        // K3 from shared memory (every CTA, identically); update_row(i) brings its row
+        if (!lst.sel_valid && lst.fin_mode != FIN_UPDATE_ROW) {
             long long row = 0;
             if (tid == 0) sh.err = 0;
             __syncthreads();
@@ -2404,8 +2430,35 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
         const double* Ri = Rb + sel * n;
         const double* Ai = Ab + sel * p;
         // ---- phase A: y = B·R_iᵀ and z = BᵀB·R_iᵀ (dots with R_i), g = A·A_iᵀ ----
-        {
-            const long long nd = q + n;
+        if (P.b_rp) {
+            // CSR B: y over B's rows and z = BᵀB·R_iᵀ over the CSR BᵀB (formed once in
+            // the reference's order, solver.hpp:172, :293), a warp per row
+            for (long long it = gw; it < q + n; it += nw) {
+                const bool isy = it < q;
+                const long long r = isy ? it : it - q;
+                const long long* rp = isy ? P.b_rp : P.btb_rp;
+                const int* ci = isy ? P.b_ci : P.btb_ci;
+                const double* vv = isy ? P.b_v : P.btb_v;
+                double a = 0.0;
+                for (long long e = rp[r] + lane; e < rp[r + 1]; e += 32)
+                    a += __ldg(vv + e) * __ldcg(Ri + __ldg(ci + e));
+                a = warp_sum(a);
+                if (lane == 0) (isy ? yo : zo)[r] = a;
+            }
+        }
+        if (P.g_rp && rank == 0) {
+            // CSR A: scatter G_i into g (CTA 0, after clearing the previous row's
+            // entries); phase C reads g after the barrier
+            if (g_prev >= 0)
+                for (long long e = P.g_rp[g_prev] + tid; e < P.g_rp[g_prev + 1]; e += kT)
+                    go[P.g_ci[e]] = 0.0;
+            __syncthreads();
+            for (long long e = P.g_rp[sel] + tid; e < P.g_rp[sel + 1]; e += kT)
+                go[P.g_ci[e]] = P.g_v[e];
+        }
+        if (P.g_rp) g_prev = sel;
+        if (!P.b_rp || (!Gm && !P.g_rp)) {
+            const long long nd = P.b_rp ? 0 : q + n;
             for (long long it = gw; it < nd; it += 2 * nw) {
                 const long long it1 = it + nw;
                 const double* r0 = it < q ? Bb + it * n : BtB + (it - q) * n;
@@ -2422,7 +2475,7 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
                     }
                 }
             }
-            if (!Gm) {
+            if (!Gm && !P.g_rp) {
                 for (long long it = gw; it < m; it += 2 * nw) {
                     const long long it1 = it + nw;
                     double a0, a1;
@@ -2530,7 +2583,7 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
                     if (lane == 0) rsq[l] = rs;
                 }
             }
-            x_update(Ai, coef);
+            x_update(Ai, coef, sel);
         }
         PT_MARK(4);
         grid.sync();
@@ -2596,6 +2649,10 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
                     pe += sh.scan[w];
                     maxidx_merge(pm, pa, sh.redv[w], sh.redi[w]);
                 }
+                if (P.a_rp) {  // CSR A: the incremental tracker, clamped (solver.hpp:290)
+                    pe = __dadd_rn(lst.err_sq, pe);
+                    if (pe < 0.0) pe = 0.0;
+                }
                 lst.r_fro_sq = ps;
                 lst.max_ratio = pm;
                 lst.argmax = pa;
@@ -2608,6 +2665,9 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
                     lst.err_code = 4;
                     lst.err_k = lst.k;
                     lst.err_val = sqrt(fabs(ps));
+                } else if (lst.fin_mode == FIN_UPDATE_ROW) {  // no k++, trace or stop check
+                    lst.metric = P.stop_kind == 0 ? pe / P.ref_sq : rel;
+                    lst.k_limit = lst.k;
                 } else {
                     const unsigned long long k = lst.k;
                     const double metric = P.stop_kind == 0 ? pe / P.ref_sq : rel;
@@ -2626,6 +2686,10 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
             __syncthreads();
         }
         PT_MARK(5);
+    }
+    if (P.g_rp && rank == 0 && g_prev >= 0) {  // leave g all-zero for the next launch
+        __syncthreads();
+        for (long long e = P.g_rp[g_prev] + tid; e < P.g_rp[g_prev + 1]; e += kT) go[P.g_ci[e]] = 0.0;
     }
     if (rank == 0 && tid == 0) *P.st = lst;
     PT_STORE();

@@ -496,9 +496,9 @@ struct axb_solver {
     const axb_matrix* in_A = nullptr;
     const axb_matrix* in_B = nullptr;
     bool sp_a = false, sp_b = false;
-    DevBuf<long long> a_rp, g_rp, b_rp, bt_rp;
-    DevBuf<int> a_ci, g_ci, b_ci, bt_ci;
-    DevBuf<double> a_v, g_v, b_v, bt_v;
+    DevBuf<long long> a_rp, g_rp, b_rp, bt_rp, btb_rp;
+    DevBuf<int> a_ci, g_ci, b_ci, bt_ci, btb_ci;
+    DevBuf<double> a_v, g_v, b_v, bt_v, btb_v;
     uint64_t nnz_a = 0, nnz_g = 0, nnz_b = 0;
     DevBuf<long long> tr_row, forced;
     // row sharding (§8(e))
@@ -814,6 +814,12 @@ struct axb_solver {
             upload(bt_rp, bt.rp, "B^T row_ptr", stream);
             upload(bt_ci, bt.ci, "B^T col_idx", stream);
             upload(bt_v, bt.v, "B^T values", stream);
+            // btb_ = BᵀB (solver.hpp:172) as the Gram of Bᵀ: entry (c, c') sums
+            // B_jc·B_jc' over ascending j, the reference's matmul order
+            const Csr btb = gram_csr(bt);
+            upload(btb_rp, btb.rp, "B^T B row_ptr", stream);
+            upload(btb_ci, btb.ci, "B^T B col_idx", stream);
+            upload(btb_v, btb.v, "B^T B values", stream);
         }
         const double* a_all = a_sq.p;
         if (sharded) {  // every rank holds all ‖A_i‖² (BK/RBK selection, ‖A‖²_F, CDF)
@@ -1078,8 +1084,8 @@ struct axb_solver {
             const int lat_env = env_int("AXB_PERSIST_LAT", 256);
             const int bforce = env_int("AXB_PERSIST_BTB", -1);
             const bool btb_ok = bforce == 1 || (bforce < 0 && 8.0 * (double)n * (double)n <= 16e6);
-            P.persist_lat = (P.persist && !sp_a && !sp_b && (long long)m <= kPersistLatRows &&
-                             lat_env != 0 && btb_ok)
+            P.persist_lat = (P.persist && (long long)m <= kPersistLatRows && lat_env != 0 &&
+                             (btb_ok || sp_b))
                                 ? (lat_env == 128 ? 128 : 256) : 0;
             // latency-bound: every SM's load parallelism, barrier cost barely grows
             if (P.persist_lat) P.persist_grid = env_int("AXB_PERSIST_GRID", sms);
@@ -1087,7 +1093,7 @@ struct axb_solver {
         // z = BᵀB·R_iᵀ in the latency body (btb_, solver.hpp:172, :293): y and z
         // then share one phase; cached when BᵀB is small (L2-resident)
         P.BtB = nullptr;
-        if (P.persist_lat) {
+        if (P.persist_lat && !sp_b) {  // CSR B: the latency body reads the CSR BᵀB
             {
                 BtB.alloc(n * n, "BtB");
                 DevBuf<double> Bt;
@@ -1111,6 +1117,7 @@ struct axb_solver {
         P.g_rp = sp_a ? g_rp.p : nullptr; P.g_ci = g_ci.p; P.g_v = g_v.p;
         P.b_rp = sp_b ? b_rp.p : nullptr; P.b_ci = b_ci.p; P.b_v = b_v.p;
         P.bt_rp = sp_b ? bt_rp.p : nullptr; P.bt_ci = bt_ci.p; P.bt_v = bt_v.p;
+        P.btb_rp = sp_b ? btb_rp.p : nullptr; P.btb_ci = btb_ci.p; P.btb_v = btb_v.p;
 
         // DevState: RngStream(cfg.seed) (rng.hpp:20-25), k = 0
         DevState s0{};

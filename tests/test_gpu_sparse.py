@@ -41,7 +41,12 @@ def banded(rng, rows, cols, hb):
 @pytest.mark.parametrize("tag,theta", [(O.GRBK, None), (O.RGRBK, 0.3), (O.MWRBK, None),
                                        (O.RBK, None), (O.BK, None)])
 @pytest.mark.parametrize("which", ["A", "B", "AB"])
-def test_csr_operands_match_oracle(axb, orc, tag, theta, which):
+@pytest.mark.parametrize("body", ["latency", "general"])
+def test_csr_operands_match_oracle(axb, orc, tag, theta, which, body, monkeypatch):
+    """Both persistent bodies: the latency body (m ≤ 2048; z = BᵀB·R_iᵀ over the
+    CSR BᵀB) and the general body (z = yᵀB over Bᵀ's rows)."""
+    if body == "general":
+        monkeypatch.setenv("AXB_PERSIST_LAT", "0")
     rng = np.random.default_rng(11)
     m, p, q, n = 300, 240, 40, 160
     Ad, Bd = banded(rng, m, p, 4), banded(rng, q, n, 6)
@@ -98,10 +103,15 @@ def test_csr_x0_update_row_checkpoint_run(axb, orc):
     assert rel(s.R(), so.R()) <= 1e-10
     np.testing.assert_array_equal(s.steps(200), so.steps(200))
     assert s.exact_metric() == pytest.approx(so.exact_metric(), rel=1e-9)
-    # run() to tolerance with refresh checkpoints (±2 iterations: fresh vs running ‖R‖²)
+    # run() to tolerance with refresh checkpoints on a well-conditioned banded A
+    # (±2 iterations: the device's fresh ‖R‖² against the reference's running sum)
+    for i in range(m):
+        Ad[i, int(i * p / m)] += 2.0
+    Cm = (Ad @ Xs) @ Bd
     cfg_o = O.make_config(method=O.MWRBK, stop_kind=O.SOLUTION_RRN, tol=1e-12, reference=Xs,
                           refresh_interval=500, max_iter=200000)
-    rep_o = O.Solver(orc, Ad, Bd, Cm, None, cfg_o).run()
+    rep_o = O.Solver(orc, Ad, Bd, Cm, None, cfg_o).run()[0]
+    assert rep_o.terminated_by == 0
     cfg = axb.SolveConfig(method=axb.Method.mwrbk(), stop=axb.StopRule.solution_rrn(1e-12, Xs),
                           refresh_interval=500, max_iter=200000)
     rep = axb.Solver(sp.csr_matrix(Ad), sp.csr_matrix(Bd), Cm, None, cfg).run()
