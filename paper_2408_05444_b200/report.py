@@ -1,10 +1,15 @@
 """Report and trace formats of the reference, for drop-in CLIs.
 
 Byte-compatible restatements of report.hpp:
-  trace_to_csv          report.hpp:55-61   (RFC-4180, CRLF, %.17g, inf/-inf)
-  solve_report_to_json  report.hpp:102-117 (+ "stop"/"tol" as axbsolve.cpp:208-209)
-  dumps_json            nlohmann::json::dump(2): keys sorted, 2-space indent, "\\n"
-validated by schemas/solve_report.schema.json's required keys and enums.
+  trace_to_csv            report.hpp:55-61   (RFC-4180, CRLF, %.17g, inf/-inf)
+  benchmark_to_csv        report.hpp:63-75
+  restore_metrics_to_csv  report.hpp:88-97
+  solve_report_to_json    report.hpp:102-117 (+ "stop"/"tol" as axbsolve.cpp:208-209)
+  benchmark_to_json       report.hpp:119-136
+  dumps_json              nlohmann::json::dump(2): keys sorted, 2-space indent, UTF-8
+                          unescaped, shortest round-trip doubles, "\\n" appended
+Pinned byte for byte against the reference's own writers (tests/test_report.py,
+fixtures from tests/golden/make_report_golden.cpp).
 """
 from __future__ import annotations
 
@@ -52,6 +57,33 @@ def benchmark_to_csv(rows) -> str:  # report.hpp:63-75
     return out
 
 
+def restore_metrics_to_csv(rows) -> str:  # report.hpp:88-97
+    """rows: objects with image, method, theta (None or float), iterations,
+    psnr_blurred, psnr_restored, ssim_blurred, ssim_restored."""
+    out = _row(["image", "method", "theta", "iterations", "psnr_blurred", "psnr_restored",
+                "ssim_blurred", "ssim_restored"])
+    for r in rows:
+        out += _row([r.image, r.method, "" if r.theta is None else _num(r.theta), str(r.iterations),
+                     _num(r.psnr_blurred), _num(r.psnr_restored), _num(r.ssim_blurred),
+                     _num(r.ssim_restored)])
+    return out
+
+
+def benchmark_to_json(rows) -> list:  # report.hpp:119-136
+    out = []
+    for r in rows:
+        j = {"problem_id": r.problem_id, "method": r.method}
+        if r.theta is not None:
+            j["theta"] = float(r.theta)
+        j.update({"alpha_rule": r.alpha_rule, "trials": int(r.trials), "it_mean": float(r.it_mean),
+                  "it_std": float(r.it_std), "wall_mean_s": float(r.wall_mean_s)})
+        if r.speed_up_vs_rbk is not None:
+            j["speed_up_vs_rbk"] = float(r.speed_up_vs_rbk)
+        j["failures"] = int(r.failures)
+        out.append(j)
+    return out
+
+
 def solve_report_to_json(rep: SolveReport, stop: Optional[str] = None,
                          tol: Optional[float] = None) -> dict:
     j = {
@@ -76,14 +108,16 @@ def solve_report_to_json(rep: SolveReport, stop: Optional[str] = None,
 
 
 def dumps_json(obj) -> str:
-    return json.dumps(obj, indent=2, sort_keys=True) + "\n"
+    """nlohmann::json::dump(2) + "\\n" (axbsolve.cpp:210): std::map key order,
+    UTF-8 left unescaped, doubles shortest round-trip ("1000000.0", "2.5e-07")."""
+    return json.dumps(obj, indent=2, sort_keys=True, ensure_ascii=False) + "\n"
 
 
 def write_solve_outputs(out_dir: str, rep: SolveReport, stop: str, tol: float,
                         trace: bool = True) -> None:
     """report.json (+ trace.csv) as `axbsolve solve` writes them (axbsolve.cpp:205-212)."""
     os.makedirs(out_dir, exist_ok=True)
-    with open(os.path.join(out_dir, "report.json"), "w", newline="") as f:
+    with open(os.path.join(out_dir, "report.json"), "w", newline="", encoding="utf-8") as f:
         f.write(dumps_json(solve_report_to_json(rep, stop, tol)))
     if trace:
         with open(os.path.join(out_dir, "trace.csv"), "w", newline="") as f:
