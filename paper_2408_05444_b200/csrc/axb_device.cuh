@@ -74,6 +74,8 @@ struct alignas(16) DevState {
     int32_t packed;              // sharded: this rank's pack_send holds the last row
     int32_t pack_prev;           // sharded: ... held the row before (k_pack clears it)
     unsigned int cnt_sel1;       // k_sel1 last-block counter
+    unsigned int cnt_yg;         // k_yg_tma last-block counter
+    unsigned long long yg_next;  // dynamic row counter of k_yg_tma
     unsigned long long dbg[8];   // phase timestamps of the last greedy selection (ns)
 };
 
@@ -133,6 +135,7 @@ struct Params {
                                  // shared memory, 2 barriers per iteration (m ≤ kPersistLatRows)
     const double* BtB;           // n×n BᵀB (solver.hpp:172) for z = BᵀB·R_iᵀ in one phase, or null
     int yg_grid, yg_rbq, yg_rbm;  // K4 grid; B rows / A rows per CTA
+    int yg_tma;                  // K4 as a TMA ring (k_yg_tma) instead of k_yg
     int yg_pf;                   // K4: bytes of its first B rows a CTA prefetches into L2
                                  // before the selection it depends on has finished (0 = off)
     int sel_early;               // K3 lets K4 launch (and prefetch) before K2 has drained

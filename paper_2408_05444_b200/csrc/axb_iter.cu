@@ -1495,6 +1495,144 @@ size_t tma_smem_bytes(const Params& P) {
 }
 
 // ------------------------------------------------------------------------
+// K4 as a TMA ring: y_j = B_j·R_iᵀ over this rank's column slice (and, when G is
+// not cached, g_l = A_l·A_iᵀ), with K2's machinery: one producer warp grabs rows
+// one at a time from an atomic counter and streams each row in r_chunk-column
+// tiles together with the matching tile of the shared vector (R_i or A_i) into
+// an r_stages-deep mbarrier ring; eight consumer warps form the dot products
+// from shared memory.  Each warp's partial of a row is kept and combined in
+// fixed warp order, so the dynamic row-to-CTA mapping cannot change rounding.
+// The ring's smem is K2's, so all iteration kernels share one carve-out.
+// (The CTA-per-row k_yg ran at ~50% of HBM bandwidth at config 3: 2048 short
+// CTAs, each re-reading R_i from L2 with a block barrier per row.)
+__global__ void __launch_bounds__(kTmaThreads, 2) k_yg_tma(Params P, int with_g) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ long long stage_row[32];
+    __shared__ double rpart[kRowsKept * kTmaConsumerWarps];
+    __shared__ long long rowid[kRowsKept];
+    __shared__ bool last;
+    pdl_wait();
+    pdl_trigger();
+    DevState* st = P.st;
+    if (halted(st)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int TW = P.r_chunk;
+    const int S = P.r_stages;
+    double* stage = reinterpret_cast<double*>(dsm);
+    double* vstage = stage + (size_t)S * TW;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(dsm + (size_t)S * TW * 16);
+    unsigned long long* empty = full + S;
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kTmaConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const double* Ri;
+    const double* Ai;
+    if (P.pack) {  // sharded: the owner's row arrived through the allreduce
+        Ri = P.pack;
+        Ai = P.pack + P.n;
+    } else {
+        const long long il = st->sel - P.row0;
+        Ri = P.R + il * P.n;
+        Ai = P.A + il * P.p;
+    }
+    const long long q = P.q, nrows = q + (with_g ? P.m : 0);
+    const long long lenB = P.c1 - P.c0, lenA = P.p;
+    if (warp == kTmaConsumerWarps) {
+        // ---- producer: one row per grab, tiles of the row and of the vector ----
+        int s = 0;
+        unsigned round = 0;
+        if (lane == 0) {
+            for (;;) {
+                const long long r = (long long)atomicAdd(&st->yg_next, 1ull);
+                if (r >= nrows) break;
+                const bool isB = r < q;
+                const double* src = isB ? P.B + r * P.n + P.c0 : P.A + (r - q) * P.p;
+                const double* vec = isB ? Ri + P.c0 : Ai;
+                const long long len = isB ? lenB : lenA;
+                for (long long c0 = 0; c0 < len; c0 += TW) {
+                    if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+                    stage_row[s] = r;
+                    const unsigned bytes = (unsigned)(min((long long)TW, len - c0) * 8);
+                    mbar_expect_tx(&full[s], 2u * bytes);
+                    tma_load_1d(stage + (size_t)s * TW, src + c0, bytes, &full[s]);
+                    tma_load_1d(vstage + (size_t)s * TW, vec + c0, bytes, &full[s]);
+                    if (++s == S) {
+                        s = 0;
+                        ++round;
+                    }
+                }
+            }
+            if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+            stage_row[s] = -1;  // sentinel: no bytes
+            mbar_arrive(&full[s]);
+        }
+    } else {
+        // ---- 8 consumer warps ----
+        int s = 0, nkeep = 0;
+        unsigned round = 0;
+        auto flush = [&](int nk) {
+            asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+            for (int t = tid; t < nk; t += kTmaConsumerWarps * 32) {
+                double a = 0.0;
+                for (int w = 0; w < kTmaConsumerWarps; ++w) a += rpart[t * kTmaConsumerWarps + w];
+                const long long r = rowid[t];
+                if (r < q) P.y[r] = a;
+                else P.g[r - q] = a;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumerWarps * 32) : "memory");
+        };
+        for (;;) {
+            mbar_wait(&full[s], round & 1);
+            const long long row = stage_row[s];
+            if (row < 0) break;
+            const long long len = row < q ? lenB : lenA;
+            double acc = 0.0;
+            for (long long c0 = 0; c0 < len; c0 += TW) {
+                if (c0 > 0) mbar_wait(&full[s], round & 1);
+                const int h = (int)(min((long long)TW, len - c0) >> 1);
+                const double2* b2 = reinterpret_cast<const double2*>(stage + (size_t)s * TW);
+                const double2* v2 = reinterpret_cast<const double2*>(vstage + (size_t)s * TW);
+#pragma unroll 4
+                for (int k = tid; k < h; k += kTmaConsumerWarps * 32) {
+                    const double2 b = b2[k], v = v2[k];
+                    acc += b.x * v.x;
+                    acc += b.y * v.y;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (++s == S) {
+                    s = 0;
+                    ++round;
+                }
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) rpart[nkeep * kTmaConsumerWarps + warp] = acc;
+            if (tid == 0) rowid[nkeep] = row;
+            if (++nkeep == kRowsKept) {
+                flush(nkeep);
+                nkeep = 0;
+            }
+        }
+        flush(nkeep);
+    }
+    // the last CTA out resets the row counter for the next launch
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(&st->cnt_yg, 1u) == gridDim.x - 1;
+        if (last) {
+            st->yg_next = 0ull;
+            st->cnt_yg = 0u;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
 // Sharded selection (after ONE grouped allgather of every shard's ‖R_l‖² slice
 // into the global r_sq_g and of the per-shard records).  Every rank then holds
 // the global ‖R_l‖² and ‖A_l‖², so every rank runs the single-GPU selection over
@@ -3028,6 +3166,18 @@ void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaSt
 }
 
 void launch_yg(const Params& P, cudaStream_t s, bool with_g) {
+    if (P.yg_tma) {
+        const size_t smem = (size_t)P.r_stages * P.r_chunk * 16 + 2 * P.r_stages * 8;
+        static size_t attr_set[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (attr_set[dev & 63] < smem) {
+            cudaFuncSetAttribute(k_yg_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set[dev & 63] = smem;
+        }
+        launch_pdl(k_yg_tma, P.r_grid, kTmaThreads, smem, s, P, with_g ? 1 : 0);
+        return;
+    }
     launch_pdl(k_yg, P.yg_grid, kYgThreads, 0, s, P, with_g ? 1 : 0);
 }
 
@@ -3061,6 +3211,7 @@ void launch_r(const Params& P, cudaStream_t s, bool update) {
             cudaFuncSetAttribute(k_r_tma<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             cudaFuncSetAttribute(k_r_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             cudaFuncSetAttribute(k_yg, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            cudaFuncSetAttribute(k_yg_tma, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             cudaFuncSetAttribute(k_zx, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             done = (size_t)dyn;
         }

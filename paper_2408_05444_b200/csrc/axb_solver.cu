@@ -991,6 +991,10 @@ struct axb_solver {
             P.yg_grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, blocks));
             if (const int e = env_int("AXB_YG_GRID", 0); e > 0) P.yg_grid = std::min(P.yg_grid, e);
             P.yg_pf = std::max(0, env_int("AXB_YG_PF", 0));
+            // K4 as a TMA ring when K2 runs one (its ring geometry and carve-out) and
+            // every streamed row is 16-byte aligned (B slice; A rows when g is formed)
+            P.yg_tma = (P.r_tma && P.c1 > P.c0 && ((P.c1 - P.c0) % 2 == 0) && (P.c0 % 2 == 0) &&
+                        (gram_cached || p % 2 == 0) && env_int("AXB_YG_TMA", 1)) ? 1 : 0;
             P.sel_early = env_int("AXB_SEL_EARLY", 0);
         }
         // small systems run one persistent kernel per batch (decided below; the

@@ -397,7 +397,8 @@ def test_concurrent_handles_on_sm_shares(axb, orc):
 @pytest.mark.parametrize("tag", [O.MWRBK, O.GRBK])
 def test_csr_operands_match_dense_and_oracle(axb, orc, tag):
     """solve(const Matrix&…) with CSR A and B (test_solver.cpp:546-561): the CSR
-    run equals the dense run bit for bit and the oracle's rows / X."""
+    run (kept sparse on the device) selects the dense run's and the
+    oracle's rows, X within 1e-10 of both (its sums run over stored entries only)."""
     import scipy.sparse as sp
 
     rng = np.random.default_rng(6501)
@@ -411,7 +412,7 @@ def test_csr_operands_match_dense_and_oracle(axb, orc, tag):
     sc = axb.Solver(sp.csr_matrix(Ad), sp.csr_matrix(Bd), Cm, None, cfg)
     rd, rc, ro = sg.steps(1500), sc.steps(1500), so.steps(1500)
     np.testing.assert_array_equal(rc, rd)
-    np.testing.assert_array_equal(sc.X(), sg.X())
+    assert rel(sc.X(), sg.X()) <= RTOL_X
     np.testing.assert_array_equal(rd, ro)
     assert rel(sc.X(), so.X()) <= RTOL_X
 
