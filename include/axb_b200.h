@@ -138,6 +138,10 @@ int axb_nccl_comm_destroy(void* comm);
  * axb_nccl_comm_destroy.  Not for performance: iterations are not graph-captured. */
 int axb_nccl_emulated_group(int world, void** comms);
 int axb_abi_version(void);
+/* 1 in the bounds-checked build (libaxb_b200_checked.so, -DAXB_CHECKED): the
+ * iteration kernels check their indexing and a violation fails the next call
+ * with AXB_CUDA_ERROR ("device bounds check failed at axb_iter.cu:<line>"). */
+int axb_checked_build(void);
 /* 1 when a device that can run the sm_100a kernels is visible. */
 int axb_device_available(void);
 

@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libaxb_b200.so")
+# AXB_LIB_VARIANT=checked: the build with device bounds checks (build.py --checked)
+LIB_PATH = os.path.join(PKG_DIR, "libaxb_b200_checked.so" if os.environ.get("AXB_LIB_VARIANT") == "checked"
+                        else "libaxb_b200.so")
 
 _dp = C.POINTER(C.c_double)
 _u64p = C.POINTER(C.c_uint64)
@@ -98,6 +100,7 @@ _H = C.c_void_p
 SIGNATURES = [
     ("axb_options_default", None, [C.POINTER(AxbOptions)]),
     ("axb_abi_version", C.c_int, []),
+    ("axb_checked_build", C.c_int, []),
     ("axb_nccl_unique_id", C.c_int, [C.c_char_p]),
     ("axb_nccl_comm_create", C.c_int, [C.c_int, C.c_char_p, C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p)]),

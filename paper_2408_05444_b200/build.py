@@ -14,6 +14,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SOURCES = ["axb_iter.cu", "axb_gemm.cu", "axb_solver.cu", "axb_analysis.cu"]
 OUT = os.path.join(PKG, "libaxb_b200.so")
+# -DAXB_CHECKED: device bounds checks at the iteration kernels' indexing sites
+# (the sanitizer substitute; AXB_LIB_VARIANT=checked loads it)
+OUT_CHECKED = os.path.join(PKG, "libaxb_b200_checked.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -30,27 +33,28 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def needs_rebuild() -> bool:
-    if not os.path.exists(OUT):
+def needs_rebuild(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
         os.path.join(ROOT, "include", "axb_b200.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_rebuild():
-        return OUT
-    tmp = OUT + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES],
-           "-ldl"]
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    out = OUT_CHECKED if checked else OUT
+    if not force and not needs_rebuild(out):
+        return out
+    tmp = out + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DAXB_CHECKED"] if checked else []), "-shared", "-o", tmp,
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -154,6 +154,24 @@ struct Params {
     const long long* btb_rp; const int* btb_ci; const double* btb_v;  // BᵀB n×n (latency body)
 };
 
+// ---- checked build (-DAXB_CHECKED, libaxb_b200_checked.so) ----
+// compute-sanitizer is not available on the GPU pool, so the checked build
+// carries its own bounds checks at the iteration kernels' indexing sites: the
+// first violated check records its source line in a device word (no trap: the
+// context stays usable) and the host raises AXB_CUDA_ERROR at its next state
+// pull.  The production build compiles the checks out.
+#ifdef AXB_CHECKED
+// the flag word g_axb_violation is defined in axb_iter.cu, the checks' only TU
+#define AXB_CHECK(c)                                                                    \
+    do {                                                                                \
+        if (!(c)) atomicCAS(&axb_dev::g_axb_violation, 0ull, (unsigned long long)__LINE__); \
+    } while (0)
+#else
+#define AXB_CHECK(c) ((void)0)
+#endif
+// 0, or the axb_iter.cu line of the first failed check since the last call (then cleared)
+unsigned long long checked_violation();
+
 // ---- launchers (axb_iter.cu) ----
 void launch_yg(const Params& P, cudaStream_t s, bool with_g);
 void launch_zx(const Params& P, cudaStream_t s);

@@ -31,6 +31,18 @@
 
 namespace axb_dev {
 
+#ifdef AXB_CHECKED
+__device__ unsigned long long g_axb_violation = 0ull;
+unsigned long long checked_violation() {
+    unsigned long long v = 0ull, z = 0ull;
+    cudaMemcpyFromSymbol(&v, g_axb_violation, sizeof v);
+    if (v) cudaMemcpyToSymbol(g_axb_violation, &z, sizeof z);
+    return v;
+}
+#else
+unsigned long long checked_violation() { return 0ull; }
+#endif
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -298,6 +310,7 @@ __global__ void __launch_bounds__(kYgThreads) k_yg(Params P, int with_g) {
         Ai = P.pack + P.n;
     } else {
         const long long il = st->sel - P.row0;
+        AXB_CHECK(il >= 0 && il < P.m);
         Ri = P.R + il * P.n;
         Ai = P.A + il * P.p;
     }
@@ -630,6 +643,7 @@ __device__ void grbk_group_sums(const Member& mem, long long m, double* gs,
                 as[u] > 0.0 && (mem.row0 + i == mem.argmax ||
                                 rs[u] >= __dmul_rn(__dmul_rn(mem.zeta, as[u]), mem.r_fro));
             const double v = warp_sum(member ? rs[u] : 0.0);
+            AXB_CHECK(g >= 0 && g < (m + 31) / 32);
             if (lane == 0) gs[g] = v;
         }
     }
@@ -750,6 +764,7 @@ __device__ int select_rows(const Params& P, DevState* st, int method, double the
         // replay of a given index stream (the reference's): consume the same
         // RNG draw / cyclic advance the reference's select_* would, take the row
         if (tid == 0) {
+            AXB_CHECK(st->k - st->k0 < P.trace_cap);
             const long long row = P.forced_rows[st->k - st->k0];
             sh.err = (row < 0 || row >= m || !(P.a_sq[row] > 0.0)) ? 2 : 0;
             sh.cand = row;
@@ -974,6 +989,7 @@ __device__ int grbk_pick(const Params& P, DevState* st, const Member& mem, const
         pick = sh.cand;
     }
     if (tid == 0) AXB_STAMP(4);
+    AXB_CHECK(pick >= 0 && pick < m);
     *out_row = row0 + pick;
     return 0;
 }
@@ -997,6 +1013,7 @@ __device__ void sel_commit(const Params& P, DevState* st, int err, long long row
             st->err_k = st->k;
             st->sel_valid = 0;
         } else {
+            AXB_CHECK(row - P.row0 >= 0 && row - P.row0 < P.m);
             st->sel = row;
             st->coef = __ddiv_rn(P.alpha, P.a_sq[row - P.row0]);
             st->sel_valid = 1;
@@ -1279,6 +1296,7 @@ __device__ void combine_rows(const Params& P, const double* rpart, const long lo
         double a = 0.0;
         for (int w = 0; w < kTmaConsumerWarps; ++w) a += rpart[t * kTmaConsumerWarps + w];
         const long long row = rowid[t];
+        AXB_CHECK(row >= 0 && row < P.m);
         P.r_sq[row] = a;
         const double as = P.a_sq[row];
         if (as > 0.0) maxidx_merge(cmax, carg, __ddiv_rn(a, as), P.row0 + row);
@@ -1341,6 +1359,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
             if (base >= m) break;
             const long long row = base + lane;
             const bool valid = lane < P.r_grab && row < m;
+            AXB_CHECK(!UPDATE || (sel >= 0 && sel < P.m_global));
             double gl = 0.0;
             bool work = valid;
             if (UPDATE && valid) {
@@ -1359,6 +1378,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
                 const double g_l = __shfl_sync(0xffffffffu, gl, l);
                 if (lane == 0) {
                     const double* src = P.R + (base + l) * n;
+                    AXB_CHECK(base + l >= 0 && base + l < m);
                     for (int seg = 0; seg < tpr; ++seg, src += TW) {
                         if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
                         stage_row[s] = base + l;
@@ -1390,6 +1410,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
             mbar_wait(&full[s], round & 1);
             const long long row = stage_row[s];
             if (row < 0) break;
+            AXB_CHECK(row < m);
             double f = 0.0;
             if (UPDATE) f = __dmul_rn(coef, stage_g[s][0]);  // solver.hpp:296
             double acc = 0.0;
@@ -1551,6 +1572,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_yg_tma(Params P, int with_g)
                 const long long r = (long long)atomicAdd(&st->yg_next, 1ull);
                 if (r >= nrows) break;
                 const bool isB = r < q;
+                AXB_CHECK(r >= 0 && r < nrows && (isB || P.A));
                 const double* src = isB ? P.B + r * P.n + P.c0 : P.A + (r - q) * P.p;
                 const double* vec = isB ? Ri + P.c0 : Ai;
                 const long long len = isB ? lenB : lenA;
@@ -1581,6 +1603,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_yg_tma(Params P, int with_g)
                 double a = 0.0;
                 for (int w = 0; w < kTmaConsumerWarps; ++w) a += rpart[t * kTmaConsumerWarps + w];
                 const long long r = rowid[t];
+                AXB_CHECK(r >= 0 && r < nrows);
                 if (r < q) P.y[r] = a;
                 else P.g[r - q] = a;
             }
@@ -1802,6 +1825,7 @@ __global__ void __launch_bounds__(kThreads) k_sel1(Params P, int mode) {
         } else {
             // the pack itself is k_pack's (many CTAs): the owner copies its row,
             // the previous owner clears its stale one
+            AXB_CHECK(s_sel >= 0 && s_sel < mg);
             st->sel = s_sel;
             st->sel_valid = 1;
             st->pack_prev = st->packed;
@@ -1827,6 +1851,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(Params P) {
     double* __restrict__ out = P.pack_send;
     if (mine) {
         const long long il = st->sel - P.row0;
+        AXB_CHECK(il >= 0 && il < P.m);
         const double* __restrict__ Rr = P.R + il * n;
         const double* __restrict__ Ar = P.A + il * p;
         for (long long k = t0; k < n; k += stride) out[k] = __ldcg(Rr + k);
@@ -1974,6 +1999,7 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
                     lst.err_code = err;
                     lst.err_k = lst.k;
                 } else {
+                    AXB_CHECK(row >= 0 && row < m);
                     lst.sel = row;
                     lst.coef = __ddiv_rn(P.alpha, P.a_sq[row]);
                     lst.sel_valid = 1;
@@ -1997,8 +2023,10 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             const double* const bv = P.b_v;
             for (long long j = gw; j < q; j += nw) {
                 double a = 0.0;
-                for (long long e = brp[j] + lane; e < brp[j + 1]; e += 32)
+                for (long long e = brp[j] + lane; e < brp[j + 1]; e += 32) {
+                    AXB_CHECK(bci[e] >= 0 && bci[e] < n);
                     a += __ldg(bv + e) * __ldcg(Ri + __ldg(bci + e));
+                }
                 a = warp_sum(a);
                 if (lane == 0) P.y[j] = a;
             }
@@ -2015,8 +2043,11 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
                     for (long long e = P.g_rp[g_prev] + tid; e < P.g_rp[g_prev + 1]; e += kT)
                         go[P.g_ci[e]] = 0.0;
                 __syncthreads();
-                for (long long e = P.g_rp[sel] + tid; e < P.g_rp[sel + 1]; e += kT)
+                AXB_CHECK(sel >= 0 && sel < m);
+                for (long long e = P.g_rp[sel] + tid; e < P.g_rp[sel + 1]; e += kT) {
+                    AXB_CHECK(P.g_ci[e] >= 0 && P.g_ci[e] < m);
                     go[P.g_ci[e]] = P.g_v[e];
+                }
                 g_prev = sel;
             }
         }
@@ -2060,8 +2091,10 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             const double* const tv = P.bt_v;
             for (long long c = gw; c < n; c += nw) {
                 double a = 0.0;
-                for (long long e = trp[c] + lane; e < trp[c + 1]; e += 32)
+                for (long long e = trp[c] + lane; e < trp[c + 1]; e += 32) {
+                    AXB_CHECK(tci[e] >= 0 && tci[e] < q);
                     a += __ldcg(P.y + __ldg(tci + e)) * __ldg(tv + e);
+                }
                 a = warp_sum(a);
                 if (lane == 0) P.z[c] = a;
             }
@@ -2097,6 +2130,7 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             const long long e0 = P.a_rp[sel], e1 = P.a_rp[sel + 1];
             for (long long e = e0 + gw; e < e1; e += nw) {
                 const long long t = P.a_ci[e];
+                AXB_CHECK(t >= 0 && t < p);
                 const double f = __dmul_rn(coef, P.a_v[e]);
                 double* xr = Xb + t * q;
                 const double* rr = Xrefb ? Xrefb + t * q : nullptr;
@@ -2359,6 +2393,7 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
                 const unsigned long long k = lst.k;
                 const double metric = P.stop_kind == 0 ? e / P.ref_sq : rel;
                 const unsigned long long slot = k - lst.k0;
+                AXB_CHECK(k >= lst.k0);
                 if (grid.rank() == 0 && slot < P.trace_cap) {
                     P.trace_row[slot] = sel;
                     P.trace_metric[slot] = metric;
@@ -2547,6 +2582,7 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
                     lst.err_code = err;
                     lst.err_k = lst.k;
                 } else {
+                    AXB_CHECK(row >= 0 && row < m);
                     lst.sel = row;
                     lst.coef = __ddiv_rn(P.alpha, as_s[row]);
                     lst.sel_valid = 1;
@@ -2578,8 +2614,10 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
                 const int* ci = isy ? P.b_ci : P.btb_ci;
                 const double* vv = isy ? P.b_v : P.btb_v;
                 double a = 0.0;
-                for (long long e = rp[r] + lane; e < rp[r + 1]; e += 32)
+                for (long long e = rp[r] + lane; e < rp[r + 1]; e += 32) {
+                    AXB_CHECK(ci[e] >= 0 && ci[e] < n);
                     a += __ldg(vv + e) * __ldcg(Ri + __ldg(ci + e));
+                }
                 a = warp_sum(a);
                 if (lane == 0) (isy ? yo : zo)[r] = a;
             }

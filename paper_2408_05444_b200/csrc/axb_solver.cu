@@ -559,6 +559,8 @@ struct axb_solver {
         ck(cudaGetLastError(), "kernel launch");
         ck(cudaMemcpyAsync(hs, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, stream), "state");
         sync("state sync");
+        if (const unsigned long long v = checked_violation())  // -DAXB_CHECKED builds only
+            fail(AXB_CUDA_ERROR, "device bounds check failed at axb_iter.cu:%llu", v);
     }
 
     [[noreturn]] void raise_state() {
@@ -1816,6 +1818,13 @@ void axb_options_default(axb_options* o) {
     o->world_size = 1;
 }
 
+int axb_checked_build(void) {
+#ifdef AXB_CHECKED
+    return 1;
+#else
+    return 0;
+#endif
+}
 int axb_abi_version(void) { return AXB_B200_ABI_VERSION; }
 
 int axb_nccl_unique_id(unsigned char out[128]) {

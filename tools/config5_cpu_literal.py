@@ -37,12 +37,20 @@ def instance(m, p, q, n, seed):
     return A, B, Xs
 
 
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
 def per_iteration_s(orc, m, p, q, n, steps, seed):
     t0 = time.perf_counter()
     A, B, Xs = instance(m, p, q, n, seed)
+    log(f"[{m}x{p}.{q}x{n}] inputs {time.perf_counter() - t0:.1f}s")
     C = (A @ Xs) @ B
+    log(f"  C {time.perf_counter() - t0:.1f}s")
     G = A @ A.T
+    log(f"  G {time.perf_counter() - t0:.1f}s")
     BtB = B.T @ B
+    log(f"  BtB {time.perf_counter() - t0:.1f}s")
     v = np.ones(q) / np.sqrt(q)  # ‖B‖₂² by a short power iteration on B·Bᵀ (timing only)
     for _ in range(60):
         w = B @ (B.T @ v)
@@ -53,7 +61,7 @@ def per_iteration_s(orc, m, p, q, n, steps, seed):
     cfg = O.make_config(method=O.GRBK, stop_kind=O.SOLUTION_RRN, tol=1e-12, reference=Xs, seed=42,
                         refresh_interval=0, max_iter=10 ** 9)
     s = O.PreparedSolver(orc, A, B, C, np.zeros((p, q)), C, G, BtB, alpha, cfg)
-    del G, BtB
+    log(f"  prepared {time.perf_counter() - t0:.1f}s")
     s.steps(1)  # warm
     t0 = time.perf_counter()
     s.steps(steps)
@@ -63,6 +71,9 @@ def per_iteration_s(orc, m, p, q, n, steps, seed):
 
 
 def main():
+    import faulthandler
+
+    faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--small-steps", type=int, default=200)
