@@ -263,6 +263,12 @@ int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]);
  * [2] the grouped ‖R_l‖²-slice + record allgather, [3] the global selection
  * kernels (k_sel1 + k_pack), [4] the selected-row allreduce.  Zeros on one GPU. */
 int axb_solver_collective_times(const axb_solver* s, double out_ms[5]);
+/* Diagnostics: time K1 alone.  D = Cin − A·B (Cin may be NULL: D = A·B) on DEVICE
+ * pointers, row-major FP64: A is M×K; B is K×N, or N×K when b_trans (D = A·Bᵀ).
+ * Runs one untimed launch and `reps` timed ones on the current device; *ms is
+ * the average device time of a launch (CUDA events). */
+int axb_debug_dgemm(const double* A, const double* B, const double* Cin, double* D, uint64_t M,
+                    uint64_t N, uint64_t K, int32_t b_trans, int32_t reps, double* ms);
 /* Enable per-kernel CUDA-event timing of K2 inside steps()/run() (adds events to
  * the captured graph; off by default). */
 int axb_solver_set_profiling(axb_solver* s, int32_t on);

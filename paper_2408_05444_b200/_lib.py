@@ -154,6 +154,8 @@ SIGNATURES = [
     ("axb_solver_collective_times", C.c_int, [_H, _dp]),
     ("axb_solver_debug_state", C.c_int, [_H, _u64p]),
     ("axb_solver_set_profiling", C.c_int, [_H, C.c_int32]),
+    ("axb_debug_dgemm", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                  C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, _dp]),
     ("axb_solvers_run", C.c_int,
      [C.POINTER(_H), C.c_uint32, C.POINTER(AxbReport), C.POINTER(_dp), C.POINTER(C.c_int32)]),
     # reference solutions

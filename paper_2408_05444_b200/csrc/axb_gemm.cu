@@ -14,7 +14,10 @@
 // 34.2 / 35.0 vs 31.5 / 32.2 TFLOP/s; cuBLAS DGEMM 35.8 / 36.0.
 // Epilogue fuses the "C −" subtraction, the Σ D² partials (‖R‖²) and the
 // Σ (R_old − D)² partials (the drift guard), so a checkpoint is one pass.
+#include <cuda.h>  // CUtensorMap (types only: the encoder is fetched through cudart)
+
 #include <cmath>
+#include <cstdlib>
 
 #include "axb_device.cuh"
 
@@ -240,6 +243,291 @@ __global__ void __launch_bounds__(THREADS, 2) k_dgemm(GemmArgs g) {
     }
 }
 
+// ------------------------------------------------------------------------
+// k_dgemm_tma — the same 64×128×16 tile fed by TMA instead of cp.async.
+//
+// One producer warp (its lane 0) issues `cp.async.bulk.tensor.2d` (SASS UTMALDG)
+// box loads into a 4-stage ring guarded by full/empty mbarriers; the four
+// consumer warps only wait on a barrier, read DMMA fragments from shared memory
+// and issue `mma.sync.m8n8k4.f64` — no address arithmetic, no cp.async issue
+// slots and no CTA-wide barrier in the main loop.  Out-of-range rows, columns
+// and k are zero-filled by the tensor map's bounds, so there are no predicates.
+//
+// Shared-memory layout: every box row is 16 doubles = 128 B under
+// CU_TENSOR_MAP_SWIZZLE_128B (16-byte chunk c of row r sits at chunk c ^ (r&7)).
+// A dense 128-byte pitch puts every row on bank 0, so which tile row / column a
+// DMMA lane takes is permuted to make each half-warp's 16 fragment loads hit 16
+// distinct 8-byte slots:
+//   * k-contiguous tiles (A; B when b_trans): the lane of fragment row gq reads
+//     tile row 8·i + π(gq), π(g) = 2·(g&3) + (g>>2), so a half-warp's rows have
+//     distinct (r&7)>>1 and its two k-chunks land on 8 distinct swizzled chunks;
+//   * n-contiguous tiles (B as K×N): eight 16×16 boxes side by side; fragment
+//     column j of the 8-wide DMMA tile `ni` reads box ni>>1, column
+//     8·((j>>1)&1) + (j&1) + 2·(j>>2) + 4·(ni&1).
+// The epilogue applies the same permutations to the global row / column of each
+// accumulator, so results are those of the plain mapping.
+constexpr int T_STAGES = 4, T_CONS_WARPS = 4, T_THREADS = (T_CONS_WARPS + 1) * 32;
+constexpr int T_A_BYTES = BM * BK * 8;  // 8 KB
+constexpr int T_B_BYTES = BK * BN * 8;  // 16 KB
+constexpr int T_STAGE_BYTES = T_A_BYTES + T_B_BYTES;
+constexpr size_t T_SMEM = (size_t)T_STAGES * T_STAGE_BYTES + 1024 /*alignment slack*/ + 128;
+
+__device__ __forceinline__ unsigned g_smem_u32(const void* ptr) {
+    return (unsigned)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void g_mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void g_mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void g_mbar_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void g_mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+
+template <bool BTRANS>
+__global__ void __launch_bounds__(T_THREADS, 2)
+k_dgemm_tma(GemmArgs g, const __grid_constant__ CUtensorMap mapA,
+            const __grid_constant__ CUtensorMap mapB) {
+    extern __shared__ unsigned char t_dsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long m0 = (long long)blockIdx.y * BM, n0 = (long long)blockIdx.x * BN;
+    if (g.sym && n0 + BN <= m0) return;  // strictly below the diagonal: mirrored later
+    const int KT = (int)((g.K + BK - 1) / BK);
+    const unsigned base = (g_smem_u32(t_dsm) + 1023u) & ~1023u;
+    const unsigned char* sbase = t_dsm + (base - g_smem_u32(t_dsm));  // the ring, generic view
+    const unsigned bars = base + T_STAGES * T_STAGE_BYTES;  // full[S], empty[S]
+    if (tid == 0) {
+        for (int i = 0; i < T_STAGES; ++i) {
+            g_mbar_init(bars + 8 * i, 1);
+            g_mbar_init(bars + 8 * (T_STAGES + i), T_CONS_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int pg = 2 * (gq & 3) + (gq >> 2);  // π(gq)
+
+    if (warp == T_CONS_WARPS) {
+        if (lane == 0) {
+            for (int kt = 0; kt < KT; ++kt) {
+                const int s = kt % T_STAGES;
+                if (kt >= T_STAGES) g_mbar_wait(bars + 8 * (T_STAGES + s), ((kt / T_STAGES) - 1) & 1);
+                const unsigned full = bars + 8 * s;
+                const unsigned a_s = base + s * T_STAGE_BYTES, b_s = a_s + T_A_BYTES;
+                g_mbar_expect_tx(full, T_STAGE_BYTES);
+                tma_load_2d(a_s, &mapA, kt * BK, (int)m0, full);
+                if (BTRANS) {
+                    tma_load_2d(b_s, &mapB, kt * BK, (int)n0, full);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < BN / 16; ++b)
+                        tma_load_2d(b_s + b * (BK * 128), &mapB, (int)n0 + b * 16, kt * BK, full);
+                }
+            }
+        }
+    } else {
+        // per-lane fragment offsets (bytes) inside a stage
+        unsigned offA[BK / 4];  // k-contiguous tile, row 8·i + π(gq)
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; ++kk)
+            offA[kk] = pg * 128 + (((2 * kk + (tq >> 1)) ^ pg) << 4) + (tq & 1) * 8;
+        // n-contiguous boxes: k row 4kk+tq, chunk cj ^ 2e ^ (4(kk&1)+tq), half j&1
+        const int cj = 4 * ((gq >> 1) & 1) + (gq >> 2);
+        unsigned offB[2][2];  // [kk&1][e]
+#pragma unroll
+        for (int k1 = 0; k1 < 2; ++k1)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                offB[k1][e] = tq * 128 + (((cj ^ (2 * e) ^ (4 * k1 + tq)) & 7) << 4) + (gq & 1) * 8;
+        for (int kt = 0; kt < KT; ++kt) {
+            const int s = kt % T_STAGES;
+            g_mbar_wait(bars + 8 * s, (kt / T_STAGES) & 1);
+            const unsigned char* a_s = sbase + s * T_STAGE_BYTES + wm * (FM * 8 * 128);
+            const unsigned char* b_s = sbase + s * T_STAGE_BYTES + T_A_BYTES;
+            auto lds64 = [](const unsigned char* p) { return *reinterpret_cast<const double*>(p); };
+#pragma unroll
+            for (int kk = 0; kk < BK / 4; ++kk) {
+                double af[FM], bf[FN];
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi) af[mi] = lds64(a_s + mi * 1024 + offA[kk]);
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) {
+                    if (BTRANS)
+                        bf[ni] = lds64(b_s + (wn * FN + ni) * 1024 + offA[kk]);
+                    else
+                        bf[ni] = lds64(b_s + (wn * (FN / 2) + (ni >> 1)) * (BK * 128) + kk * 512 +
+                                       offB[kk & 1][ni & 1]);
+                }
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < FN; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+            }
+            __syncwarp();
+            if (lane == 0) g_mbar_arrive(bars + 8 * (T_STAGES + s));
+        }
+    }
+
+    // ---- fused epilogue (consumer warps hold the accumulators) ----
+    double sq = 0.0, df = 0.0;
+    if (warp < T_CONS_WARPS) {
+        const bool v2 = !BTRANS && ((g.ldd | g.ldc | g.ldr) & 1) == 0;
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi) {
+            const long long r = m0 + wm * FM * 8 + mi * 8 + pg;
+            if (r >= g.M) continue;
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) {
+                long long c, c1;
+                if (BTRANS) {
+                    const int j0 = 2 * tq, j1 = 2 * tq + 1;
+                    c = n0 + (wn * FN + ni) * 8 + 2 * (j0 & 3) + (j0 >> 2);
+                    c1 = n0 + (wn * FN + ni) * 8 + 2 * (j1 & 3) + (j1 >> 2);
+                } else {
+                    c = n0 + (wn * (FN / 2) + (ni >> 1)) * 16 + 8 * (tq & 1) + 2 * (tq >> 1) +
+                        4 * (ni & 1);
+                    c1 = c + 1;
+                }
+                const bool one = c < g.N, two = c1 < g.N;
+                if (!one && !two) continue;
+                double o0 = acc[mi][ni][0], o1 = acc[mi][ni][1];
+                if (g.Cin) {
+                    if (one && two && v2) {
+                        const double2 cc = *reinterpret_cast<const double2*>(g.Cin + r * g.ldc + c);
+                        o0 = cc.x - o0;
+                        o1 = cc.y - o1;
+                    } else {
+                        if (one) o0 = g.Cin[r * g.ldc + c] - o0;
+                        if (two) o1 = g.Cin[r * g.ldc + c1] - o1;
+                    }
+                }
+                sq += (one ? o0 * o0 : 0.0) + (two ? o1 * o1 : 0.0);
+                if (g.Rold) {
+                    const double d0 = one ? g.Rold[r * g.ldr + c] - o0 : 0.0;
+                    const double d1 = two ? g.Rold[r * g.ldr + c1] - o1 : 0.0;
+                    df += d0 * d0 + d1 * d1;
+                }
+                if (g.store) {
+                    if (one && two && v2) {
+                        *reinterpret_cast<double2*>(g.D + r * g.ldd + c) = make_double2(o0, o1);
+                    } else {
+                        if (one) g.D[r * g.ldd + c] = o0;
+                        if (two) g.D[r * g.ldd + c1] = o1;
+                    }
+                }
+            }
+        }
+    }
+    if (g.sq_part || g.diff_part) {
+        __shared__ double red[2][T_CONS_WARPS];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            df += __shfl_xor_sync(0xffffffffu, df, o);
+        }
+        if (lane == 0 && warp < T_CONS_WARPS) {
+            red[0][warp] = sq;
+            red[1][warp] = df;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, b = 0.0;
+            for (int w = 0; w < T_CONS_WARPS; ++w) {
+                a += red[0][w];
+                b += red[1][w];
+            }
+            const long long bid = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+            if (g.sq_part) g.sq_part[bid] = a;
+            if (g.diff_part) g.diff_part[bid] = b;
+        }
+    }
+}
+
+// cuTensorMapEncodeTiled, fetched through the runtime (no libcuda link dependency)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// row-major FP64 matrix rows×cols (leading dimension ld) as a 2-D map with a
+// box of box_rows × 16 columns (128 B), 128-byte swizzle, zero fill out of range
+bool make_map(CUtensorMap* map, const double* ptr, long long rows, long long cols, long long ld,
+              unsigned box_rows) {
+    EncodeTiledFn enc = encode_tiled_fn();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    const cuuint32_t box[2] = {16, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA needs 16-byte aligned bases and row pitches and 32-bit box coordinates
+bool tma_eligible(const GemmArgs& g) {
+    const char* e = getenv("AXB_GEMM_TMA");  // read per launch: tests toggle it
+    if (e && atoi(e) == 0) return false;
+    const long long lim = 1ll << 31;
+    return ((g.lda | g.ldb) & 1) == 0 &&
+           ((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B)) & 15) == 0 &&
+           g.M + BM < lim && g.N + BN < lim && g.K + BK < lim;
+}
+
+template <bool BT>
+bool launch_tma(const GemmArgs& g, cudaStream_t s) {
+    CUtensorMap mapA, mapB;
+    if (!make_map(&mapA, g.A, g.M, g.K, g.lda, BM)) return false;
+    if (BT) {
+        if (!make_map(&mapB, g.B, g.N, g.K, g.ldb, BN)) return false;
+    } else {
+        if (!make_map(&mapB, g.B, g.K, g.N, g.ldb, BK)) return false;
+    }
+    static bool attr[64] = {};  // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+        cudaFuncSetAttribute(k_dgemm_tma<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T_SMEM);
+        if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
+    k_dgemm_tma<BT><<<grid, T_THREADS, T_SMEM, s>>>(g, mapA, mapB);
+    return true;
+}
+
 __global__ void __launch_bounds__(1024) k_reduce_parts(const double* part, long long n,
                                                        double* out) {
     __shared__ double red[32];
@@ -296,6 +584,7 @@ int gemm_num_ctas(long long M, long long N) {
 
 void launch_gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0) return;
+    if (tma_eligible(g) && (g.b_trans ? launch_tma<true>(g, s) : launch_tma<false>(g, s))) return;
     const bool v16 = ((g.lda | g.ldb) & 1) == 0 && ((reinterpret_cast<uintptr_t>(g.A) |
                                                        reinterpret_cast<uintptr_t>(g.B)) & 15) == 0;
     if (g.b_trans) {

@@ -2302,6 +2302,38 @@ int axb_solver_debug_state(axb_solver* s, uint64_t out[8]) {
         for (int i = 0; i < 8; ++i) out[i] = s->hs->dbg[i];
     });
 }
+int axb_debug_dgemm(const double* A, const double* B, const double* Cin, double* D, uint64_t M,
+                    uint64_t N, uint64_t K, int32_t b_trans, int32_t reps, double* ms) {
+    if (!A || !B || !D || !ms || reps <= 0) return AXB_CONFIG_ERROR;
+    axb_dev::GemmArgs g{};
+    g.M = (long long)M;
+    g.N = (long long)N;
+    g.K = (long long)K;
+    g.A = A;
+    g.lda = (long long)K;
+    g.B = B;
+    g.ldb = (long long)(b_trans ? K : N);
+    g.b_trans = b_trans;
+    g.D = D;
+    g.ldd = (long long)N;
+    g.Cin = Cin;
+    g.ldc = (long long)N;
+    g.store = 1;
+    cudaEvent_t e0, e1;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+        return AXB_CUDA_ERROR;
+    axb_dev::launch_gemm(g, 0);
+    cudaEventRecord(e0, 0);
+    for (int r = 0; r < reps; ++r) axb_dev::launch_gemm(g, 0);
+    cudaEventRecord(e1, 0);
+    const cudaError_t err = cudaEventSynchronize(e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = (double)t / reps;
+    return err == cudaSuccess && cudaGetLastError() == cudaSuccess ? AXB_OK : AXB_CUDA_ERROR;
+}
 int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]) {
     const double nl = s->k2_launches ? (double)s->k2_launches : 1.0;
     out_ms[0] = s->yg_ms / nl;

@@ -1,0 +1,66 @@
+"""K1 (DMMA GEMM) — the TMA-fed kernel against the cp.async one and numpy.
+
+Both kernels accumulate every output element over k in the same order (DMMA
+k-steps of 4, ascending), so the residual R0 = C − (A·X0)·B and the cached Gram
+G = A·Aᵀ must agree BITWISE between them; numpy (a different summation order)
+agrees to rounding.  Shapes cover partial tiles in M, N and K, and operands whose
+pitch is odd (no 16-byte alignment: the cp.async kernel is the only path).
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (64, 16, 16, 128),      # exactly one tile
+    (130, 50, 34, 150),     # partial tiles everywhere
+    (500, 100, 80, 400),    # config 1
+    (257, 36, 130, 1026),   # several k tiles, ragged N
+    (96, 24, 18, 272),      # K = 18: partial last k tile (zero-filled by the map)
+    (70, 7, 9, 33),         # odd pitches: falls back to the cp.async kernel
+]
+
+
+def _residual(axb, A, B, C, X0, tma, cache_gram=-1, steps=0):
+    os.environ["AXB_GEMM_TMA"] = "1" if tma else "0"
+    try:
+        cfg = axb.SolveConfig(method=axb.Method.mwrbk(), max_iter=10 ** 6, refresh_interval=0)
+        s = axb.Solver(A, B, C, X0, cfg, axb.Options(cache_gram=cache_gram))
+        rows = s.steps(steps) if steps else None
+        return s.R(), s.X(), rows, s.exact_residual_rel()
+    finally:
+        os.environ.pop("AXB_GEMM_TMA", None)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_r0_tma_equals_cp_async_bitwise(axb, shape):
+    m, p, q, n = shape
+    rng = np.random.default_rng(sum(shape))
+    A, B = rng.standard_normal((m, p)), rng.standard_normal((q, n))
+    X0, C = rng.standard_normal((p, q)), rng.standard_normal((m, n))
+    R1, _, _, e1 = _residual(axb, A, B, C, X0, True)
+    R0, _, _, e0 = _residual(axb, A, B, C, X0, False)
+    assert np.array_equal(R1, R0), "TMA-fed and cp.async-fed DMMA kernels differ"
+    assert e1 == e0
+    Rn = C - (A @ X0) @ B
+    assert np.linalg.norm(R1 - Rn) <= 1e-13 * np.linalg.norm(Rn)
+
+
+@pytest.mark.parametrize("shape", [(130, 50, 34, 150), (300, 64, 48, 256)])
+def test_gram_tma_equals_cp_async(axb, shape):
+    """G = A·Aᵀ through the b_trans tile (k-contiguous boxes for both operands)."""
+    m, p, q, n = shape
+    rng = np.random.default_rng(7 + sum(shape))
+    A, B = rng.standard_normal((m, p)), rng.standard_normal((q, n))
+    Xs = rng.standard_normal((p, q))
+    C = (A @ Xs) @ B
+    _, X1, rows1, _ = _residual(axb, A, B, C, None, True, cache_gram=1, steps=60)
+    _, X0, rows0, _ = _residual(axb, A, B, C, None, False, cache_gram=1, steps=60)
+    assert np.array_equal(rows1, rows0)
+    assert np.array_equal(X1, X0)
+    # and against g = A·A_iᵀ formed per step (no cached Gram at all)
+    _, Xg, rowsg, _ = _residual(axb, A, B, C, None, True, cache_gram=0, steps=60)
+    assert np.array_equal(rows1, rowsg)
+    assert np.linalg.norm(X1 - Xg) <= 1e-12 * np.linalg.norm(Xg)
