@@ -270,6 +270,8 @@ constexpr int T_STAGES = 4, T_CONS_WARPS = 4, T_THREADS = (T_CONS_WARPS + 1) * 3
 constexpr int T_A_BYTES = BM * BK * 8;  // 8 KB
 constexpr int T_B_BYTES = BK * BN * 8;  // 16 KB
 constexpr int T_STAGE_BYTES = T_A_BYTES + T_B_BYTES;
+constexpr int T_C_STAGES = 3;  // epilogue stages holding the Cin tile (3 + 3 + 2 boxes of 8 KB)
+static_assert(3 * T_A_BYTES == T_STAGE_BYTES && T_C_STAGES * 3 >= BN / 16 && T_C_STAGES <= T_STAGES, "Cin staging");
 constexpr size_t T_SMEM = (size_t)T_STAGES * T_STAGE_BYTES + 1024 /*alignment slack*/ + 128;
 
 __device__ __forceinline__ unsigned g_smem_u32(const void* ptr) {
@@ -299,10 +301,16 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
         ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar) : "memory");
 }
 
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool getenv_no_prefetch(const GemmArgs& g) { return g.no_pf != 0; }
+
 template <bool BTRANS>
 __global__ void __launch_bounds__(T_THREADS, 2)
 k_dgemm_tma(GemmArgs g, const __grid_constant__ CUtensorMap mapA,
-            const __grid_constant__ CUtensorMap mapB) {
+            const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapC,
+            int c_tma) {
     extern __shared__ unsigned char t_dsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long m0 = (long long)blockIdx.y * BM, n0 = (long long)blockIdx.x * BN;
@@ -330,7 +338,19 @@ k_dgemm_tma(GemmArgs g, const __grid_constant__ CUtensorMap mapA,
     const int pg = 2 * (gq & 3) + (gq >> 2);  // π(gq)
 
     if (warp == T_CONS_WARPS) {
-        if (lane == 0) {
+        if (lane != 0) {
+            // idle producer lanes: bulk-prefetch the tile's epilogue operands (Cin,
+            // Rold) into L2 so the epilogue's loads are L2 hits
+            const bool pf_c = !c_tma && g.Cin && (g.ldc & 1) == 0 &&
+                              (reinterpret_cast<uintptr_t>(g.Cin) & 15) == 0;
+            const bool pf_r = g.Rold && (g.ldr & 1) == 0 && (reinterpret_cast<uintptr_t>(g.Rold) & 15) == 0;
+            const long long w = (g.N - n0 < BN ? g.N - n0 : BN) & ~1ll;
+            if (w > 0 && (pf_c || pf_r) && !getenv_no_prefetch(g))
+                for (int r = lane - 1; r < BM && m0 + r < g.M; r += 31) {
+                    if (pf_c) l2_prefetch_bulk(g.Cin + (m0 + r) * g.ldc + n0, (unsigned)(w * 8));
+                    if (pf_r) l2_prefetch_bulk(g.Rold + (m0 + r) * g.ldr + n0, (unsigned)(w * 8));
+                }
+        } else {
             for (int kt = 0; kt < KT; ++kt) {
                 const int s = kt % T_STAGES;
                 if (kt >= T_STAGES) g_mbar_wait(bars + 8 * (T_STAGES + s), ((kt / T_STAGES) - 1) & 1);
@@ -344,6 +364,22 @@ k_dgemm_tma(GemmArgs g, const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                     for (int b = 0; b < BN / 16; ++b)
                         tma_load_2d(b_s + b * (BK * 128), &mapB, (int)n0 + b * 16, kt * BK, full);
+                }
+            }
+            if (c_tma) {
+                // the Cin tile follows the k-tiles through the ring: eight 64×16 boxes
+                // (the A-tile geometry), three per stage, in flight while the
+                // consumers finish the last k-tiles
+#pragma unroll
+                for (int u = 0; u < T_C_STAGES; ++u) {
+                    const int j = KT + u, s = j % T_STAGES;
+                    if (j >= T_STAGES) g_mbar_wait(bars + 8 * (T_STAGES + s), ((j / T_STAGES) - 1) & 1);
+                    const unsigned full = bars + 8 * s;
+                    const int nb = (BN / 16 - 3 * u) < 3 ? (BN / 16 - 3 * u) : 3;
+                    g_mbar_expect_tx(full, nb * T_A_BYTES);
+                    for (int b = 0; b < nb; ++b)
+                        tma_load_2d(base + s * T_STAGE_BYTES + b * T_A_BYTES, &mapC,
+                                    (int)n0 + (3 * u + b) * 16, (int)m0, full);
                 }
             }
         }
@@ -394,6 +430,13 @@ k_dgemm_tma(GemmArgs g, const __grid_constant__ CUtensorMap mapA,
     double sq = 0.0, df = 0.0;
     if (warp < T_CONS_WARPS) {
         const bool v2 = !BTRANS && ((g.ldd | g.ldc | g.ldr) & 1) == 0;
+        if (c_tma) {
+#pragma unroll
+            for (int u = 0; u < T_C_STAGES; ++u) {
+                const int j = KT + u;
+                g_mbar_wait(bars + 8 * (j % T_STAGES), (j / T_STAGES) & 1);
+            }
+        }
 #pragma unroll
         for (int mi = 0; mi < FM; ++mi) {
             const long long r = m0 + wm * FM * 8 + mi * 8 + pg;
@@ -414,7 +457,17 @@ k_dgemm_tma(GemmArgs g, const __grid_constant__ CUtensorMap mapA,
                 if (!one && !two) continue;
                 double o0 = acc[mi][ni][0], o1 = acc[mi][ni][1];
                 if (g.Cin) {
-                    if (one && two && v2) {
+                    if (!BTRANS && c_tma) {
+                        // box b of the Cin tile, row 8·i + π(gq), 16-byte chunk under the 128 B swizzle
+                        const int b = wn * (FN / 2) + (ni >> 1), j = KT + b / 3;
+                        const int rl = wm * FM * 8 + mi * 8 + pg;
+                        const int ch = 4 * (tq & 1) + (tq >> 1) + 2 * (ni & 1);
+                        const double2 cc = *reinterpret_cast<const double2*>(
+                            sbase + (j % T_STAGES) * T_STAGE_BYTES + (b % 3) * T_A_BYTES + rl * 128 +
+                            ((ch ^ pg) << 4));
+                        o0 = cc.x - o0;
+                        o1 = cc.y - o1;
+                    } else if (one && two && v2) {
                         const double2 cc = *reinterpret_cast<const double2*>(g.Cin + r * g.ldc + c);
                         o0 = cc.x - o0;
                         o1 = cc.y - o1;
@@ -508,9 +561,19 @@ bool tma_eligible(const GemmArgs& g) {
 }
 
 template <bool BT>
-bool launch_tma(const GemmArgs& g, cudaStream_t s) {
-    CUtensorMap mapA, mapB;
+bool launch_tma(const GemmArgs& g0, cudaStream_t s) {
+    GemmArgs g = g0;
+    if (const char* e = getenv("AXB_GEMM_PF")) g.no_pf = atoi(e) == 0;
+    CUtensorMap mapA, mapB, mapC;
     if (!make_map(&mapA, g.A, g.M, g.K, g.lda, BM)) return false;
+    // Cin through the ring when its rows are 16-byte aligned (else global loads)
+    int c_tma = !BT && g.Cin && (g.ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(g.Cin) & 15) == 0;
+    if (const char* e = getenv("AXB_GEMM_CTMA")) c_tma = c_tma && atoi(e) != 0;
+    if (c_tma) {
+        if (!make_map(&mapC, g.Cin, g.M, g.N, g.ldc, BM)) return false;
+    } else {
+        mapC = mapA;
+    }
     if (BT) {
         if (!make_map(&mapB, g.B, g.N, g.K, g.ldb, BN)) return false;
     } else {
@@ -524,7 +587,7 @@ bool launch_tma(const GemmArgs& g, cudaStream_t s) {
         if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
-    k_dgemm_tma<BT><<<grid, T_THREADS, T_SMEM, s>>>(g, mapA, mapB);
+    k_dgemm_tma<BT><<<grid, T_THREADS, T_SMEM, s>>>(g, mapA, mapB, mapC, c_tma);
     return true;
 }
 
