@@ -263,6 +263,11 @@ int axb_solver_kernel_times(const axb_solver* s, double out_ms[3]);
  * [2] the grouped ‖R_l‖²-slice + record allgather, [3] the global selection
  * kernels (k_sel1 + k_pack), [4] the selected-row allreduce.  Zeros on one GPU. */
 int axb_solver_collective_times(const axb_solver* s, double out_ms[5]);
+/* Diagnostics: the graph path's in-pipeline kernel timeline, a ring of 64
+ * iterations × {K4, K4b+K5, K2, K3} × {earliest CTA start, latest CTA end} in
+ * device-clock ns (out[64*8]); `reset` re-arms it.  Returns 1 when the library
+ * was built with -DAXB_TRACE_TIMELINE, else 0 (out zeroed). */
+int axb_debug_timeline(uint64_t out[512], int32_t reset);
 /* Diagnostics: time K1 alone.  D = Cin − A·B (Cin may be NULL: D = A·B) on DEVICE
  * pointers, row-major FP64: A is M×K; B is K×N, or N×K when b_trans (D = A·Bᵀ).
  * Runs one untimed launch and `reps` timed ones on the current device; *ms is

@@ -237,6 +237,7 @@ struct GemmArgs {
     int sym;  // D = A·Aᵀ: compute only tiles on/above the diagonal (mirror with launch_mirror_lower)
     int no_pf;  // k_dgemm_tma: skip the L2 prefetch of the epilogue operands (AXB_GEMM_PF=0)
 };
+int timeline_read(unsigned long long* out, int reset);
 int gemm_num_ctas(long long M, long long N);
 void launch_gemm(const GemmArgs& g, cudaStream_t s);
 void launch_reduce_parts(const double* part, long long n, double* out, cudaStream_t s);

@@ -60,15 +60,34 @@ __device__ __forceinline__ void pdl_trigger() {
 
 // phase timestamps of the greedy selection into DevState::dbg (build with
 // -DAXB_TRACE_SELECT; read with axb_solver_debug_state, tools/sel_timing.py)
-#ifdef AXB_TRACE_SELECT
+#if defined(AXB_TRACE_SELECT) || defined(AXB_TRACE_TIMELINE)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#endif
+#ifdef AXB_TRACE_SELECT
 #define AXB_STAMP(slot) (st->dbg[slot] = gtime())
 #else
 #define AXB_STAMP(slot) ((void)0)
+#endif
+
+// In-pipeline timeline of the graph path's iteration kernels (build with
+// -DAXB_TRACE_TIMELINE; read with axb_debug_timeline, tools/timeline.py): per
+// iteration (ring of 64) the earliest CTA start after its dependency wait and the
+// latest CTA end of K4 (0), K4b+K5 (1), K2 (2) and K3 k_sel_greedy (3).  Device
+// clock (globaltimer), so it shows what events cannot: the programmatic overlap.
+#ifdef AXB_TRACE_TIMELINE
+__device__ unsigned long long g_axb_tl[64][8];
+#define TL_BEGIN(id, back)                                              \
+    const unsigned tl_slot = (unsigned)((P.st->k - (back)) & 63u);       \
+    if (threadIdx.x == 0) atomicMin(&g_axb_tl[tl_slot][2 * (id)], gtime())
+#define TL_END(id) \
+    do { if (threadIdx.x == 0) atomicMax(&g_axb_tl[tl_slot][2 * (id) + 1], gtime()); } while (0)
+#else
+#define TL_BEGIN(id, back) ((void)0)
+#define TL_END(id) ((void)0)
 #endif
 
 __device__ __forceinline__ bool halted(const DevState* st) {
@@ -409,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_zx(Params P) {
     pdl_trigger();
     DevState* st = P.st;
     if (halted(st)) return;
+    TL_BEGIN(1, 0);
     const int tid = threadIdx.x;
     // CTAs [0, x_ctas) update X (the larger units, dispatched first), the rest
     // form z — small slab × row-chunk units that even out the tail
@@ -463,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_zx(Params P) {
         if (P.z_nj == 1) {
             if (c < cend) P.z[c] = a0;
             if (c + 1 < cend) P.z[c + 1] = a1;
+            TL_END(1);
             return;
         }
         double* zp = P.zpart + (long long)jc * P.n;
@@ -472,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_zx(Params P) {
         __syncthreads();
         if (tid == 0) last = atomicAdd(P.zcnt + slab, 1u) == (unsigned)(P.z_nj - 1);
         __syncthreads();
+        TL_END(1);
         if (!last) return;
         __threadfence();
         for (long long cc = c; cc < c + 2 && cc < cend; ++cc) {
@@ -480,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_zx(Params P) {
             P.z[cc] = s;
         }
         if (tid == 0) P.zcnt[slab] = 0u;
+        TL_END(1);
         return;
     }
     // ---- X update (solver.hpp:272-290): one warp per row t of X ----
@@ -547,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_zx(Params P) {
             }
         }
     }
+    TL_END(1);
     if (!track) return;
     acc = block_sum(acc, red);
     if (tid == 0) {
@@ -564,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_zx(Params P) {
         st->err_sq = s;
         st->cnt_x = 0u;
     }
+    TL_END(1);
 }
 
 // ------------------------------------------------------------------------
@@ -1317,6 +1342,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
     pdl_trigger();
     DevState* st = P.st;
     if (UPDATE && halted(st)) return;
+    TL_BEGIN(2, 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long m = P.m, n = P.n;
     const int TW = P.r_chunk;
@@ -1465,6 +1491,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
         last = atomicAdd(&st->cnt_r, 1u) == gridDim.x - 1;
     }
     __syncthreads();
+    TL_END(2);
     if (!last) return;
     __threadfence();
     double sum = 0.0, mx = -INFINITY;
@@ -1509,6 +1536,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_r_tma(Params P) {
     }
     // the TMA ring is idle now: reuse it as selection scratch
     finalize<UPDATE>(P, st, sum, mx, ax, stage, (long long)S * TW);
+    TL_END(2);
 }
 
 size_t tma_smem_bytes(const Params& P) {
@@ -1536,6 +1564,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_yg_tma(Params P, int with_g)
     pdl_trigger();
     DevState* st = P.st;
     if (halted(st)) return;
+    TL_BEGIN(0, 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int TW = P.r_chunk;
     const int S = P.r_stages;
@@ -1645,6 +1674,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_yg_tma(Params P, int with_g)
     }
     // the last CTA out resets the row counter for the next launch
     __syncthreads();
+    TL_END(0);
     if (tid == 0) {
         __threadfence();
         last = atomicAdd(&st->cnt_yg, 1u) == gridDim.x - 1;
@@ -1890,6 +1920,7 @@ __global__ void __launch_bounds__(kThreads) k_sel_greedy(Params P) {
     pdl_trigger();
     DevState* st = P.st;
     if (!st->sel_pending) return;
+    TL_BEGIN(3, 1);
     const long long m = P.m, ng = (m + 31) / 32;
     const bool live = st->r_fro_sq > 0.0;
     if (live) {
@@ -1903,6 +1934,7 @@ __global__ void __launch_bounds__(kThreads) k_sel_greedy(Params P) {
         last = atomicAdd(&st->cnt_sel, 1u) == gridDim.x - 1;
     }
     __syncthreads();
+    TL_END(3);
     if (!last) return;
     __threadfence();
     sel_snapshot(st, sh);
@@ -1918,6 +1950,7 @@ __global__ void __launch_bounds__(kThreads) k_sel_greedy(Params P) {
         st->sel_pending = 0;
         st->cnt_sel = 0u;
     }
+    TL_END(3);
 }
 
 constexpr int kPersistThreads = 256;
@@ -3183,6 +3216,28 @@ __global__ void k_cumsum_seq(const double* a_sq, long long m, double* cum, doubl
 }
 
 }  // namespace
+
+// copy out (and optionally reset) the timeline ring; zeros unless built with
+// -DAXB_TRACE_TIMELINE
+int timeline_read(unsigned long long* out, int reset) {
+#ifdef AXB_TRACE_TIMELINE
+    if (out && cudaMemcpyFromSymbol(out, g_axb_tl, sizeof(unsigned long long) * 64 * 8) != cudaSuccess)
+        return 0;
+    if (reset) {
+        static unsigned long long init[64][8];
+        for (int i = 0; i < 64; ++i)
+            for (int j = 0; j < 8; ++j) init[i][j] = (j & 1) ? 0ull : ~0ull;
+        cudaMemcpyToSymbol(g_axb_tl, init, sizeof init);
+    }
+    return 1;
+#else
+    if (out)
+        for (int i = 0; i < 64 * 8; ++i) out[i] = 0ull;
+    (void)reset;
+    return 0;
+#endif
+}
+
 
 // ------------------------------------------------------------------------
 // launchers

@@ -2302,6 +2302,9 @@ int axb_solver_debug_state(axb_solver* s, uint64_t out[8]) {
         for (int i = 0; i < 8; ++i) out[i] = s->hs->dbg[i];
     });
 }
+int axb_debug_timeline(uint64_t out[512], int32_t reset) {
+    return axb_dev::timeline_read(reinterpret_cast<unsigned long long*>(out), reset);
+}
 int axb_debug_dgemm(const double* A, const double* B, const double* Cin, double* D, uint64_t M,
                     uint64_t N, uint64_t K, int32_t b_trans, int32_t reps, double* ms) {
     if (!A || !B || !D || !ms || reps <= 0) return AXB_CONFIG_ERROR;
