@@ -45,9 +45,20 @@ def per_iteration_s(orc, m, p, q, n, steps, seed):
     t0 = time.perf_counter()
     A, B, Xs = instance(m, p, q, n, seed)
     log(f"[{m}x{p}.{q}x{n}] inputs {time.perf_counter() - t0:.1f}s")
-    C = (A @ Xs) @ B
+    # products in row blocks: the host BLAS takes 32-bit dimensions and element
+    # counts (a one-call 65536×65536 result overflows them and crashes)
+    blk = 4096
+    T = A @ Xs
+    C = np.empty((m, n))
+    for i0 in range(0, m, blk):
+        C[i0:i0 + blk] = T[i0:i0 + blk] @ B
+    del T
     log(f"  C {time.perf_counter() - t0:.1f}s")
-    G = A @ A.T
+    G = np.empty((m, m))
+    At = np.ascontiguousarray(A.T)
+    for i0 in range(0, m, blk):
+        G[i0:i0 + blk] = A[i0:i0 + blk] @ At
+    del At
     log(f"  G {time.perf_counter() - t0:.1f}s")
     BtB = B.T @ B
     log(f"  BtB {time.perf_counter() - t0:.1f}s")
