@@ -515,6 +515,7 @@ struct axb_solver {
     std::vector<double> a_sq_h;
     double a_fro_sq = 0.0, b_spec = 0.0, alpha = 0.0, c_fro = 0.0, ref_sq = 0.0;
     bool alpha_outside = false, gram_cached = false;
+    bool chain_xb = false;  // residual product as A·(X·B) instead of (A·X)·B
     uint64_t k = 0;
     bool sel_valid = false;
     Params P{};
@@ -889,7 +890,17 @@ struct axb_solver {
         // one decision for all ranks: forming G gathers A (a collective), and a
         // rank whose free memory differed must not take the other branch
         if (sharded) gram_cached = global_sum(gram_cached ? 1.0 : 0.0) == (double)world;
-        T.alloc(m * q, "T");
+        // association of the residual product (matrix-chain order): the reference
+        // evaluates (A·X)·B, 2mpq + 2mqn FLOP; A·(X·B) costs 2pqn + 2mpn and is
+        // taken when it is at least 5% cheaper (config 5: 3.96e13 vs 4.40e13;
+        // never for a world-8 shard, whose m is m/8).  Same product to rounding.
+        {
+            const double left = (double)m * p * q + (double)m * q * n;
+            const double right = (double)p * q * n + (double)m * p * n;
+            const int e = env_int("AXB_CHAIN_XB", -1);
+            chain_xb = !sp_a && !sp_b && (e >= 0 ? e != 0 : right < 0.95 * left);
+        }
+        T.alloc(std::max(m * q, chain_xb ? p * n : (uint64_t)0), "T");
         const int gparts = gemm_num_ctas((long long)m, (long long)std::max(n, m));
         gemm_sq.alloc(gparts, "gemm parts");
         gemm_diff.alloc(gparts, "gemm parts");
@@ -1251,6 +1262,27 @@ struct axb_solver {
 
     // D = C − (A·X)·B into out (store) with optional Σ D² and Σ (Rold − D)² partials
     void exact_residual_into(double* out, double* sq, const double* rold, bool store) {
+        if (chain_xb) {  // T = X·B (p×n), then C − A·T
+            GemmArgs t1{};
+            t1.M = p; t1.N = n; t1.K = q;
+            t1.A = X.p; t1.lda = q;
+            t1.B = B.p; t1.ldb = n;
+            t1.D = T.p; t1.ldd = n;
+            t1.store = 1;
+            launch_gemm(t1, stream);
+            GemmArgs t2{};
+            t2.M = m; t2.N = n; t2.K = p;
+            t2.A = A.p; t2.lda = p;
+            t2.B = T.p; t2.ldb = n;
+            t2.D = out; t2.ldd = n;
+            t2.Cin = C.p; t2.ldc = n;
+            t2.Rold = rold; t2.ldr = n;
+            t2.sq_part = sq;
+            t2.diff_part = rold ? gemm_diff.p : nullptr;
+            t2.store = store ? 1 : 0;
+            launch_gemm(t2, stream);
+            return;
+        }
         if (sp_a) {  // T = A·X over A's stored entries (matrix.hpp sparse matmul)
             launch_spmm_csr(a_rp.p, a_ci.p, a_v.p, (long long)m, X.p, (long long)q, T.p, stream);
         } else {

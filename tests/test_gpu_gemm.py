@@ -64,3 +64,27 @@ def test_gram_tma_equals_cp_async(axb, shape):
     _, Xg, rowsg, _ = _residual(axb, A, B, C, None, True, cache_gram=0, steps=60)
     assert np.array_equal(rows1, rowsg)
     assert np.linalg.norm(X1 - Xg) <= 1e-12 * np.linalg.norm(Xg)
+
+
+def test_residual_chain_order(axb):
+    """R0 = C − A·X0·B with the product associated as A·(X0·B) (taken when it is
+    ≥ 5% cheaper, e.g. config 5) and as the reference's (A·X0)·B: same product to
+    rounding, both within 1e-13 of numpy."""
+    m, p, q, n = 512, 64, 64, 256  # pn(q+m) = 0.90·mq(p+n): the auto rule picks A·(X·B)
+    rng = np.random.default_rng(99)
+    A, B = rng.standard_normal((m, p)), rng.standard_normal((q, n))
+    X0, C = rng.standard_normal((p, q)), rng.standard_normal((m, n))
+    Rn = C - (A @ X0) @ B
+    out = {}
+    for mode in ("0", "1", None):
+        if mode is None:
+            os.environ.pop("AXB_CHAIN_XB", None)
+        else:
+            os.environ["AXB_CHAIN_XB"] = mode
+        try:
+            out[mode], _, _, _ = _residual(axb, A, B, C, X0, True)
+        finally:
+            os.environ.pop("AXB_CHAIN_XB", None)
+        assert np.linalg.norm(out[mode] - Rn) <= 1e-13 * np.linalg.norm(Rn)
+    assert np.array_equal(out[None], out["1"]), "the auto rule should pick A·(X·B) here"
+    assert np.linalg.norm(out["0"] - out["1"]) <= 1e-14 * np.linalg.norm(Rn)
