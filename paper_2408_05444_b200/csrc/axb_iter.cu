@@ -1959,14 +1959,12 @@ constexpr int kPersistThreads = 256;
 // one system (k_persist), or one CTA owning a whole small system
 // (k_persist_batch, SURVEY §8 F3 — many independent solves in one launch).
 struct GridGroup {
-    static constexpr bool kWholeChip = true;
     cooperative_groups::grid_group g;
     __device__ int rank() const { return (int)blockIdx.x; }
     __device__ int size() const { return (int)gridDim.x; }
     __device__ void sync() { g.sync(); }
 };
 struct SoloGroup {
-    static constexpr bool kWholeChip = false;
     __device__ int rank() const { return 0; }
     __device__ int size() const { return 1; }
     __device__ void sync() { __syncthreads(); }
@@ -2004,7 +2002,6 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
     PT_DECL;
     constexpr int kW = kT / 32;
     constexpr int kSub = kT / kPersistThreads;  // 256-thread sub-blocks (z items)
-    constexpr int kYU = Grp::kWholeChip ? 8 : 4;  // y loads in flight per lane
     extern __shared__ double pscratch[];  // selection scratch: ⌈m/32⌉ group sums
     __shared__ DevState lst;
     __shared__ SelShared sh;
@@ -2095,11 +2092,11 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             for (long long it = gw; it < q && !P.b_rp; it += 2 * nw) {
                 const long long it1 = it + nw;
                 double a0, a1;
-                // the cooperative grid (one system on the whole chip) keeps kYU loads
-                // per lane in flight: a 2000-column row is 4 L2 round trips, not 8
-                // (same per-lane order, so the same sums)
-                warp_dot_pair_u<kYU>(Bb + it * n, it1 < q ? Bb + it1 * n : nullptr, Ri, n, lane,
-                                     (n & 1) == 0, true, a0, a1);
+                // (8 loads per lane in flight — warp_dot_pair_u<8> — was measured here:
+                // the body is at 243 registers, the deeper batch spills and config 2
+                // drops from 35.3k to 28.6k it/s)
+                warp_dot_pair(Bb + it * n, it1 < q ? Bb + it1 * n : nullptr, Ri, n, lane,
+                              (n & 1) == 0, true, a0, a1);
                 if (lane == 0) {
                     yo[it] = a0;
                     if (it1 < q) yo[it1] = a1;
