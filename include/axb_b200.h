@@ -172,11 +172,17 @@ typedef struct {
     const double* values;
 } axb_matrix;
 
-/* solve(const Matrix& A, const Matrix& B, …) dispatch — solver.hpp:518-526.
- * CSR operands are expanded on the device path: every reference loop over stored
- * entries (RowView, gram_mmt, matmul's zero skip) adds exact zeros in the dense
- * form, so results are unchanged, and K2 skips the rows whose Gram coefficient
- * is exactly zero (the sparse-G iteration of solver.hpp:294-295). */
+/* solve(const Matrix& A, const Matrix& B, …) dispatch — solver.hpp:518-526, i.e.
+ * Solver<AMat,BMat> over dense or CSR operands.  CSR operands are validated as
+ * SparseMatrix does (matrix.hpp:94-175: ascending columns, finite non-zero
+ * values) and STAY SPARSE on the device: a CSR A is never expanded — its Gram
+ * G = A·Aᵀ is formed as CSR in the reference's order (matrix.hpp:496-535) and the
+ * iteration walks stored entries only (X over nz(A_i), R over nz(G_i),
+ * solver.hpp:272-273, :294-295); a CSR B is kept as CSR together with Bᵀ for the
+ * y and z passes (:489-492), plus one dense q×n copy for ‖B‖₂ and the residual
+ * GEMM (the reference itself holds the dense n×n BᵀB, :172).  Host arrays only.
+ * Row-sharded handles (opt.nccl_comm) take dense operands: CSR is expanded
+ * there, every stored-entry loop then adding exact zeros. */
 int axb_solver_create_ex(const axb_matrix* A, const axb_matrix* B, const double* C,
                          const double* X0, const axb_config* cfg, const axb_options* opt,
                          axb_solver** out);
