@@ -13,8 +13,9 @@ L2, so no explicit flush is needed between iterations.
 
 N > 1 (torchrun): one process per GPU and ONE system, row-sharded:
 each rank owns m/N rows of A, C, R and a column slice of B; per iteration the
-library issues NCCL collectives inside its CUDA graphs (y allreduce, z allgather,
-record/mass allgathers, owner-row allreduce).  Strong scaling: value = K global
+library issues four NCCL collectives inside its CUDA graphs (y allreduce, z
+allgather, one grouped allgather of the row-norm slices and shard records,
+owner-row allreduce).  Strong scaling: value = K global
 iterations / max-over-ranks device time.  A is generated in 8 fixed row blocks,
 so the global system is bit-identical at N = 1, 2, 4, 8.  --shard forces the
 sharded code path on one GPU (1-rank communicator).

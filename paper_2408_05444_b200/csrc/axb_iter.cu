@@ -1082,7 +1082,7 @@ __device__ void finalize(const Params& P, DevState* st, double s, double mx, lon
     __syncthreads();
     if (P.pack) {
         // sharded: publish this shard's record; the global reduction, the stop
-        // logic and the selection run in k_sel1/k_sel2 after the allgather
+        // logic and the selection run in k_sel1 after the grouped allgather
         if (tid == 0) {
             st->cnt_r = 0u;
             double* rec = P.recs + 4 * P.rank;
@@ -1866,13 +1866,13 @@ __global__ void __launch_bounds__(kThreads) k_sel1(Params P, int mode) {
 
 // Sharded selection, part 3: R_i | A_i | i | coef into pack_send on the owning
 // rank (zeros where this rank packed the previous row), across pack_grid CTAs.
-// The copy had run in k_sel2's single CTA as one dependent load→store chain per
+// The copy had run in the selection kernel's single CTA as one dependent load→store chain per
 // thread: ~80 µs per iteration on the owner at the world-8 shard of config 5.
 __global__ void __launch_bounds__(kThreads) k_pack(Params P) {
     pdl_wait();
     pdl_trigger();
     const DevState* st = P.st;
-    if (st->status != ST_RUN || st->k >= st->k_limit) return;  // k_sel2 did not select
+    if (st->status != ST_RUN || st->k >= st->k_limit) return;  // k_sel1 did not select
     const bool mine = st->packed != 0, was = st->pack_prev != 0;
     if (!mine && !was) return;
     const long long n = P.n, p = P.p;

@@ -1,13 +1,18 @@
 """CPU simulation of the row-sharded iteration (test infrastructure).
 
-Mirrors, step for step, what csrc/axb_iter.cu (k_yg/k_zx/k_r_tma in sharded
-mode, k_sel1, k_sel2) and csrc/axb_solver.cu (enqueue_iteration) do across
-ranks, with torch.distributed (gloo) standing in for NCCL:
+Mirrors, step for step, what csrc/axb_iter.cu (k_yg_tma/k_zx/k_r_tma in sharded
+mode, k_sel1, k_pack) and csrc/axb_solver.cu (enqueue_iteration) do across
+ranks, with torch.distributed (gloo) standing in for NCCL — four exchanges per
+iteration:
 
   pack (owner's R_i | A_i | i | coef) → allreduce      y partial (column slice) → allreduce
-  z slice → allgather                                    local R update, records → allgather
-  global ‖R‖², max/argmax in rank order → GRBK shard masses → allgather
-  rank-ordered prefix, one shared xoshiro draw, owner searches its rows
+  z slice → allgather
+  local R update → ONE grouped allgather: every shard's ‖R_l‖² slice and record
+  then EVERY rank: global ‖R‖², max/argmax in rank order, and the single-GPU
+  selection over the global rows (membership, ordered member-mass prefix, one draw
+  from the identical xoshiro state, upper_bound and the walk back over zero
+  weights, solver.hpp:241-254, rng.hpp:84-99) — all ranks agree with no further
+  exchange; the owner fills the pack.
 
 Used by tests/test_shard_gloo.py (world_size 2) against the oracle.
 """
@@ -65,14 +70,16 @@ class Shard:
     def unit(self):
         return float(self.orc.rng_next_u64(C.byref(self.rng)) >> 11) * 2.0 ** -53
 
-    # -- k_sel1 / k_sel2
+    # -- the grouped norms exchange + k_sel1's commit
     def records(self):
         r_sq = np.einsum("ij,ij->i", self.R, self.R)
-        self.r_sq = r_sq
         ratios = np.where(self.a_sq > 0, r_sq / np.where(self.a_sq > 0, self.a_sq, 1), -np.inf)
         j = int(np.argmax(ratios))  # first max = smallest index
         rec = np.array([float(np.sum(r_sq)), ratios[j], float(self.row0 + j)])
-        recs = self.allgather(rec).reshape(self.world, 3)
+        # one grouped exchange: the ‖R_l‖² slice and the record of every shard
+        both = self.allgather(np.concatenate([r_sq, rec])).reshape(self.world, self.ml + 3)
+        self.r_sq_g = both[:, :self.ml].reshape(-1)
+        recs = both[:, self.ml:]
         s, mx, ax = 0.0, -np.inf, None
         for r in range(self.world):  # rank order, smallest index on ties
             s += recs[r, 0]
@@ -80,6 +87,7 @@ class Shard:
                 mx, ax = recs[r, 1], recs[r, 2]
         self.r_fro, self.max_ratio, self.argmax = s, mx, int(ax)
 
+    # -- k_sel1's selection: every rank, over the GLOBAL rows, identically
     def select(self):
         if self.method == O.MWRBK:
             return self.argmax
@@ -97,31 +105,22 @@ class Shard:
             return lo
         th = self.theta
         zeta = th * (self.max_ratio / self.r_fro) + (1.0 - th) / self.a_fro
-        rows = np.arange(self.ml) + self.row0
-        member = (self.a_sq > 0) & ((rows == self.argmax) |
-                                     (self.r_sq >= zeta * self.a_sq * self.r_fro))
-        mass = np.where(member, self.r_sq, 0.0)
-        masses = self.allgather(np.array([float(np.sum(mass))]))
-        total = float(np.sum(masses))
-        target = self.unit() * total
-        before, owner = 0.0, None
-        for r in range(self.world):
-            if before + masses[r] > target:
-                owner = r
-                break
-            before += masses[r]
-        if owner != self.rank:
-            return None  # only the owner knows the row; the pack carries it
-        cum = before + np.cumsum(mass)
-        hit = np.nonzero(member & (cum > target))[0]
-        return self.row0 + int(hit[0])
+        rows = np.arange(len(self.a_sq_g))
+        member = (self.a_sq_g > 0) & ((rows == self.argmax) |
+                                       (self.r_sq_g >= zeta * self.a_sq_g * self.r_fro))
+        idx = np.nonzero(member)[0]
+        cum = np.cumsum(self.r_sq_g[idx])  # ascending member order (solver.hpp:243-248)
+        target = self.unit() * cum[-1]
+        lo = int(np.searchsorted(cum, target, side="right"))  # upper_bound (rng.hpp:93)
+        if lo >= len(cum):
+            lo = len(cum) - 1
+        while lo > 0 and cum[lo] == cum[lo - 1]:  # walk back over zero weights (:96-97)
+            lo -= 1
+        return int(idx[lo])
 
     def step(self):
-        sel = self.select()
-        if self.method != O.GRBK and self.method != O.RGRBK:
-            owner = sel // self.ml
-        else:
-            owner = self.rank if sel is not None else -1
+        sel = self.select()  # the same row on every rank
+        owner = sel // self.ml
         pack = np.zeros(self.n + self.p + 2)
         if owner == self.rank:
             il = sel - self.row0

@@ -1,6 +1,8 @@
-"""CPU, world_size 2 over gloo: the row-sharded decomposition (records / masses
-allgathers, rank-ordered prefix, shared draw, owner pack allreduce, column-split
-y/z, row-split X) reproduces the single-process oracle's rows and iterates.
+"""CPU, world_size 2 over gloo: the row-sharded decomposition (one grouped
+allgather of the ‖R_l‖² slices and shard records, every rank selecting over the
+global rows with the shared draw, owner pack allreduce, column-split y/z,
+row-split X: four exchanges per iteration) reproduces the single-process
+oracle's rows and iterates.
 Runs here without a GPU; the CUDA path of the same schedule is exercised on a
 1-rank NCCL communicator by tests/test_gpu_parity.py::test_sharded_mode_one_rank."""
 import os
