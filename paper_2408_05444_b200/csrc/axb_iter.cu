@@ -284,6 +284,48 @@ __device__ void warp_dot_pair_u(const double* __restrict__ row0, const double* _
     out1 = two ? warp_sum(acc1) : 0.0;
 }
 
+// CSR A: one 32·kXS-column segment of X_t += f·y with the reference's incremental
+// error term Σ_j (d1² − d0²) (solver.hpp:272-289), all loads of the segment issued
+// before the arithmetic (one L2 round trip per segment).  Per lane the columns
+// ascend, every product and sum is separately rounded.
+constexpr int kXS = 8;
+__device__ __forceinline__ double x_segment_inc(double* __restrict__ xr, const double* __restrict__ rr,
+                                                const double* __restrict__ yb, long long q,
+                                                long long seg, double f, int lane) {
+    const long long k0 = seg * (32 * kXS) + lane;
+    double xv[kXS], yv[kXS], rv[kXS];
+#pragma unroll
+    for (int u = 0; u < kXS; ++u) {
+        const long long k = k0 + 32 * u;
+        if (k < q) {
+            xv[u] = xr[k];
+            yv[u] = __ldcg(yb + k);
+            rv[u] = rr ? rr[k] : 0.0;
+        }
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < kXS; ++u) {
+        const long long k = k0 + 32 * u;
+        if (k < q) {
+            const double x1 = __dadd_rn(xv[u], __dmul_rn(f, yv[u]));
+            xr[k] = x1;
+            if (rr) {
+                const double d0 = __dsub_rn(xv[u], rv[u]), d1 = __dsub_rn(x1, rv[u]);
+                acc += __dsub_rn(__dmul_rn(d1, d1), __dmul_rn(d0, d0));
+            }
+        }
+    }
+    return acc;
+}
+
+// the same behind a call: the latency body sits at the 255-register cap, and
+// inlining the segment's 24 staged loads there spills inside its phases
+__device__ __noinline__ double x_segment_inc_call(double* xr, const double* rr, const double* yb,
+                                                  long long q, long long seg, double f, int lane) {
+    return x_segment_inc(xr, rr, yb, q, seg, f, lane);
+}
+
 // ------------------------------------------------------------------------
 // K4: y = B·R_iᵀ (solver.hpp:270) [+ g = A·A_iᵀ, the Gram column of :294].
 // A CTA computes 8 row dots (one per warp) against the shared vector, which is
@@ -1959,12 +2001,14 @@ constexpr int kPersistThreads = 256;
 // one system (k_persist), or one CTA owning a whole small system
 // (k_persist_batch, SURVEY §8 F3 — many independent solves in one launch).
 struct GridGroup {
+    static constexpr bool kWholeChip = true;  // one system on the cooperative grid
     cooperative_groups::grid_group g;
     __device__ int rank() const { return (int)blockIdx.x; }
     __device__ int size() const { return (int)gridDim.x; }
     __device__ void sync() { g.sync(); }
 };
 struct SoloGroup {
+    static constexpr bool kWholeChip = false;  // one CTA per system (k_persist_batch)
     __device__ int rank() const { return 0; }
     __device__ int size() const { return 1; }
     __device__ void sync() { __syncthreads(); }
@@ -2162,24 +2206,24 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
         if (P.a_rp) {
             // CSR A: X_t += (coef·A_it)·y for t ∈ nz(A_i) only, and the reference's
             // incremental ‖X−X_ref‖² tracker, Σ_j (d1² − d0²) per updated row
-            // (solver.hpp:272-289); a warp per stored entry
+            // (solver.hpp:272-289); a warp per (stored entry, 256-column segment),
+            // so a 15-entry row of a 1024-column X keeps 60 warps busy for one
+            // L2 round trip each instead of 15 warps for 32 dependent ones
             const long long e0 = P.a_rp[sel], e1 = P.a_rp[sel + 1];
-            for (long long e = e0 + gw; e < e1; e += nw) {
+            const long long nseg = (q + 32 * kXS - 1) / (32 * kXS);
+            for (long long it = gw; it < (e1 - e0) * nseg; it += nw) {
+                const long long e = e0 + it / nseg;
                 const long long t = P.a_ci[e];
                 AXB_CHECK(t >= 0 && t < p);
                 const double f = __dmul_rn(coef, P.a_v[e]);
-                double* xr = Xb + t * q;
-                const double* rr = Xrefb ? Xrefb + t * q : nullptr;
-                for (long long k = lane; k < q; k += 32) {
-                    const double x0 = xr[k];
-                    const double x1 = __dadd_rn(x0, __dmul_rn(f, __ldcg(yb + k)));
-                    xr[k] = x1;
-                    if (rr) {
-                        const double rv = rr[k];
-                        const double d0 = __dsub_rn(x0, rv), d1 = __dsub_rn(x1, rv);
-                        xacc += __dsub_rn(__dmul_rn(d1, d1), __dmul_rn(d0, d0));
-                    }
-                }
+                // inlined on the cooperative grid; behind a call in the batched kernel,
+                // which runs at a 128-register cap
+                if constexpr (Grp::kWholeChip)
+                    xacc += x_segment_inc(Xb + t * q, Xrefb ? Xrefb + t * q : nullptr, yb, q,
+                                          it % nseg, f, lane);
+                else
+                    xacc += x_segment_inc_call(Xb + t * q, Xrefb ? Xrefb + t * q : nullptr, yb, q,
+                                               it % nseg, f, lane);
             }
         }
         for (long long t = gw; t < p && !P.a_rp; t += nw) {
@@ -2542,23 +2586,19 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
         double xacc = 0.0;
         if (P.a_rp) {
             // CSR A: rows t ∈ nz(A_i) only, incremental Σ_j (d1² − d0²) per row
-            // (solver.hpp:272-289); the warp's slot holds its delta
+            // (solver.hpp:272-289), a warp per (stored entry, 256-column segment);
+            // the X-owning warps are the last min(p, nw) and each one's slot holds
+            // its delta
             const long long w = nw - 1 - gw;
-            for (long long e = P.a_rp[sel] + w; e < P.a_rp[sel + 1]; e += nw) {
+            const long long nx = min(p, nw);
+            const long long e0 = P.a_rp[sel], e1 = P.a_rp[sel + 1];
+            const long long nseg = (q + 32 * kXS - 1) / (32 * kXS);
+            for (long long it = w; w < nx && it < (e1 - e0) * nseg; it += nx) {
+                const long long e = e0 + it / nseg;
                 const long long t = P.a_ci[e];
                 const double f = __dmul_rn(coef, P.a_v[e]);
-                double* xr = Xb + t * q;
-                const double* rr = Xrefb ? Xrefb + t * q : nullptr;
-                for (long long k = lane; k < q; k += 32) {
-                    const double x0 = xr[k];
-                    const double x1 = __dadd_rn(x0, __dmul_rn(f, __ldcg(yo + k)));
-                    xr[k] = x1;
-                    if (rr) {
-                        const double rv = rr[k];
-                        const double d0 = __dsub_rn(x0, rv), d1 = __dsub_rn(x1, rv);
-                        xacc += __dsub_rn(__dmul_rn(d1, d1), __dmul_rn(d0, d0));
-                    }
-                }
+                xacc += x_segment_inc_call(Xb + t * q, Xrefb ? Xrefb + t * q : nullptr, yo, q,
+                                           it % nseg, f, lane);
             }
             xacc = warp_sum(xacc);
             if (lane == 0 && w < p) xpart[w] = xacc;

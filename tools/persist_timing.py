@@ -12,9 +12,14 @@ orc = O.oracle()
 cases = {"config1": O.generate(orc, 7, 500, 100, 80, 400)[:4]}
 A2, B2, X2, C2 = configs.config2(seed=2); cases["config2"] = (A2, B2, X2, C2)
 cases["tall"] = O.generate(orc, 3, 8192, 64, 32, 96)[:4]
+import scipy.sparse as sp
+A4, B4, X4, C4 = configs.config4_channel(seed=4, nn=1024, half_band=7)
+cases["config4"] = (A4, B4, X4, C4)
+cases["config4csr"] = (sp.csr_matrix(A4), sp.csr_matrix(B4), X4, C4)
 names = ["select", "y", "z1+X", "z2|pick", "R", "finalize", "barriers"]
 methods = {"grbk": axb.Method.grbk(), "mwrbk": axb.Method.mwrbk(), "rbk": axb.Method.rbk()}
-runs = [("config1", mt) for mt in methods] + [("config2", "grbk"), ("tall", "grbk")]
+runs = ([("config1", mt) for mt in methods] + [("config2", "grbk"), ("config2", "mwrbk"), ("tall", "grbk"),
+                                               ("config4", "grbk"), ("config4csr", "grbk")])
 for name, mt in runs:
     A, B, X, Cm = cases[name]
     cfg = axb.SolveConfig(method=methods[mt], stop=axb.StopRule.solution_rrn(0.0, X), seed=42,
