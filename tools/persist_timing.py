@@ -19,11 +19,13 @@ cases["config4csr"] = (sp.csr_matrix(A4), sp.csr_matrix(B4), X4, C4)
 names = ["select", "y", "z1+X", "z2|pick", "R", "finalize", "barriers"]
 methods = {"grbk": axb.Method.grbk(), "mwrbk": axb.Method.mwrbk(), "rbk": axb.Method.rbk()}
 runs = ([("config1", mt) for mt in methods] + [("config2", "grbk"), ("config2", "mwrbk"), ("tall", "grbk"),
-                                               ("config4", "grbk"), ("config4csr", "grbk")])
+                                               ("config4", "grbk"), ("config4csr", "grbk"),
+                                               ("config4:rr", "grbk"), ("config4csr:rr", "grbk")])
 for name, mt in runs:
-    A, B, X, Cm = cases[name]
-    cfg = axb.SolveConfig(method=methods[mt], stop=axb.StopRule.solution_rrn(0.0, X), seed=42,
-                          refresh_interval=0)
+    A, B, X, Cm = cases[name.split(":")[0]]
+    # ":rr" = the bench's fixed-budget stop (residual_rel): no X_ref, so no error tracking
+    stop = axb.StopRule.residual_rel(0.0) if name.endswith(":rr") else axb.StopRule.solution_rrn(0.0, X)
+    cfg = axb.SolveConfig(method=methods[mt], stop=stop, seed=42, refresh_interval=0)
     s = axb.Solver(A, B, Cm, None, cfg, axb.Options(spectral_max_iter=200000))
     s.steps(50); s.steps(2000)
     d = (C.c_uint64 * 8)(); lib.axb_solver_debug_state(s._h, d)
