@@ -909,13 +909,18 @@ def main():
         for c in (1, 2, 3, 4):
             sc = dict(CONFIGS[c])
             k = SUB_STEPS[c]
-            if "channels" in sc:
-                subs[str(c)] = channels_arm(args, sc, ctx, k, args.warmup,
-                                            with_cpu=not args.no_cpu_baseline, cpu_budget_s=10.0)
-            else:
-                subs[str(c)] = system_arm(args, sc, c, ctx, k, args.warmup,
-                                          with_cpu=not args.no_cpu_baseline, cpu_budget_s=10.0,
-                                          with_tol=(c == 1 and not args.no_tol))
+            # a failing side measurement must not take the headline line with it
+            try:
+                if "channels" in sc:
+                    subs[str(c)] = channels_arm(args, sc, ctx, k, args.warmup,
+                                                with_cpu=not args.no_cpu_baseline, cpu_budget_s=10.0)
+                else:
+                    subs[str(c)] = system_arm(args, sc, c, ctx, k, args.warmup,
+                                              with_cpu=not args.no_cpu_baseline, cpu_budget_s=10.0,
+                                              with_tol=(c == 1 and not args.no_tol))
+            except Exception as ex:  # noqa: BLE001
+                log(f"[bench] config {c} failed: {type(ex).__name__}: {ex}")
+                subs[str(c)] = {"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()
         line["configs"] = subs
     if rank == 0:
