@@ -759,11 +759,19 @@ def system_arm(args, cfg, cfg_id, ctx, steps, warmup, sharded=False, comm=0,
     # time-to-tolerance on config 1 (the reference's CPU-runnable case)
     ttt = None
     if rank == 0 and with_tol:
-        ttt = time_to_tol(axb, local)
+        try:
+            ttt = time_to_tol(axb, local)
+        except Exception as ex:  # noqa: BLE001  (a side measurement: keep the line)
+            log(f"[bench] time_to_tol failed: {type(ex).__name__}: {ex}")
+            ttt = {"error": f"{type(ex).__name__}: {ex}"}
 
     cpu = None
     if rank == 0 and with_cpu:
-        cpu = cpu_baseline(cfg, cpu_budget_s)
+        try:
+            cpu = cpu_baseline(cfg, cpu_budget_s)
+        except Exception as ex:  # noqa: BLE001
+            log(f"[bench] cpu_baseline failed: {type(ex).__name__}: {ex}")
+            cpu = {"error": f"{type(ex).__name__}: {ex}"}
     line = {
         "metric": "kaczmarz_iterations_per_sec", "value": round(value, 2), "unit": "iter/s",
         "n_gpus": world, "steps": steps, "warmup": warmup,
