@@ -1,15 +1,18 @@
 """Randomised shape sweep against the oracle (robustness probe): every execution
 path (latency body, general persistent body, graph path with the TMA or the
 register-streaming K2, G cached or not) and every method.
-usage: python tools/fuzz_shapes.py [cases] [seed]"""
+usage: python tools/fuzz_shapes.py [cases] [seed] [only: comma-separated case numbers]
+A case that leaves the oracle's rows is followed by a diagnosis line (tools/fuzz_diag.py)."""
 import sys, time
-sys.path.insert(0, "."); sys.path.insert(0, "tests")
+sys.path.insert(0, "."); sys.path.insert(0, "tests"); sys.path.insert(0, "tools")
 import numpy as np
 import oracle_lib as O
 import paper_2408_05444_b200 as axb
+from fuzz_diag import diagnose
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+only = {int(x) for x in sys.argv[3].split(",")} if len(sys.argv) > 3 else None
 orc = O.oracle()
 meths = [(O.GRBK, None, axb.Method.grbk()), (O.MWRBK, None, axb.Method.mwrbk()),
          (O.RBK, None, axb.Method.rbk()), (O.BK, None, axb.Method.bk()),
@@ -30,7 +33,10 @@ for c in range(cases):
     tag, theta, meth = meths[rng.integers(0, len(meths))]
     gram = int(rng.integers(-1, 2))
     steps = 150
-    A, B, X, Cm = O.generate(orc, int(rng.integers(1, 10 ** 6)), m, p, q, n)
+    gseed = int(rng.integers(1, 10 ** 6))
+    if only is not None and c not in only:
+        continue
+    A, B, X, Cm = O.generate(orc, gseed, m, p, q, n)
     cfg_o = O.make_config(method=tag, theta=theta, seed=7, stop_kind=O.SOLUTION_RRN, tol=0.0,
                           reference=X, refresh_interval=0)
     desc = f"case {c}: {m}x{p}.{q}x{n} {meth} cache_gram={gram}"
@@ -47,6 +53,8 @@ for c in range(cases):
         if not ok:
             bad += 1
         print(f"{'ok ' if ok else 'BAD'} {desc}: first mismatch {mism[:3]}, |dX|/|X| {e:.2e}", flush=True)
+        if mism.size:
+            print("    " + diagnose(orc, A, B, Cm, X, tag, theta, 7, int(mism[0])), flush=True)
     except Exception as ex:  # noqa: BLE001
         bad += 1
         print(f"ERR {desc}: {type(ex).__name__}: {ex}", flush=True)
