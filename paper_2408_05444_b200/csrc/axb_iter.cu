@@ -2579,6 +2579,10 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
     }
     __syncthreads();
 
+    // dense A: X items = (row, 32·kR-column segment); CSR A keeps one slot per X row
+    const long long x_nseg = (q + 32 * kR - 1) / (32 * kR);
+    const long long x_items = p * x_nseg;
+    const long long x_slots = P.a_rp ? min(p, nw) : min(x_items, nw);
     // X_t += (coef·A_it)·y (solver.hpp:272-289), warp per row, rows taken from the
     // LAST warps (the R rows start at the first), so a warp rarely does both;
     // each warp's Σ (X − X_ref)² goes to xpart[gw] (fixed slots, fixed order)
@@ -2590,7 +2594,7 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
             // the X-owning warps are the last min(p, nw) and each one's slot holds
             // its delta
             const long long w = nw - 1 - gw;
-            const long long nx = min(p, nw);
+            const long long nx = x_slots;
             const long long e0 = P.a_rp[sel], e1 = P.a_rp[sel + 1];
             const long long nseg = (q + 32 * kXS - 1) / (32 * kXS);
             for (long long it = w; w < nx && it < (e1 - e0) * nseg; it += nx) {
@@ -2604,12 +2608,24 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
             if (lane == 0 && w < p) xpart[w] = xacc;
             return;
         }
-        for (long long t = nw - 1 - gw; t < p; t += nw) {
-            const double f = __dmul_rn(coef, Ai[t]);
-            if (f == 0.0 && !Xrefb) continue;  // A_it = 0: X_t unchanged (solver.hpp:272-273)
-            double* xr = Xb + t * q;
-            const double* rr = Xrefb ? Xrefb + t * q : nullptr;
-            for (long long k0 = lane; k0 < q; k0 += 32 * kR) {
+        // items = (row t, segment of 32·kR columns), taken by the warps from the last
+        // one down: a long row is spread over several warps, each with ONE batch of
+        // loads (a 1024-column row of X was 8 dependent L2 round trips in one warp),
+        // and the row's A_it values are fetched lane-parallel first, so rows with
+        // A_it = 0 (banded A) cost nothing more
+        const long long w = nw - 1 - gw;
+        for (long long it0 = w; it0 < x_items; it0 += 32 * nw) {
+            const long long itl = it0 + (long long)lane * nw;  // lane j: this warp's j-th item
+            const double fl = itl < x_items ? __dmul_rn(coef, Ai[itl / x_nseg]) : 0.0;
+            for (int j = 0; j < 32; ++j) {
+                const long long it = it0 + (long long)j * nw;
+                if (it >= x_items) break;
+                const double f = __shfl_sync(0xffffffffu, fl, j);
+                if (f == 0.0 && !Xrefb) continue;  // A_it = 0: X_t unchanged (solver.hpp:272-273)
+                const long long t = it / x_nseg;
+                double* xr = Xb + t * q;
+                const double* rr = Xrefb ? Xrefb + t * q : nullptr;
+                const long long k0 = (it % x_nseg) * (32 * kR) + lane;
                 double xv[kR], yv[kR], rv[kR];
 #pragma unroll
                 for (int u = 0; u < kR; ++u) {
@@ -2635,8 +2651,8 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
             }
         }
         xacc = warp_sum(xacc);
-        // slot = the warp's first X row: only the min(p, nw) X-owning warps write
-        if (lane == 0 && nw - 1 - gw < p) xpart[nw - 1 - gw] = xacc;
+        // slot = the warp's first X item: only the x_slots X-owning warps write
+        if (lane == 0 && w < x_slots) xpart[w] = xacc;
     };
 
     long long g_prev = -1;  // CSR A: the Gram row scattered into g last (CTA 0)
@@ -2864,7 +2880,7 @@ __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
                     }
                 }
             }
-            const long long nx = min(p, nw);
+            const long long nx = x_slots;
             for (long long b0 = tid; b0 < nx; b0 += 4 * kT) {
                 double v[4];
 #pragma unroll
