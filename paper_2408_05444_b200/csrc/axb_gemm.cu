@@ -5,15 +5,21 @@
 // at every drift checkpoint (:420, :427-436) and at every exact-metric confirm
 // (:412-419), plus G = A·Aᵀ (gram_mmt, matrix.hpp:481-494) when the Gram
 // columns are cached.  sm_100a has no tcgen05 f64 kind, so the FP64 tensor path
-// is `mma.sync.m8n8k4.f64` (SASS DMMA.8x8x4); operands are staged global→shared
-// with cp.async in a 3-stage ring.
+// is `mma.sync.m8n8k4.f64` (SASS DMMA.8x8x4).
 //
-// CTA tile 64×128×16, 4 warps (2×2), warp tile 32×64 = 4×8 DMMA tiles, two CTAs
-// per SM (≤ 256 registers, 92 KB smem each).  Measured against the 128×128
-// one-CTA-per-SM tile (tools/gemm_variants.cu, config-3 / config-5 shapes):
-// 34.2 / 35.0 vs 31.5 / 32.2 TFLOP/s; cuBLAS DGEMM 35.8 / 36.0.
-// Epilogue fuses the "C −" subtraction, the Σ D² partials (‖R‖²) and the
-// Σ (R_old − D)² partials (the drift guard), so a checkpoint is one pass.
+// Two kernels share one tile — CTA 64×128×16, 4 compute warps (2×2), warp tile
+// 32×64 = 4×8 DMMA tiles, two CTAs per SM — and one fused epilogue (the "C −"
+// subtraction, the Σ D² partials for ‖R‖² and the Σ (R_old − D)² partials of the
+// drift guard, so a checkpoint is one pass):
+//   * k_dgemm_tma (below, the production path): operands arrive as TMA tensor
+//     boxes issued by a fifth, producer warp into a 4-stage mbarrier ring; the C
+//     tile of the epilogue follows the k-tiles through the same ring.
+//     36.3 TFLOP/s at the config-5 shape (cuBLAS DGEMM 35.7, measured DMMA peak
+//     36.99), 34.8–35.0 at the config-3 shapes (cuBLAS 33.5–35.0).
+//   * k_dgemm (round 1; operands whose rows are not 16-byte aligned): cp.async
+//     into a 3-stage ring of padded tiles, 33.4 / 31.3–31.5 TFLOP/s.
+// Every output element accumulates over k in the same order in both, so they
+// agree bitwise (tests/test_gpu_gemm.py).
 #include <cuda.h>  // CUtensorMap (types only: the encoder is fetched through cudart)
 
 #include <cmath>
