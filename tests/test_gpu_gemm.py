@@ -88,3 +88,29 @@ def test_residual_chain_order(axb):
         assert np.linalg.norm(out[mode] - Rn) <= 1e-13 * np.linalg.norm(Rn)
     assert np.array_equal(out[None], out["1"]), "the auto rule should pick A·(X·B) here"
     assert np.linalg.norm(out["0"] - out["1"]) <= 1e-14 * np.linalg.norm(Rn)
+
+
+@pytest.mark.parametrize("b_trans", [0, 1])
+def test_debug_dgemm_export(axb, b_trans):
+    """axb_debug_dgemm (K1 timed alone, device pointers): D = C − A·B and D = A·Bᵀ."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2408_05444_b200 import _lib
+
+    lib = _lib.load()
+    M, N, K = 200, 144, 96
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(M, K, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn((N, K) if b_trans else (K, N), dtype=torch.float64, device="cuda", generator=g)
+    Cm = torch.randn(M, N, dtype=torch.float64, device="cuda", generator=g)
+    D = torch.empty_like(Cm)
+    ms = C.c_double()
+    torch.cuda.synchronize()
+    rc = lib.axb_debug_dgemm(A.data_ptr(), B.data_ptr(), None if b_trans else Cm.data_ptr(), D.data_ptr(),
+                             M, N, K, b_trans, 2, C.byref(ms))
+    assert rc == 0 and ms.value > 0.0
+    ref = A @ B.T if b_trans else Cm - A @ B
+    assert (D - ref).norm().item() <= 1e-13 * ref.norm().item()
+    assert lib.axb_debug_timeline(None, 0) in (0, 1)  # 1 only in a -DAXB_TRACE_TIMELINE build
