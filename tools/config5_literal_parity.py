@@ -14,7 +14,7 @@ B 8192×32768 N(0,1/32768), X* N(0,1), C = A·X*·B, X0 = 0, ME-GRBK.
 Prints one JSON line: the selected rows of both, the first mismatch, X and ‖R_l‖²
 relative differences.  Needs ~95 GB of host RAM and ~8 minutes.
 
-    python tools/config5_literal_parity.py [--steps 24]
+    python tools/config5_literal_parity.py [--steps 24] [--method grbk|mwrbk|rgrbk025|rgrbk075]
 """
 import argparse
 import json
@@ -41,6 +41,7 @@ def main():
     faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--method", default="grbk", choices=["grbk", "mwrbk", "rgrbk025", "rgrbk075"])
     ap.add_argument("--scale", type=int, default=1, help="divide every dimension (smoke test of the tool)")
     args = ap.parse_args()
     d = args.scale
@@ -60,7 +61,10 @@ def main():
     del T
     log(f"inputs and C {time.perf_counter() - t0:.0f}s")
 
-    cfg = axb.SolveConfig(method=axb.Method.grbk(), stop=axb.StopRule.solution_rrn(0.0, Xs), seed=42,
+    meth, tag, theta = {"grbk": (axb.Method.grbk(), O.GRBK, None), "mwrbk": (axb.Method.mwrbk(), O.MWRBK, None),
+                        "rgrbk025": (axb.Method.rgrbk(0.25), O.RGRBK, 0.25),
+                        "rgrbk075": (axb.Method.rgrbk(0.75), O.RGRBK, 0.75)}[args.method]
+    cfg = axb.SolveConfig(method=meth, stop=axb.StopRule.solution_rrn(0.0, Xs), seed=42,
                           refresh_interval=0, max_iter=10 ** 9)
     s = axb.Solver(A, B, C, None, cfg, axb.Options(spectral_max_iter=200000, cache_gram=1))
     alpha = s.alpha()
@@ -79,7 +83,7 @@ def main():
     BtB = B.T @ B
     log(f"G, BtB {time.perf_counter() - t0:.0f}s")
     orc = O.oracle()
-    cfg_o = O.make_config(method=O.GRBK, stop_kind=O.SOLUTION_RRN, tol=0.0, reference=Xs, seed=42,
+    cfg_o = O.make_config(method=tag, theta=theta, stop_kind=O.SOLUTION_RRN, tol=0.0, reference=Xs, seed=42,
                           refresh_interval=0, max_iter=10 ** 9)
     so = O.PreparedSolver(orc, A, B, C, np.zeros((p, q)), C, G, BtB, alpha, cfg_o)
     t1 = time.perf_counter()
@@ -92,7 +96,7 @@ def main():
     rows_g = np.asarray(rows_g, dtype=np.int64)
     rows_c = np.asarray(rows_c, dtype=np.int64)
     mism = np.nonzero(rows_g != rows_c)[0]
-    out = {"tool": "config5_literal_parity", "instance": f"{m}x{p}.{q}x{n}", "method": "GRBK", "steps": args.steps,
+    out = {"tool": "config5_literal_parity", "instance": f"{m}x{p}.{q}x{n}", "method": args.method, "steps": args.steps,
            "alpha": alpha, "rows_device": rows_g.tolist(), "rows_oracle": rows_c.tolist(),
            "index_mismatches": int(mism.size), "first_mismatch": int(mism[0]) if mism.size else None,
            "X_rel_diff": float(np.linalg.norm(Xg - Xc) / max(np.linalg.norm(Xc), 1e-300)),
