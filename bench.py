@@ -286,6 +286,12 @@ def channels_arm(args, cfg, ctx, steps, warmup, with_cpu=True, cpu_budget_s=15.0
     rank, world, local = ctx.rank, ctx.world, ctx.local
     mine = [c for c in range(cfg["channels"]) if c % world == rank]
     data = {c: make_channel(cfg, 4, c) for c in mine}
+    if getattr(args, "csr", False):
+        # the blur operators as CSR (the reference's own restoration passes SparseMatrix
+        # operands, imaging.hpp:183-196): they stay sparse on the device (DESIGN §7 F1)
+        import scipy.sparse as sp
+
+        data = {c: (sp.csr_matrix(d[0]), sp.csr_matrix(d[1]), d[2], d[3]) for c, d in data.items()}
     mk = lambda: axb.SolveConfig(method=axb.Method.grbk(), stop=axb.StopRule.residual_rel(0.0),  # noqa: E731
                                  max_iter=10 ** 9, seed=42, refresh_interval=1000)
     # ‖B‖₂ on the device: the blur's top singular gap is tiny (the reference's own
@@ -357,7 +363,8 @@ def channels_arm(args, cfg, ctx, steps, warmup, with_cpu=True, cpu_budget_s=15.0
         outs = [h.X() for h in hs]
         torch.cuda.synchronize(local)
         e2e_s = ctx.allmax(time.perf_counter() - t0)
-        h2d = sum(d[0].nbytes + d[1].nbytes + d[2].nbytes for d in data.values())
+        nb = lambda a: a.nbytes if hasattr(a, "nbytes") else a.data.nbytes + a.indices.nbytes + a.indptr.nbytes  # noqa: E731
+        h2d = sum(nb(d[0]) + nb(d[1]) + d[2].nbytes for d in data.values())
         d2h = sum(o.nbytes for o in outs)
         e2e = {"value": units / e2e_s, "unit": "iter/s",
                "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
@@ -376,6 +383,7 @@ def channels_arm(args, cfg, ctx, steps, warmup, with_cpu=True, cpu_budget_s=15.0
         "data": "synthetic (numpy seeded blur operator, smooth field, Gaussian noise)",
         "config": {"workload": cfg["desc"], "m": nn, "p": nn, "q": nn, "n": nn,
                    "channels": cfg["channels"], "method": "grbk", "refresh_interval": 1000,
+                   "operands": "CSR" if getattr(args, "csr", False) else "dense",
                    "parallelism": f"channel c on GPU c mod {world} (independent solves, no collective; "
                                   f"a GPU's channels run concurrently on equal SM shares)",
                    "l2": "per-channel working set (40 MB) is L2-resident: latency-bound"},
@@ -856,6 +864,8 @@ def main():
     ap.add_argument("--shard", action="store_true",
                     help="use the row-sharded path even on one GPU (1-rank NCCL communicator)")
     ap.add_argument("--watchdog-s", type=float, default=1500.0)
+    ap.add_argument("--csr", action="store_true",
+                    help="config 4: pass the blur operators as CSR (default: dense arrays)")
     ap.add_argument("--half-band", type=int, default=None,
                     help="config 4: blur half-band (default 7; BASELINE's 'bandwidth 15' read "
                          "as half-band 7, half-band 15 the other reading, SURVEY §8 D4)")
