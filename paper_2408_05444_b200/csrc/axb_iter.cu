@@ -2539,8 +2539,20 @@ template <class Grp, int kT>
 __device__ __forceinline__ void persist_body_lat(const Params& P, Grp grid) {
     PT_DECL;
     constexpr int kW = kT / 32;
-    constexpr int kU = kT <= 256 ? 8 : 4;  // loads in flight per lane (register budget)
-    constexpr int kR = 4;  // R-row pairs: 3 streams per lane
+    // loads in flight per lane in the dots (kU) and the row updates (kR; R-row pairs
+    // are 3 streams per lane).  The body sits at the 255-register cap, and the spills
+    // cost more than deeper batches gain: kU 8 → 4 took the spill stores from 424
+    // to 128 bytes and config 1 from 13.7 to 12.5 µs per iteration, a config-4
+    // channel from 20.3 to 18.1 µs (tools/sweep_lat_batch.sh; 5 and 6 are worse
+    // than both, kR 2, 3 and 6 worse than 4).  -DAXB_LAT_KU / -DAXB_LAT_KR override.
+#ifndef AXB_LAT_KU
+#define AXB_LAT_KU 4
+#endif
+#ifndef AXB_LAT_KR
+#define AXB_LAT_KR 4
+#endif
+    constexpr int kU = kT <= 256 ? AXB_LAT_KU : 4;
+    constexpr int kR = AXB_LAT_KR;
     extern __shared__ __align__(16) double psm[];
     __shared__ DevState lst;
     __shared__ SelShared sh;
