@@ -326,6 +326,42 @@ __device__ __noinline__ double x_segment_inc_call(double* xr, const double* rr, 
     return x_segment_inc(xr, rr, yb, q, seg, f, lane);
 }
 
+// one row dot with kU vector loads per lane issued before the FMAs (the single-row
+// form of warp_dot_pair_u: same per-lane order, two thirds of its registers)
+template <int kU>
+__device__ __forceinline__ double warp_dot_u(const double* __restrict__ row, const double* __restrict__ v,
+                                             long long len, int lane, bool vec2, bool coherent_v) {
+    double acc = 0.0;
+    if (vec2) {
+        const double2* r0 = reinterpret_cast<const double2*>(row);
+        const double2* v2 = reinterpret_cast<const double2*>(v);
+        const long long h = len >> 1;
+        for (long long k0 = lane; k0 < h; k0 += 32 * kU) {
+            double2 a[kU], b[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const long long k = k0 + 32 * u;
+                if (k < h) {
+                    b[u] = coherent_v ? __ldcg(v2 + k) : __ldg(v2 + k);
+                    a[u] = __ldg(r0 + k);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const long long k = k0 + 32 * u;
+                if (k < h) {
+                    acc += a[u].x * b[u].x;
+                    acc += a[u].y * b[u].y;
+                }
+            }
+        }
+    } else {
+        for (long long k = lane; k < len; k += 32)
+            acc += __ldg(row + k) * (coherent_v ? __ldcg(v + k) : __ldg(v + k));
+    }
+    return warp_sum(acc);
+}
+
 // ------------------------------------------------------------------------
 // K4: y = B·R_iᵀ (solver.hpp:270) [+ g = A·A_iᵀ, the Gram column of :294].
 // A CTA computes 8 row dots (one per warp) against the shared vector, which is
@@ -2133,12 +2169,19 @@ __device__ __forceinline__ void persist_body(const Params& P, Grp grid) {
             double* const go = P.g;
             const double* const Bb = P.B;
             const double* const Ab = P.A;
+            if (Grp::kWholeChip && q <= nw && !P.b_rp) {
+                // fewer rows than warps (config 2: 400 rows, 1184 warps): one row per
+                // warp, 6 loads per lane in flight — a 2000-column row is 6 L2 round
+                // trips instead of 8.  (8 in flight, or the pair form, spill: the body is
+                // at 243 registers, and config 2 dropped from 35.3k to 28.6k it/s.)
+                if (gw < q) {
+                    const double a0 = warp_dot_u<6>(Bb + gw * n, Ri, n, lane, (n & 1) == 0, true);
+                    if (lane == 0) yo[gw] = a0;
+                }
+            } else
             for (long long it = gw; it < q && !P.b_rp; it += 2 * nw) {
                 const long long it1 = it + nw;
                 double a0, a1;
-                // (8 loads per lane in flight — warp_dot_pair_u<8> — was measured here:
-                // the body is at 243 registers, the deeper batch spills and config 2
-                // drops from 35.3k to 28.6k it/s)
                 warp_dot_pair(Bb + it * n, it1 < q ? Bb + it1 * n : nullptr, Ri, n, lane,
                               (n & 1) == 0, true, a0, a1);
                 if (lane == 0) {
